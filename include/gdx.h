@@ -1,0 +1,164 @@
+/*
+ * gdx.h -- C ABI of the B200 graph-analytics backend (libgdx.so).
+ *
+ * Drop-in for the execution of the four corpus entry points of the reference
+ * (arxiv/paper_2401_02472, /root/reference/proj):
+ *
+ *   reference interface                                   replaced by
+ *   ----------------------------------------------------  -----------------------------
+ *   CsrGraph spans (core/include/graphdsl/csr.hpp:39-44)  gdx_graph_create (gdx_csr_view)
+ *   CsrGraph::buildFromEdges (core/src/csr.cpp:28-94)     gdx_graph_build_from_edges
+ *   ComputeSSSP via interp::run (corpus/sssp.sp:6-20,     gdx_sssp
+ *     interpreter.hpp:87-88); golden computesssp
+ *     (tests/golden/sssp/cuda/sssp_cuda.cu:136)
+ *   ComputePR  (corpus/pr.sp:5-33); computepr             gdx_pagerank
+ *     (tests/golden/pr/cuda/pr_cuda.cu:150)
+ *   ComputeTC  (corpus/tc.sp:6-18); computetc             gdx_tc
+ *     (tests/golden/tc/cuda/tc_cuda.cu:144)
+ *   ComputeBC  (corpus/bc.sp:6-25); computebc             gdx_bc
+ *     (tests/golden/bc/cuda/bc_cuda.cu:149)
+ *   CompileError kinds (diagnostics.hpp:31-57)            gdx_status + gdx_last_error()
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross this boundary.  Every
+ *    function returns a gdx_status; on failure gdx_last_error() (thread-local)
+ *    holds "<Kind>: <message>" where Kind mirrors the reference's CompileError
+ *    kinds (RuntimeError, NonTermination, InvalidEdge, ...).
+ *  - Output pointers may be host memory (pageable or pinned) or device memory
+ *    on the graph's device (unified addressing decides; cudaMemcpyDefault).
+ *  - A graph handle owns its device memory and one CUDA stream; it must be used
+ *    by one host thread at a time.  Distinct handles may run concurrently.
+ *  - Results are bit-exact with the reference for SSSP distances and triangle
+ *    counts and within 1e-6 relative for PageRank and BC.
+ */
+#ifndef GDX_H
+#define GDX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDX_ABI_VERSION 1
+
+typedef enum {
+    GDX_OK = 0,
+    GDX_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument / InvalidEdge / NegativeWeight */
+    GDX_ERR_OUT_OF_RANGE = 2,     /* node id out of range (RuntimeError in interp::run) */
+    GDX_ERR_RUNTIME = 3,          /* other RuntimeError (e.g. division by zero) */
+    GDX_ERR_NON_TERMINATION = 4,  /* fixedPoint cap exceeded (interpreter.cpp:977-986) */
+    GDX_ERR_CUDA = 5,
+    GDX_ERR_OUT_OF_MEMORY = 6,
+    GDX_ERR_UNSUPPORTED = 7,
+    GDX_ERR_NCCL = 8
+} gdx_status;
+
+typedef struct gdx_graph gdx_graph;
+
+/* Exactly the reference's GraphCsr (sssp_cuda.cu:8-17) plus `directed`.
+ * weights may be NULL (all 1).  rev_* may be NULL: the reverse CSR is then
+ * rebuilt on the device with csr.cpp:77-94 semantics.  dests may be NULL only
+ * when rev_offsets/rev_srcs are given (PageRank-only graphs). */
+typedef struct {
+    int32_t n;
+    int32_t m;
+    int32_t directed;
+    const int32_t* offsets;     /* n+1 */
+    const int32_t* dests;       /* m   */
+    const int32_t* weights;     /* m   */
+    const int32_t* rev_offsets; /* n+1 */
+    const int32_t* rev_srcs;    /* m   */
+    const int32_t* rev_eid;     /* m   */
+} gdx_csr_view;
+
+/* Per-call statistics (algorithmic work, used for GTEPS / roofline). */
+typedef struct {
+    int32_t rounds;           /* fixedPoint rounds / BFS levels / tiles */
+    int32_t launches;         /* kernels launched by the call */
+    int64_t vertices_visited; /* SSSP: sum of frontier sizes; BC: reached (s,v) pairs */
+    int64_t edges_visited;    /* edges scanned */
+    int64_t updates;          /* SSSP successful relaxations; BC DAG edges */
+    double algorithmic_bytes; /* SURVEY.md 8(d) formula for this call */
+} gdx_stats;
+
+const char* gdx_last_error(void);
+int gdx_abi_version(void);
+int gdx_device_count(int* count);
+
+/* ---- graph lifetime ------------------------------------------------------ */
+int gdx_graph_create(const gdx_csr_view* view, int device, gdx_graph** out);
+int gdx_graph_destroy(gdx_graph* g);
+int gdx_graph_info(const gdx_graph* g, int32_t* n, int32_t* m, int32_t* directed);
+/* Copies the device CSR back; any pointer may be NULL to skip that array. */
+int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* weights,
+                       int32_t* rev_offsets, int32_t* rev_srcs, int32_t* rev_eid);
+/* The CUDA stream (cudaStream_t) all kernels of this handle run on.  Setting
+ * it to a caller stream (e.g. torch.cuda.current_stream()) orders the calls
+ * with the caller's work; NULL restores the handle's own stream. */
+int gdx_graph_set_stream(gdx_graph* g, void* stream);
+int gdx_graph_get_stream(gdx_graph* g, void** stream);
+
+/* ---- device graph construction (csr.cpp:28-94 on the GPU) ----------------
+ * u/v/w are host or device arrays of nedges input edges (w may be NULL).
+ * Semantics are exactly CsrGraph::buildFromEdges: validation errors
+ * (InvalidEdge / NegativeWeight), undirected doubling with self loops stored
+ * once, sort by (u,v), duplicates keep the minimum weight, stable reverse CSR. */
+int gdx_graph_build_from_edges(int32_t n, int64_t nedges, const int32_t* u, const int32_t* v,
+                               const int32_t* w, int directed, int device, gdx_graph** out);
+
+/* Counter-based synthetic generators on the GPU.
+ * kind: 0 = RMAT (a,b,c; d = 1-a-b-c), 1 = uniform, 2 = 2-D grid (side x side,
+ * each lattice edge kept with probability keep).  The edge list is built into
+ * a CSR with buildFromEdges semantics.  Weights (if whi >= wlo >= 0) are
+ * counter-hashed per unordered pair (symmetric on undirected graphs). */
+typedef struct {
+    int32_t kind;
+    int32_t nodes;    /* RMAT/uniform: vertex count; grid: side */
+    int64_t edges;    /* RMAT/uniform: edges drawn (before dedup) */
+    uint64_t seed;
+    double a, b, c;   /* RMAT */
+    double keep;      /* grid */
+    int32_t directed;
+    int32_t wlo, whi; /* weights; whi < wlo => unweighted (all 1) */
+} gdx_gen_params;
+int gdx_graph_generate(const gdx_gen_params* p, int device, gdx_graph** out);
+/* Counter-hash weights in [lo, hi] (symmetric for undirected graphs). */
+int gdx_graph_set_hash_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t seed);
+
+/* ---- the four entry points -------------------------------------------------
+ * ComputeSSSP: dist_out[n] int64, unreachable = INT64_MAX/2 (oracles.hpp:12).
+ * The corpus postconditions hold on return: `modified` is all false and
+ * `finished` is true (test_interpreter.cpp:34-44). */
+int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats);
+
+/* ComputePR: rank_out[n] f64; *rounds_out = fixedPoint rounds executed
+ * (== the interpreter's final `iter`), at most max_iter+1 (pr.sp:25). */
+int gdx_pagerank(gdx_graph* g, double damping, double threshold, int32_t max_iter,
+                 double* rank_out, int32_t* rounds_out, gdx_stats* stats);
+
+/* ComputeTC: the tc.sp count (== its return value). */
+int gdx_tc(gdx_graph* g, int64_t* count_out, gdx_stats* stats);
+/* Same count restricted to middle vertices v in [v_begin, v_end) (sharding). */
+int gdx_tc_range(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_out,
+                 gdx_stats* stats);
+
+/* ComputeBC: bc_out[n] f64, unnormalised, sources excluded, accumulated in
+ * source-set order semantics (bc.sp:6-25). */
+int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out, gdx_stats* stats);
+
+/* ---- measurement ------------------------------------------------------------
+ * When enabled, the library brackets every kernel launch of this handle with
+ * CUDA events on the launching stream.  gdx_profile_read reports, per kernel
+ * name, the summed device time (ms) and launch count since the last reset. */
+int gdx_profile_enable(gdx_graph* g, int enable);
+int gdx_profile_reset(gdx_graph* g);
+/* Writes up to cap entries; *count = number of distinct kernels. */
+int gdx_profile_read(gdx_graph* g, char* names /* cap*64 bytes */, double* ms, int64_t* launches,
+                     int32_t cap, int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDX_H */

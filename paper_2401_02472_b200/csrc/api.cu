@@ -1,0 +1,262 @@
+// api.cu -- C-ABI plumbing: error reporting, graph handle lifetime, upload,
+// download, streams and per-kernel profiling.  Algorithm entry points live in
+// sssp.cu / pagerank.cu / tc.cu / bc.cu; construction in build.cu.
+#include <cstring>
+
+#include "gdx_internal.cuh"
+#include "plans.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+gdx_graph::~gdx_graph() {
+    // Plans hold device buffers; release them before the stream goes away.
+    pr.reset();
+    sssp.reset();
+    tc.reset();
+    bc.reset();
+    if (pinned) cudaFreeHost(pinned);
+    if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+namespace gdx {
+
+int guard_impl(const std::function<void()>& f) {
+    try {
+        f();
+        return GDX_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "OutOfMemory: host allocation failed";
+        return GDX_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("RuntimeError: ") + e.what();
+        return GDX_ERR_RUNTIME;
+    }
+}
+
+static void new_handle(gdx_graph* g, int device) {
+    int ndev = 0;
+    GDX_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: device " + std::to_string(device) +
+                                           " out of range [0, " + std::to_string(ndev) + ")");
+    g->device = device;
+    GDX_CUDA(cudaSetDevice(device));
+    GDX_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+    GDX_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+    g->stream = g->own_stream;
+    GDX_CUDA(cudaMallocHost(&g->pinned, 4096));
+}
+
+gdx_graph* make_graph(int device) {
+    auto* g = new gdx_graph;
+    try {
+        new_handle(g, device);
+    } catch (...) {
+        delete g;
+        throw;
+    }
+    return g;
+}
+
+__global__ void k_max_weight(const int32_t* __restrict__ w, int64_t m, int32_t* out,
+                             int32_t* neg) {
+    int32_t local = 0;
+    int32_t bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = w[i];
+        local = max(local, x);
+        bad |= x < 0;
+    }
+    for (int o = 16; o; o >>= 1) {
+        local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, local);
+        if (bad) atomicOr(neg, 1);
+    }
+}
+
+// Computes max_weight (SSSP chooses 32- or 64-bit distances from it) and
+// rejects negative weights (csr.cpp:36-39 NegativeWeight).
+void finalize_graph(gdx_graph* g) {
+    g->max_weight = 1;
+    if (g->weighted && g->m > 0) {
+        DevBuf<int32_t> tmp(2);
+        GDX_CUDA(cudaMemsetAsync(tmp.get(), 0, 2 * sizeof(int32_t), g->stream));
+        k_max_weight<<<blocks_for(g->m, 256, g->num_sms * 8), 256, 0, g->stream>>>(
+            g->weights.get(), g->m, tmp.get(), tmp.get() + 1);
+        GDX_LAUNCH_CHECK();
+        int32_t h[2];
+        GDX_CUDA(cudaMemcpyAsync(h, tmp.get(), sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        if (h[1]) fail(GDX_ERR_INVALID_ARGUMENT, "NegativeWeight: graph has a negative weight");
+        g->max_weight = h[0];
+    }
+}
+
+}  // namespace gdx
+
+using namespace gdx;
+
+extern "C" {
+
+const char* gdx_last_error(void) { return g_last_error.c_str(); }
+int gdx_abi_version(void) { return GDX_ABI_VERSION; }
+
+int gdx_device_count(int* count) {
+    return guard_impl([&] { GDX_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int gdx_graph_create(const gdx_csr_view* v, int device, gdx_graph** out) {
+    return guard_impl([&] {
+        if (!v || !out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null view/out");
+        if (v->n < 0 || v->m < 0) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: negative size");
+        if (!v->offsets) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: offsets required");
+        bool has_rev = v->rev_offsets && v->rev_srcs;
+        if (!v->dests && !has_rev)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: dests or rev_offsets/rev_srcs required");
+        std::unique_ptr<gdx_graph> g(make_graph(device));
+        DeviceGuard dg(device);
+        g->n = v->n;
+        g->m = v->m;
+        g->directed = v->directed != 0;
+        g->weighted = v->weights != nullptr;
+        cudaStream_t s = g->stream;
+        const size_t nb = (size_t(v->n) + 1) * sizeof(int32_t), mb = size_t(v->m) * sizeof(int32_t);
+        g->offsets.alloc(size_t(v->n) + 1);
+        GDX_CUDA(cudaMemcpyAsync(g->offsets.get(), v->offsets, nb, cudaMemcpyDefault, s));
+        if (v->dests) {
+            g->dests.alloc(v->m);
+            GDX_CUDA(cudaMemcpyAsync(g->dests.get(), v->dests, mb, cudaMemcpyDefault, s));
+        }
+        if (v->weights) {
+            g->weights.alloc(v->m);
+            GDX_CUDA(cudaMemcpyAsync(g->weights.get(), v->weights, mb, cudaMemcpyDefault, s));
+        }
+        if (has_rev) {
+            g->rev_offsets.alloc(size_t(v->n) + 1);
+            g->rev_srcs.alloc(v->m);
+            GDX_CUDA(cudaMemcpyAsync(g->rev_offsets.get(), v->rev_offsets, nb, cudaMemcpyDefault, s));
+            GDX_CUDA(cudaMemcpyAsync(g->rev_srcs.get(), v->rev_srcs, mb, cudaMemcpyDefault, s));
+            if (v->rev_eid) {
+                g->rev_eid.alloc(v->m);
+                GDX_CUDA(cudaMemcpyAsync(g->rev_eid.get(), v->rev_eid, mb, cudaMemcpyDefault, s));
+            }
+        } else {
+            build_reverse_device(g.get());
+        }
+        finalize_graph(g.get());
+        GDX_CUDA(cudaStreamSynchronize(s));
+        *out = g.release();
+    });
+}
+
+int gdx_graph_destroy(gdx_graph* g) {
+    return guard_impl([&] {
+        if (!g) return;
+        DeviceGuard dg(g->device);
+        cudaStreamSynchronize(g->stream);
+        delete g;
+    });
+}
+
+int gdx_graph_info(const gdx_graph* g, int32_t* n, int32_t* m, int32_t* directed) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        if (n) *n = g->n;
+        if (m) *m = g->m;
+        if (directed) *directed = g->directed;
+    });
+}
+
+int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* weights,
+                       int32_t* rev_offsets, int32_t* rev_srcs, int32_t* rev_eid) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        DeviceGuard dg(g->device);
+        const size_t nb = (size_t(g->n) + 1) * 4, mb = size_t(g->m) * 4;
+        auto need = [&](void* dst, const DevBuf<int32_t>& b, size_t bytes, const char* what) {
+            if (!dst) return;
+            if (!b.get() && bytes)
+                fail(GDX_ERR_UNSUPPORTED, std::string("Unsupported: graph has no ") + what);
+            copy_out(g, dst, b.get(), bytes);
+        };
+        need(offsets, g->offsets, nb, "offsets");
+        need(dests, g->dests, mb, "dests");
+        if (weights) {
+            if (g->weighted)
+                copy_out(g, weights, g->weights.get(), mb);
+            else {
+                GDX_CUDA(cudaStreamSynchronize(g->stream));
+                for (int32_t i = 0; i < g->m; ++i) weights[i] = 1;
+            }
+        }
+        need(rev_offsets, g->rev_offsets, nb, "rev_offsets");
+        need(rev_srcs, g->rev_srcs, mb, "rev_srcs");
+        need(rev_eid, g->rev_eid, mb, "rev_eid");
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+    });
+}
+
+int gdx_graph_set_stream(gdx_graph* g, void* stream) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        DeviceGuard dg(g->device);
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        g->stream = stream ? static_cast<cudaStream_t>(stream) : g->own_stream;
+    });
+}
+
+int gdx_graph_get_stream(gdx_graph* g, void** stream) {
+    return guard_impl([&] {
+        if (!g || !stream) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        *stream = g->stream;
+    });
+}
+
+int gdx_profile_enable(gdx_graph* g, int enable) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        g->prof.enabled = enable != 0;
+    });
+}
+
+int gdx_profile_reset(gdx_graph* g) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        DeviceGuard dg(g->device);
+        g->prof.drain();
+        g->prof.totals.clear();
+    });
+}
+
+int gdx_profile_read(gdx_graph* g, char* names, double* ms, int64_t* launches, int32_t cap,
+                     int32_t* count) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        DeviceGuard dg(g->device);
+        g->prof.drain();
+        int32_t i = 0;
+        for (auto& kv : g->prof.totals) {
+            if (i < cap) {
+                if (names) {
+                    std::strncpy(names + 64 * i, kv.first.c_str(), 63);
+                    names[64 * i + 63] = 0;
+                }
+                if (ms) ms[i] = kv.second.first;
+                if (launches) launches[i] = kv.second.second;
+            }
+            ++i;
+        }
+        if (count) *count = i;
+    });
+}
+
+}  // extern "C"

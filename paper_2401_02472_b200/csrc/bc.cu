@@ -1,0 +1,328 @@
+// bc.cu -- ComputeBC (reference corpus/bc.sp:6-25) on sm_100a.
+//
+// The reference runs one source at a time; every BFS level is a full-V
+// topology-driven launch plus a host round trip, then a second full-V launch
+// per level for the reverse pass (tests/golden/bc/cuda/bc_cuda.cu:117-219;
+// interpreter.cpp:1002-1087).
+//
+// Here a batch of S sources is processed together, level-synchronously, in
+// two persistent cooperative kernels (forward / backward) with one grid.sync
+// per level:
+//   * all (source, vertex) pairs discovered at level L form one contiguous
+//     segment of a device log, so each level is a dense work list for every
+//     source at once and the reverse pass replays the segments backwards;
+//   * forward (iterateInBFS): a level-L item pulls sigma from its level L-1
+//     parents (no atomics on sigma) and claims undiscovered neighbours with
+//     atomicCAS on level; claims are staged in shared memory and appended
+//     with one atomicAdd per block;
+//   * backward (iterateInReverse): delta(v) = sum over DAG children w in
+//     ascending id order of (sigma(v)/sigma(w)) * (1 + delta(w)) -- the exact
+//     expression and order of bc.sp:19-21 / oracles.cpp:60-67 -- then
+//     bc[v] += delta(v) for v != source;
+//   * sigma is carried as (mantissa, exponent) so path counts never overflow
+//     (the reference's double sigma overflows on large grids).
+//     Where the reference's sigma is finite the quotients are identical.
+#include <cooperative_groups.h>
+
+#include "gdx_internal.cuh"
+#include "plans.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gdx {
+
+constexpr int kBcBlock = 256;
+constexpr int kBcQueue = 4 * kBcBlock;
+
+enum { kTail = 0, kLevels = 1, kReached = 2, kFwdScan = 3, kBwdScan = 4, kDag = 5, kBcCtrs = 8 };
+
+struct BcArgs {
+    int32_t n;
+    int32_t S;
+    bool undirected;
+    const int32_t* __restrict__ offsets;
+    const int32_t* __restrict__ dests;
+    const int32_t* __restrict__ in_offsets;
+    const int32_t* __restrict__ in_srcs;
+    const int32_t* __restrict__ sources;
+    int32_t* level;
+    double2* sig;  // x = mantissa in [1,2) (or 0), y = binary exponent
+    double* delta;
+    uint64_t* log;
+    long long* lvl_cnt;
+    double* bc;
+    unsigned long long* ctr;
+};
+
+__device__ inline double2 xf_add(double2 a, double2 b) {
+    if (a.x == 0.0) return b;
+    if (b.x == 0.0) return a;
+    const double e = fmax(a.y, b.y);
+    const double s = ldexp(a.x, int(a.y - e)) + ldexp(b.x, int(b.y - e));
+    const int k = ilogb(s);
+    return make_double2(ldexp(s, -k), e + k);
+}
+
+__device__ inline double xf_ratio(double2 a, double2 b) { return ldexp(a.x / b.x, int(a.y - b.y)); }
+
+__device__ inline long long ld_volatile_ll(const long long* p) {
+    return *reinterpret_cast<const volatile long long*>(p);
+}
+
+__global__ void k_bc_seed(BcArgs a) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.S; s += gridDim.x * blockDim.x) {
+        const int32_t src = a.sources[s];
+        a.level[int64_t(s) * a.n + src] = 0;
+        a.log[s] = (uint64_t(s) << 32) | uint32_t(src);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.lvl_cnt[0] = a.S;
+}
+
+__global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint64_t s_q[kBcQueue];
+    __shared__ int s_qn;
+    __shared__ long long s_gpos;
+    const int tid = threadIdx.x;
+    unsigned long long fscan = 0, dag = 0;
+    long long beg = 0, end = a.S;
+    int L = 0;
+    for (;; ++L) {
+        for (long long base = beg + (long long)blockIdx.x * kBcBlock; base < end;
+             base += (long long)gridDim.x * kBcBlock) {
+            if (tid == 0) s_qn = 0;
+            __syncthreads();
+            const long long idx = base + tid;
+            if (idx < end) {
+                const uint64_t item = a.log[idx];
+                const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
+                const int64_t sb = int64_t(s) * a.n;
+                int32_t* lev = a.level + sb;
+                double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
+                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+                fscan += oe - ob;
+                for (int32_t e = ob; e < oe; ++e) {
+                    const int32_t w = a.dests[e];
+                    const int32_t lw = lev[w];
+                    if (a.undirected && L > 0 && lw == L - 1) {
+                        acc = xf_add(acc, a.sig[sb + w]);  // w is a parent of v
+                        ++dag;
+                    } else if (lw == -1 && atomicCAS(&lev[w], -1, L + 1) == -1) {
+                        const uint64_t x = (uint64_t(s) << 32) | uint32_t(w);
+                        const int pos = atomicAdd(&s_qn, 1);
+                        if (pos < kBcQueue) {
+                            s_q[pos] = x;
+                        } else {
+                            const long long p = atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], 1ull);
+                            a.log[end + p] = x;
+                        }
+                    }
+                }
+                if (!a.undirected && L > 0) {
+                    const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
+                    fscan += ie - ib;
+                    for (int32_t e = ib; e < ie; ++e) {
+                        const int32_t p = a.in_srcs[e];
+                        if (lev[p] == L - 1) {
+                            acc = xf_add(acc, a.sig[sb + p]);
+                            ++dag;
+                        }
+                    }
+                }
+                a.sig[sb + v] = acc;
+            }
+            __syncthreads();
+            const int qn = min(s_qn, kBcQueue);
+            if (tid == 0 && qn > 0)
+                s_gpos = (long long)atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], (unsigned long long)qn);
+            __syncthreads();
+            for (int i = tid; i < qn; i += kBcBlock) a.log[end + s_gpos + i] = s_q[i];
+            __syncthreads();
+        }
+        grid.sync();
+        const long long next = ld_volatile_ll(&a.lvl_cnt[L + 1]);
+        if (next == 0) break;
+        beg = end;
+        end += next;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        a.ctr[kTail] = (unsigned long long)end;
+        a.ctr[kLevels] = (unsigned long long)(L + 1);
+    }
+    for (int o = 16; o; o >>= 1) {
+        fscan += __shfl_xor_sync(0xffffffffu, fscan, o);
+        dag += __shfl_xor_sync(0xffffffffu, dag, o);
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&a.ctr[kFwdScan], fscan);
+        atomicAdd(&a.ctr[kDag], dag);
+    }
+}
+
+__global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const long long total = (long long)a.ctr[kTail];
+    const int levels = int(a.ctr[kLevels]);
+    unsigned long long bscan = 0, dag = 0;
+    long long end = total;
+    for (int L = levels - 1; L >= 0; --L) {
+        const long long beg = end - a.lvl_cnt[L];
+        for (long long idx = beg + (long long)blockIdx.x * kBcBlock + tid; idx < end;
+             idx += (long long)gridDim.x * kBcBlock) {
+            const uint64_t item = a.log[idx];
+            const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
+            const int64_t sb = int64_t(s) * a.n;
+            const int32_t* lev = a.level + sb;
+            const double2 sv = a.sig[sb + v];
+            double d = 0.0;
+            const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+            bscan += oe - ob;
+            for (int32_t e = ob; e < oe; ++e) {
+                const int32_t w = a.dests[e];
+                if (lev[w] == L + 1) {
+                    const double2 sw = a.sig[sb + w];
+                    if (sw.x > 0.0) {
+                        d += xf_ratio(sv, sw) * (1.0 + a.delta[sb + w]);
+                        ++dag;
+                    }
+                }
+            }
+            a.delta[sb + v] = d;
+            if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
+        }
+        end = beg;
+        grid.sync();
+    }
+    for (int o = 16; o; o >>= 1) {
+        bscan += __shfl_xor_sync(0xffffffffu, bscan, o);
+        dag += __shfl_xor_sync(0xffffffffu, dag, o);
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&a.ctr[kBwdScan], bscan);
+        atomicAdd(&a.ctr[kDag], dag);
+    }
+}
+
+}  // namespace gdx
+
+using namespace gdx;
+
+extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out,
+                      gdx_stats* stats) {
+    return guard_impl([&] {
+        if (!g || (!bc_out && g->n > 0) || (nsrc > 0 && !sources) || nsrc < 0)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        // interpreter.cpp:1115-1118 -- every node of the set must be in range.
+        std::vector<int32_t> hsrc(sources, sources + nsrc);
+        for (int32_t x : hsrc)
+            if (x < 0 || x >= g->n)
+                fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: node id " + std::to_string(x) +
+                                               " out of range [0, " + std::to_string(g->n) + ")");
+        if (!g->dests.get() && g->m > 0)
+            fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
+        if (g->n == 0) return;
+        DeviceGuard dg(g->device);
+        cudaStream_t s = g->stream;
+        if (!g->bc) g->bc = std::make_unique<BcWork>();
+        auto& W = *g->bc;
+        const int64_t n = g->n;
+        W.bc.ensure(n);
+        W.ctrs.ensure(kBcCtrs);
+        GDX_CUDA(cudaMemsetAsync(W.bc.get(), 0, n * sizeof(double), s));
+        unsigned long long totals[kBcCtrs] = {};
+        int launches = 0, max_levels = 0;
+        if (nsrc > 0) {
+            // batch size: 36 bytes per (source, vertex) of state + log
+            size_t free_b = 0, tot_b = 0;
+            GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+            const size_t per_src = size_t(n) * 36;
+            const size_t have = W.level.bytes() + W.sig.bytes() + W.delta.bytes() + W.log.bytes();
+            int64_t S = int64_t(double(free_b + have - std::min(free_b + have, (size_t(n) + 2) * 8)) *
+                                0.75 / double(per_src));
+            S = std::max<int64_t>(1, std::min<int64_t>({S, nsrc, 4096}));
+            if (W.batch < S) {
+                W.level.release();
+                W.sig.release();
+                W.delta.release();
+                W.log.release();
+                W.level.alloc(size_t(S) * n);
+                W.sig.alloc(size_t(S) * n * 2);
+                W.delta.alloc(size_t(S) * n);
+                W.log.alloc(size_t(S) * n);
+                W.batch = int32_t(S);
+            }
+            W.lvl_start.ensure(size_t(n) + 2);
+            W.sources.ensure(size_t(W.batch));
+            if (W.grid == 0) {
+                int a1 = 0, a2 = 0;
+                GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_bc_forward, kBcBlock, 0));
+                GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, k_bc_backward, kBcBlock, 0));
+                const int per_sm = std::min(a1, a2);
+                if (per_sm < 1) fail(GDX_ERR_CUDA, "CudaError: bc kernels cannot be resident");
+                W.grid = per_sm * g->num_sms;
+            }
+            BcArgs a;
+            a.n = g->n;
+            a.undirected = !g->directed;
+            a.offsets = g->offsets.get();
+            a.dests = g->dests.get();
+            a.in_offsets = g->rev_offsets.get();
+            a.in_srcs = g->rev_srcs.get();
+            a.sources = W.sources.get();
+            a.level = W.level.get();
+            a.sig = reinterpret_cast<double2*>(W.sig.get());
+            a.delta = W.delta.get();
+            a.log = W.log.get();
+            a.lvl_cnt = W.lvl_start.get();
+            a.bc = W.bc.get();
+            a.ctr = W.ctrs.get();
+            if (g->directed && (!a.in_offsets || !a.in_srcs))
+                fail(GDX_ERR_UNSUPPORTED, "Unsupported: directed BC needs the reverse CSR");
+            unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+            for (int32_t b0 = 0; b0 < nsrc; b0 += W.batch) {
+                const int32_t cnt = std::min<int32_t>(W.batch, nsrc - b0);
+                a.S = cnt;
+                GDX_CUDA(cudaMemcpyAsync(W.sources.get(), hsrc.data() + b0, cnt * 4,
+                                         cudaMemcpyHostToDevice, s));
+                GDX_CUDA(cudaMemsetAsync(W.level.get(), 0xff, size_t(cnt) * n * 4, s));
+                GDX_CUDA(cudaMemsetAsync(W.lvl_start.get(), 0, (size_t(n) + 2) * 8, s));
+                GDX_CUDA(cudaMemsetAsync(W.ctrs.get(), 0, kBcCtrs * 8, s));
+                timed_launch(g, "bc_seed", [&] { k_bc_seed<<<blocks_for(cnt, 256, 1024), 256, 0, s>>>(a); });
+                void* args[] = {&a};
+                timed_launch(g, "bc_forward", [&] {
+                    GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_bc_forward, dim3(W.grid),
+                                                         dim3(kBcBlock), args, 0, s));
+                });
+                timed_launch(g, "bc_backward", [&] {
+                    GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_bc_backward, dim3(W.grid),
+                                                         dim3(kBcBlock), args, 0, s));
+                });
+                launches += 3;
+                GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));
+                GDX_CUDA(cudaStreamSynchronize(s));
+                totals[kReached] += h[kTail];
+                totals[kFwdScan] += h[kFwdScan];
+                totals[kBwdScan] += h[kBwdScan];
+                totals[kDag] += h[kDag];
+                max_levels = std::max<int>(max_levels, int(h[kLevels]));
+            }
+        }
+        copy_out(g, bc_out, W.bc.get(), size_t(n) * sizeof(double));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        if (stats) {
+            stats->rounds = max_levels;
+            stats->launches = launches;
+            stats->vertices_visited = int64_t(totals[kReached]);
+            stats->edges_visited = int64_t(totals[kFwdScan] + totals[kBwdScan]);
+            stats->updates = int64_t(totals[kDag]);
+            // per reached (s,v): forward log 8 + offsets 8 +
+            // sigma 16 + discovery log write 8 + level CAS 4; backward log 8 +
+            // offsets 8 + sigma 16 + delta 8 + bc RMW 16.  Per scanned edge: dest 4 +
+            // level 4.  Per DAG edge use: sigma 16 (+ delta 8 backward ~ 12 avg).
+            stats->algorithmic_bytes = 100.0 * totals[kReached] +
+                                       8.0 * (totals[kFwdScan] + totals[kBwdScan]) +
+                                       28.0 * totals[kDag];
+        }
+    });
+}

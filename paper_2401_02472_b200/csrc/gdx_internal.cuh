@@ -1,0 +1,222 @@
+// gdx_internal.cuh -- shared internals of libgdx.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/gdx.h"
+
+namespace gdx {
+
+// ---------------------------------------------------------------------------
+// Errors: C++ exceptions inside the library, gdx_status at the boundary.
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    gdx_status code;
+    Error(gdx_status c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+[[noreturn]] inline void fail(gdx_status c, const std::string& msg) { throw Error(c, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    gdx_status code = e == cudaErrorMemoryAllocation ? GDX_ERR_OUT_OF_MEMORY : GDX_ERR_CUDA;
+    fail(code, std::string("CudaError: ") + what + " -> " + cudaGetErrorString(e) + " (" + file +
+                   ":" + std::to_string(line) + ")");
+}
+#define GDX_CUDA(x) ::gdx::cuda_check((x), #x, __FILE__, __LINE__)
+#define GDX_LAUNCH_CHECK() ::gdx::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Sets the calling thread's device for the scope.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) GDX_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Owning device buffer.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) count = 1;
+        GDX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    // Grow-only allocation (workspaces cached on the graph handle).
+    void ensure(size_t count) {
+        if (count > n || p == nullptr) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// Per-kernel CUDA-event timing (gdx_profile_*): events recorded on the
+// launching stream around every launch while enabled.
+struct Profiler {
+    bool enabled = false;
+    struct Rec {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<double, int64_t>> totals;
+
+    cudaEvent_t take() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        GDX_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    void drain() {  // fold completed pairs into totals (synchronises on them)
+        for (auto& r : pending) {
+            GDX_CUDA(cudaEventSynchronize(r.b));
+            float ms = 0.f;
+            GDX_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            auto& t = totals[r.name];
+            t.first += ms;
+            t.second += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+    ~Profiler() {
+        for (auto& r : pending) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+struct PrPlan;
+struct SsspWork;
+struct TcPlan;
+struct BcWork;
+
+}  // namespace gdx
+
+// The opaque handle behind gdx_graph*.
+struct gdx_graph {
+    int device = 0;
+    int32_t n = 0, m = 0;
+    bool directed = true;
+    bool weighted = false;     // false => every weight is 1
+    int32_t max_weight = 1;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+
+    gdx::DevBuf<int32_t> offsets, dests, weights, rev_offsets, rev_srcs, rev_eid;
+
+    gdx::Profiler prof;
+    std::unique_ptr<gdx::PrPlan> pr;
+    std::unique_ptr<gdx::SsspWork> sssp;
+    std::unique_ptr<gdx::TcPlan> tc;
+    std::unique_ptr<gdx::BcWork> bc;
+
+    // scratch for small device->host reads
+    int64_t* pinned = nullptr;  // 4 KB pinned host scratch
+
+    ~gdx_graph();
+};
+
+namespace gdx {
+
+// Launch helper: brackets a kernel launch with profiler events.
+template <class F>
+inline void timed_launch(gdx_graph* g, const char* name, F&& launch) {
+    if (!g->prof.enabled) {
+        launch();
+        GDX_LAUNCH_CHECK();
+        return;
+    }
+    cudaEvent_t a = g->prof.take(), b = g->prof.take();
+    GDX_CUDA(cudaEventRecord(a, g->stream));
+    launch();
+    GDX_LAUNCH_CHECK();
+    GDX_CUDA(cudaEventRecord(b, g->stream));
+    g->prof.pending.push_back({name, a, b});
+}
+
+// Copy with unified addressing (host pageable/pinned or device pointers).
+inline void copy_out(gdx_graph* g, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    GDX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream));
+}
+
+inline int blocks_for(int64_t items, int threads, int cap) {
+    int64_t b = (items + threads - 1) / threads;
+    if (b < 1) b = 1;
+    return static_cast<int>(b < cap ? b : cap);
+}
+
+// Builds the reverse CSR (csr.cpp:77-94 semantics) on the device.
+void build_reverse_device(gdx_graph* g);
+// Upload / finish a graph whose forward arrays are resident.
+void finalize_graph(gdx_graph* g);
+
+// Counter-based RNG: splitmix64 finaliser keyed
+// by (seed, stream).  Identical on host and device.
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t stream_key(uint64_t seed, uint64_t stream) {
+    return mix64(seed + stream * 0xD1B54A32D192ED03ULL);
+}
+__host__ __device__ inline uint64_t ctr_hash(uint64_t key, uint64_t ctr) {
+    return mix64(key ^ mix64(ctr));
+}
+__host__ __device__ inline double ctr_unit(uint64_t h) {
+    return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+__device__ inline uint32_t ctr_bounded(uint64_t h, uint32_t n) {
+    return static_cast<uint32_t>(__umul64hi(h, static_cast<uint64_t>(n)));
+}
+enum : uint64_t { kStreamRmat = 1, kStreamUniform = 2, kStreamGrid = 3, kStreamWeight = 4 };
+
+}  // namespace gdx

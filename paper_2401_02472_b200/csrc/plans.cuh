@@ -1,0 +1,62 @@
+// plans.cuh -- per-graph cached plans / workspaces of the four algorithms.
+// They live on the gdx_graph handle so repeated calls reuse device memory
+// (no cudaMalloc inside a steady-state call).
+#pragma once
+
+#include <functional>
+
+#include "gdx_internal.cuh"
+
+namespace gdx {
+
+int guard_impl(const std::function<void()>& f);
+gdx_graph* make_graph(int device);
+
+// PageRank merge-path plan (pagerank.cu).
+struct PrPlan {
+    int32_t ntiles = 0;
+    int32_t nslots = 0;
+    DevBuf<int32_t> tile_row, tile_edge;  // ntiles+1 merge-path coordinates
+    DevBuf<int32_t> tile_first_slot;      // slot of the tile's first row if it started earlier, else -1
+    DevBuf<int32_t> tile_carry_slot;      // slot receiving the tile's trailing partial row, else -1
+    DevBuf<int32_t> slot_row;             // row of each spanning slot
+    DevBuf<double> slot_acc;              // partial sums per slot (zeroed after use)
+    DevBuf<double> rank[2], contrib[2];
+    DevBuf<double> dangling;              // 3 rotating accumulators
+    DevBuf<int32_t> flags;                // per-round "unsettled" votes
+    int32_t flags_cap = 0;
+    int grid = 0;
+};
+
+// SSSP frontier workspace (sssp.cu).
+struct SsspWork {
+    DevBuf<uint64_t> dist;   // 32- or 64-bit distances (reinterpreted)
+    DevBuf<int32_t> stamp;   // round at which a vertex was last enqueued
+    DevBuf<int2> queue[2];   // work items (vertex, first edge)
+    DevBuf<unsigned long long> ctrs;  // rotating counters + stats
+    size_t qcap = 0;
+    int grid = 0;
+};
+
+// Triangle-counting workspace (tc.cu).
+struct TcPlan {
+    DevBuf<unsigned long long> acc;
+    DevBuf<int32_t> hi_start;  // first index of N(v) with dest > v
+};
+
+// BC batched Brandes workspace (bc.cu).
+struct BcWork {
+    int32_t batch = 0;
+    DevBuf<int32_t> level;      // [batch][n]
+    DevBuf<double> sig;         // [batch][n] x (mantissa, exponent)
+    DevBuf<double> delta;       // [batch][n]
+    DevBuf<uint64_t> log;       // (source slot << 32 | vertex), all levels
+    DevBuf<long long> lvl_start;
+    DevBuf<int32_t> sources;
+    DevBuf<double> bc;
+    DevBuf<unsigned long long> ctrs;
+    size_t log_cap = 0;
+    int grid = 0;
+};
+
+}  // namespace gdx

@@ -1,0 +1,284 @@
+// sssp.cu -- ComputeSSSP (reference corpus/sssp.sp:6-20) on sm_100a.
+//
+// The reference runs a topology-driven fixedPoint: every round scans all V
+// vertices, relaxes the out-edges of `modified` ones with atomicMin and does a
+// host round trip for the `finished` flag (tests/golden/sssp/cuda/
+// sssp_cuda.cu:117-199; interpreter.cpp:968-1000).  Here the whole fixedPoint
+// is ONE persistent cooperative kernel:
+//   * the frontier is a worklist of items (vertex, first edge); a vertex of
+//     degree d becomes ceil(d / kChunk) items, so hubs are split and every
+//     item carries at most kChunk edges;
+//   * warps grab G items at a time from a device counter and relax the
+//     concatenated edge list warp-cooperatively (lane j takes edge j of the
+//     warp's prefix-summed item lengths), atomicMin on the distance;
+//   * an improved vertex is enqueued once per round (round stamp), with a
+//     warp-aggregated atomicAdd on the next queue's tail;
+//   * rounds are separated by grid.sync(); the convergence test is "next
+//     queue empty" read on the device -- no host round trip per round.
+// Distances are 32-bit when n * max_weight fits (exact), else 64-bit; the
+// result is widened to int64 with INF = INT64_MAX/2 (oracles.hpp:12).  Any
+// correct relaxation order yields the unique shortest-path distances, so the
+// output is bit-identical to oracles::sssp and to interp::run.
+#include <cooperative_groups.h>
+
+#include "gdx_internal.cuh"
+#include "plans.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gdx {
+
+constexpr int kSsspBlock = 256;
+constexpr int kChunk = 32;  // max edges per work item
+
+// Counter layout in SsspWork::ctrs.
+enum { kQ = 0, kWork = 3, kRounds = 6, kVvis = 7, kEvis = 8, kUpd = 9, kCtrs = 16 };
+
+template <class D>
+struct SsspArgs {
+    int32_t n;
+    const int32_t* __restrict__ offsets;
+    const int32_t* __restrict__ dests;
+    const int32_t* __restrict__ weights;  // nullptr => 1
+    D* dist;
+    int32_t* stamp;
+    int2* q0;
+    int2* q1;
+    unsigned long long* ctr;
+};
+
+__device__ inline unsigned long long ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+template <class D>
+__global__ void k_sssp_init(SsspArgs<D> a, int32_t src, D inf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        a.dist[i] = i == src ? D(0) : inf;
+        a.stamp[i] = 0;
+    }
+    if (blockIdx.x == 0) {
+        int32_t b = a.offsets[src], e = a.offsets[src + 1];
+        int32_t items = (e - b + kChunk - 1) / kChunk;
+        for (int32_t t = threadIdx.x; t < items; t += blockDim.x) a.q0[t] = make_int2(src, b + t * kChunk);
+        if (threadIdx.x == 0) a.ctr[kQ + 0] = items;
+    }
+}
+
+template <class D>
+__global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const long long nwarps = (long long)gridDim.x * (kSsspBlock / 32);
+    unsigned long long vvis = 0, evis = 0, upd = 0;
+    int r = 0;
+    for (;; ++r) {
+        const int cur = r % 3, nxt = (r + 1) % 3, clr = (r + 2) % 3;
+        const int2* Q = (r & 1) ? a.q1 : a.q0;
+        int2* QN = (r & 1) ? a.q0 : a.q1;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.ctr[kQ + clr] = 0;
+            a.ctr[kWork + clr] = 0;
+        }
+        const unsigned long long qn = ld_volatile(&a.ctr[kQ + cur]);
+        // Items per warp grab: small frontiers spread over all warps.
+        unsigned long long g = qn / (unsigned long long)(nwarps * 4);
+        const int G = g < 1 ? 1 : (g > 32 ? 32 : int(g));
+        while (true) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&a.ctr[kWork + cur], (unsigned long long)G);
+            base = __shfl_sync(full, base, 0);
+            if (base >= qn) break;
+            const int cnt = int(min((unsigned long long)G, qn - base));
+            int v = 0, b = 0, len = 0;
+            D dv = 0;
+            if (lane < cnt) {
+                int2 it = Q[base + lane];
+                v = it.x;
+                b = it.y;
+                int32_t vb = a.offsets[v], ve = a.offsets[v + 1];
+                int32_t e = min(b + kChunk, ve);
+                len = e - b;
+                dv = a.dist[v];
+                vvis += (b == vb);
+            }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(full, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int total = __shfl_sync(full, incl, 31);
+            const int excl = incl - len;
+            evis += len;
+            for (int j0 = 0; j0 < total; j0 += 32) {
+                const int j = j0 + lane;
+                // owner = largest k with excl_k <= j (items past cnt have excl == total)
+                int k = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    int c = k + step;
+                    int ex = __shfl_sync(full, excl, c & 31);
+                    if (c < 32 && ex <= j) k = c;
+                }
+                const int ov = __shfl_sync(full, v, k);
+                const int ob = __shfl_sync(full, b, k);
+                const int oex = __shfl_sync(full, excl, k);
+                const D od = __shfl_sync(full, dv, k);
+                int pitems = 0, pv = 0;
+                if (j < total) {
+                    const int e = ob + (j - oex);
+                    const int nbr = a.dests[e];
+                    const D w = a.weights ? D(a.weights[e]) : D(1);
+                    const D cand = od + w;
+                    if (cand < a.dist[nbr]) {
+                        const D old = atomicMin(&a.dist[nbr], cand);
+                        if (cand < old) {
+                            ++upd;
+                            if (atomicExch(&a.stamp[nbr], r + 1) != r + 1) {
+                                int32_t d = a.offsets[nbr + 1] - a.offsets[nbr];
+                                pitems = (d + kChunk - 1) / kChunk;
+                                pv = nbr;
+                            }
+                        }
+                    }
+                }
+                (void)ov;
+                // warp-aggregated enqueue into the next round's worklist
+                int pincl = pitems;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(full, pincl, o);
+                    if (lane >= o) pincl += t;
+                }
+                const int ptotal = __shfl_sync(full, pincl, 31);
+                if (ptotal) {
+                    unsigned long long pbase = 0;
+                    if (lane == 31) pbase = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)ptotal);
+                    pbase = __shfl_sync(full, pbase, 31);
+                    if (pitems) {
+                        const int32_t first = a.offsets[pv];
+                        unsigned long long at = pbase + (pincl - pitems);
+                        for (int t = 0; t < pitems; ++t) QN[at + t] = make_int2(pv, first + t * kChunk);
+                    }
+                }
+            }
+        }
+        grid.sync();
+        if (ld_volatile(&a.ctr[kQ + nxt]) == 0) break;
+    }
+    // statistics
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        vvis += __shfl_xor_sync(full, vvis, o);
+        evis += __shfl_xor_sync(full, evis, o);
+        upd += __shfl_xor_sync(full, upd, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&a.ctr[kVvis], vvis);
+        atomicAdd(&a.ctr[kEvis], evis);
+        atomicAdd(&a.ctr[kUpd], upd);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr[kRounds] = r + 1;
+}
+
+template <class D>
+__global__ void k_sssp_widen(int32_t n, const D* __restrict__ dist, D inf, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        D d = dist[i];
+        out[i] = d == inf ? (INT64_MAX / 2) : int64_t(d);
+    }
+}
+
+template <class D>
+static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    auto& w = *g->sssp;
+    cudaStream_t s = g->stream;
+    SsspArgs<D> a;
+    a.n = g->n;
+    a.offsets = g->offsets.get();
+    a.dests = g->dests.get();
+    a.weights = g->weighted ? g->weights.get() : nullptr;
+    a.dist = reinterpret_cast<D*>(w.dist.get());
+    a.stamp = w.stamp.get();
+    a.q0 = w.queue[0].get();
+    a.q1 = w.queue[1].get();
+    a.ctr = w.ctrs.get();
+    const D inf = ~D(0);
+    if (w.grid == 0) {
+        int per_sm = 0;
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sssp_rounds<D>, kSsspBlock, 0));
+        if (per_sm < 1) fail(GDX_ERR_CUDA, "CudaError: sssp kernel cannot be resident");
+        w.grid = per_sm * g->num_sms;
+    }
+    GDX_CUDA(cudaMemsetAsync(w.ctrs.get(), 0, kCtrs * sizeof(unsigned long long), s));
+    timed_launch(g, "sssp_init", [&] {
+        k_sssp_init<D><<<blocks_for(g->n, 256, g->num_sms * 8), 256, 0, s>>>(a, src, inf);
+    });
+    timed_launch(g, "sssp_rounds", [&] {
+        void* args[] = {&a};
+        GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_sssp_rounds<D>, dim3(w.grid), dim3(kSsspBlock),
+                                             args, 0, s));
+    });
+    // Widen into the caller's buffer (host or device).  Device output: write in
+    // place; host output: widen into a device staging buffer, then copy.
+    cudaPointerAttributes pa;
+    bool dev_out = cudaPointerGetAttributes(&pa, dist_out) == cudaSuccess &&
+                   pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    int64_t* target = dev_out ? dist_out : reinterpret_cast<int64_t*>(w.queue[1].get());
+    timed_launch(g, "sssp_widen", [&] {
+        k_sssp_widen<D><<<blocks_for(g->n, 256, g->num_sms * 8), 256, 0, s>>>(g->n, a.dist, inf, target);
+    });
+    if (!dev_out) copy_out(g, dist_out, target, size_t(g->n) * sizeof(int64_t));
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h, w.ctrs.get(), kCtrs * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+        stats->rounds = int32_t(h[kRounds]);
+        stats->launches = 3;
+        stats->vertices_visited = int64_t(h[kVvis]);
+        stats->edges_visited = int64_t(h[kEvis]);
+        stats->updates = int64_t(h[kUpd]);
+        // per frontier vertex offsets pair 8 + dist + work item 8;
+        // per edge dest 4 + weight 4 + dist[nbr]; per improvement atomicMin + stamp 4 + push 8.
+        const double sd = sizeof(D), sw = g->weighted ? 4.0 : 0.0;
+        stats->algorithmic_bytes = (16.0 + sd) * h[kVvis] + (4.0 + sw + sd) * h[kEvis] +
+                                   (12.0 + sd) * h[kUpd];
+    }
+}
+
+}  // namespace gdx
+
+using namespace gdx;
+
+extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    return guard_impl([&] {
+        if (!g || !dist_out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        // interpreter.cpp:1131-1135 -- the node argument must be a valid id.
+        if (src < 0 || src >= g->n)
+            fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: node id " + std::to_string(src) +
+                                           " out of range [0, " + std::to_string(g->n) + ")");
+        if (!g->dests.get() && g->m > 0)
+            fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
+        DeviceGuard dg(g->device);
+        if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
+        auto& w = *g->sssp;
+        // every vertex enters a round's queue at most once: <= n + m/kChunk items
+        const size_t qcap = size_t(g->n) + size_t(g->m) / kChunk + 1;
+        w.dist.ensure(size_t(g->n));
+        w.stamp.ensure(size_t(g->n));
+        // queue[1] doubles as the int64 staging buffer for host outputs
+        w.queue[0].ensure(qcap);
+        w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
+        w.ctrs.ensure(kCtrs);
+        const bool narrow = int64_t(g->max_weight) * int64_t(g->n) < int64_t(0xFFFFFFFEll);
+        if (narrow)
+            run_sssp<unsigned int>(g, src, dist_out, stats);
+        else
+            run_sssp<unsigned long long>(g, src, dist_out, stats);
+    });
+}

@@ -1,0 +1,253 @@
+"""Device-resident graphs and the four entry points, over the C ABI.
+
+``DeviceGraph`` is the B200 counterpart of the reference's immutable
+``graphdsl::CsrGraph`` (core/include/graphdsl/csr.hpp:27-82): the same int32
+forward + reverse CSR arrays, uploaded once and kept in HBM, with the four
+corpus algorithms as methods.  ``HostCsr`` is the plain host-array layout used
+to move graphs in and out (it is exactly the CsrGraph span set).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import GdxCsrView, GdxGenParams, GdxStats, GraphdslError, check
+
+INF_DISTANCE = (2**63 - 1) // 2  # oracles.hpp:12 kInfiniteDistance
+
+
+def _ptr(a) -> Optional[int]:
+    """Raw address of a numpy array or torch tensor (host or device)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch.Tensor
+        if not a.is_contiguous():
+            raise GraphdslError("InvalidArgument", "tensor must be contiguous")
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise GraphdslError("InvalidArgument", "array must be C-contiguous")
+        return a.ctypes.data
+    raise GraphdslError("InvalidArgument", f"unsupported buffer type {type(a)!r}")
+
+
+def _i32(a):
+    if a is None or hasattr(a, "data_ptr"):
+        return a
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+@dataclass
+class HostCsr:
+    """Host copy of the CsrGraph arrays (csr.hpp:73-81)."""
+    n: int
+    m: int
+    directed: bool
+    offsets: np.ndarray
+    dests: np.ndarray
+    weights: np.ndarray
+    rev_offsets: np.ndarray
+    rev_srcs: np.ndarray
+    rev_eid: np.ndarray
+
+    # CsrGraph-style accessors (csr.hpp:35-47)
+    def node_count(self) -> int:
+        return self.n
+
+    def edge_count(self) -> int:
+        return self.m
+
+    def out_degree(self, v: int) -> int:
+        return int(self.offsets[v + 1] - self.offsets[v])
+
+    def in_degree(self, v: int) -> int:
+        return int(self.rev_offsets[v + 1] - self.rev_offsets[v])
+
+    def is_edge(self, u: int, v: int) -> bool:
+        lo, hi = int(self.offsets[u]), int(self.offsets[u + 1])
+        i = lo + int(np.searchsorted(self.dests[lo:hi], v))
+        return i < hi and int(self.dests[i]) == v
+
+
+class DeviceGraph:
+    """A CSR graph resident in HBM (opaque ``gdx_graph*``)."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+        n, m, d = C.c_int32(), C.c_int32(), C.c_int32()
+        check(_lib.load().gdx_graph_info(handle, C.byref(n), C.byref(m), C.byref(d)))
+        self.n, self.m, self.directed = n.value, m.value, bool(d.value)
+
+    # ---- construction ---------------------------------------------------------
+    @classmethod
+    def from_csr(cls, g, device: int = 0) -> "DeviceGraph":
+        """Upload CsrGraph arrays (numpy, or torch tensors on host or device).
+        Any of weights / rev_* / dests may be None (see gdx_csr_view)."""
+        lib = _lib.load()
+        arrs = {k: _i32(getattr(g, k, None)) for k in
+                ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")}
+        view = GdxCsrView(int(g.n), int(g.m), int(bool(g.directed)),
+                          *[_ptr(arrs[k]) for k in ("offsets", "dests", "weights", "rev_offsets",
+                                                    "rev_srcs", "rev_eid")])
+        h = C.c_void_p()
+        check(lib.gdx_graph_create(C.byref(view), device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def build_from_edges(cls, n: int, u, v, w=None, directed: bool = True,
+                         device: int = 0) -> "DeviceGraph":
+        """CsrGraph::buildFromEdges (csr.cpp:28-94) executed on the GPU."""
+        lib = _lib.load()
+        u, v, w = _i32(u), _i32(v), _i32(w)
+        h = C.c_void_p()
+        check(lib.gdx_graph_build_from_edges(int(n), int(len(u)), _ptr(u), _ptr(v), _ptr(w),
+                                             int(bool(directed)), device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def generate(cls, kind: str, nodes: int, edges: int = 0, seed: int = 1, *,
+                 a: float = 0.57, b: float = 0.19, c: float = 0.19, keep: float = 0.55,
+                 directed: bool = True, weights: Optional[tuple[int, int]] = None,
+                 device: int = 0) -> "DeviceGraph":
+        """Counter-based generators on the GPU: kind in {"rmat", "uniform", "grid"}
+        (grid: ``nodes`` is the side length)."""
+        lib = _lib.load()
+        k = {"rmat": 0, "uniform": 1, "grid": 2}[kind]
+        wlo, whi = weights if weights is not None else (1, 0)
+        p = GdxGenParams(k, int(nodes), int(edges), int(seed), a, b, c, keep,
+                         int(bool(directed)), int(wlo), int(whi))
+        h = C.c_void_p()
+        check(lib.gdx_graph_generate(C.byref(p), device, C.byref(h)))
+        return cls(h, device)
+
+    def set_hash_weights(self, lo: int, hi: int, seed: int) -> None:
+        check(_lib.load().gdx_graph_set_hash_weights(self._h, lo, hi, seed))
+
+    def download(self) -> HostCsr:
+        n, m = self.n, self.m
+        a = {k: np.empty(n + 1 if "offsets" in k else m, np.int32)
+             for k in ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")}
+        check(_lib.load().gdx_graph_download(
+            self._h, *[_ptr(a[k]) for k in ("offsets", "dests", "weights", "rev_offsets",
+                                              "rev_srcs", "rev_eid")]))
+        return HostCsr(n, m, self.directed, **a)
+
+    # ---- lifetime / streams ---------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            check(_lib.load().gdx_graph_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if not self._h:
+            raise GraphdslError("InvalidArgument", "graph handle is closed")
+        return self._h
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        check(_lib.load().gdx_graph_set_stream(self.handle, stream_ptr))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(_lib.load().gdx_graph_get_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    # ---- the four entry points ----------------------------------------------
+    def sssp(self, src: int, out=None, stats: Optional[dict] = None):
+        """ComputeSSSP -> int64 distances (INF = INT64_MAX/2).  ``out`` may be a
+        host array or a device tensor of n int64."""
+        res = out if out is not None else np.empty(self.n, np.int64)
+        st = GdxStats()
+        check(_lib.load().gdx_sssp(self.handle, int(src), _ptr(res), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res
+
+    def pagerank(self, damping: float = 0.85, threshold: float = 1e-6, max_iter: int = 100,
+                 out=None, stats: Optional[dict] = None):
+        """ComputePR -> (rank f64[n], rounds)."""
+        res = out if out is not None else np.empty(self.n, np.float64)
+        rounds = C.c_int32()
+        st = GdxStats()
+        check(_lib.load().gdx_pagerank(self.handle, float(damping), float(threshold),
+                                       int(max_iter), _ptr(res), C.byref(rounds), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res, rounds.value
+
+    def tc(self, stats: Optional[dict] = None) -> int:
+        """ComputeTC -> triangle count (tc.sp semantics)."""
+        cnt = C.c_int64()
+        st = GdxStats()
+        check(_lib.load().gdx_tc(self.handle, C.byref(cnt), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return cnt.value
+
+    def tc_range(self, v_begin: int, v_end: int, stats: Optional[dict] = None) -> int:
+        cnt = C.c_int64()
+        st = GdxStats()
+        check(_lib.load().gdx_tc_range(self.handle, int(v_begin), int(v_end), C.byref(cnt),
+                                       C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return cnt.value
+
+    def bc(self, sources: Sequence[int], out=None, stats: Optional[dict] = None):
+        """ComputeBC -> f64[n] (unnormalised, sources excluded)."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
+        if len(src) != len(sources):
+            raise GraphdslError("InvalidArgument", "bad source set")
+        res = out if out is not None else np.empty(self.n, np.float64)
+        st = GdxStats()
+        check(_lib.load().gdx_bc(self.handle, _ptr(src) if len(src) else None, len(src),
+                                 _ptr(res), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res
+
+    # ---- measurement -----------------------------------------------------------
+    def profile(self, enable: bool = True) -> None:
+        check(_lib.load().gdx_profile_enable(self.handle, int(enable)))
+
+    def profile_reset(self) -> None:
+        check(_lib.load().gdx_profile_reset(self.handle))
+
+    def profile_read(self) -> dict:
+        """{kernel: (total_ms, launches)} since the last reset."""
+        lib = _lib.load()
+        cnt = C.c_int32()
+        check(lib.gdx_profile_read(self.handle, None, None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        names = C.create_string_buffer(64 * max(k, 1))
+        ms = (C.c_double * max(k, 1))()
+        ln = (C.c_int64 * max(k, 1))()
+        check(lib.gdx_profile_read(self.handle, names, ms, ln, k, C.byref(cnt)))
+        out = {}
+        for i in range(k):
+            nm = names.raw[64 * i:64 * (i + 1)].split(b"\0", 1)[0].decode()
+            out[nm] = (ms[i], ln[i])
+        return out
+
+
+def device_count() -> int:
+    c = C.c_int()
+    check(_lib.load().gdx_device_count(C.byref(c)))
+    return c.value

@@ -1,0 +1,282 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the oracle.
+
+Bars (north star): SSSP distances and triangle counts bit-exact; PageRank and
+BC within 1e-6 relative (tightened to 1e-9 on small graphs, where the only
+difference is floating-point summation order), PageRank with the same number
+of fixedPoint rounds as the reference.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import G, known_graph, rel_err, reverse_of, sweep_graphs
+
+pytestmark = pytest.mark.gpu
+INF = (2**63 - 1) // 2
+CSR_KEYS = ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")
+
+
+def upload(gdx, g, with_rev=True):
+    if not with_rev:
+        g = G(g.n, g.m, g.directed, g.offsets, g.dests, g.weights)
+    return gdx.DeviceGraph.from_csr(g)
+
+
+def assert_same_csr(dev_host, exp, keys=CSR_KEYS):
+    for k in keys:
+        a, b = np.asarray(getattr(dev_host, k)), np.asarray(getattr(exp, k))
+        assert np.array_equal(a, b), k
+
+
+# ---- hand-checkable fixtures (reference tests) ---------------------------------
+
+def test_known_fixtures(gdx, known):
+    r = gdx.run("ComputeSSSP", known_graph(known["weighted_triangle"]), {"src": 0})
+    assert list(r.property("dist")) == [0, 5, 6]
+    assert not r.property("modified").any() and r.scalar("finished") is True
+    c = known["weighted_triangle_isolated"]
+    assert list(gdx.run("sssp", known_graph(c), {"src": 0}).property("dist")) == c["sssp0"]
+    r = gdx.run("ComputeTC", known_graph(known["k4"]), {})
+    assert r.scalar("triangleCount") == 4 and r.return_value == 4
+    r = gdx.run("ComputeBC", known_graph(known["path3"]), {"sourceSet": [0, 1, 2]})
+    assert list(r.property("bc")) == [0.0, 2.0, 0.0]
+    c = known["cycle7"]
+    bc = gdx.run("bc", known_graph(c), {"sourceSet": list(range(7))}).property("bc")
+    assert rel_err(bc, c["bc_all"]) < 1e-12
+    c = known["pr_two_cycle"]
+    r = gdx.run("ComputePR", known_graph(c), {"damping": 0.85, "threshold": 1e-9, "maxIter": 110})
+    assert rel_err(r.property("rank"), c["pr"]) < 1e-12 and r.scalar("iter") == c["pr_iter"]
+    for name, thr, mi in (("pr_rmat40", 1e-12, 1000), ("pr_maxiter3", 0.0, 3)):
+        c = known[name]
+        r = gdx.run("pr", known_graph(c), {"damping": 0.85, "threshold": thr, "maxIter": mi})
+        assert r.scalar("iter") == c["pr_iter"], name
+        assert rel_err(r.property("rank"), c["pr"]) < 1e-12, name
+    c = known["self_loops"]
+    g = known_graph(c)
+    assert list(gdx.run("sssp", g, {"src": 0}).property("dist")) == c["sssp0"]
+    assert gdx.run("tc", g, {}).return_value == c["tc"]
+    assert rel_err(gdx.run("bc", g, {"sourceSet": list(range(5))}).property("bc"), c["bc_all"]) < 1e-12
+
+
+def test_errors_match_reference(gdx, known):
+    err = known["errors"]
+    g = known_graph(known["weighted_triangle"])
+    dg = gdx.DeviceGraph.from_csr(g)
+    with pytest.raises(gdx.GraphdslError) as e:
+        dg.sssp(99)
+    assert str(e.value) == err["sssp_src_out_of_range"] and e.value.kind == "RuntimeError"
+    with pytest.raises(gdx.GraphdslError) as e:
+        dg.bc([0, 7])
+    assert str(e.value) == err["bc_source_out_of_range"]
+    with pytest.raises(gdx.GraphdslError) as e:
+        gdx.DeviceGraph.build_from_edges(2, [0], [5], None, True)
+    assert str(e.value) == err["invalid_edge"] and e.value.kind == "InvalidEdge"
+    with pytest.raises(gdx.GraphdslError) as e:
+        gdx.DeviceGraph.build_from_edges(2, [0], [1], [-3], True)
+    assert str(e.value) == err["negative_weight"]
+    # first offending edge in input order decides (csr.cpp:29-40)
+    with pytest.raises(gdx.GraphdslError, match=r"NegativeWeight: edge \(0, 1\)"):
+        gdx.DeviceGraph.build_from_edges(3, [0, 0], [1, 9], [-1, 1], True)
+    # pr.sp:9 divides by numNodes; interp raises on an empty graph
+    empty = gdx.DeviceGraph.build_from_edges(0, [], [], None, True)
+    with pytest.raises(gdx.GraphdslError, match="division by zero"):
+        empty.pagerank()
+    assert empty.tc() == 0
+    # fixedPoint cap 10n+100 (interpreter.cpp:977-986): never-settling PR
+    two = gdx.DeviceGraph.build_from_edges(2, [0, 1], [1, 0], None, True)
+    with pytest.raises(gdx.GraphdslError) as e:
+        two.pagerank(0.85, -1.0, 1000)
+    assert e.value.kind == "NonTermination"
+    r, it = two.pagerank(0.85, -1.0, 50)  # settles by maxIter: 51 rounds <= cap
+    assert it == 51
+
+
+# ---- acceptance criterion 2 sweep: 200 reference graphs ------------------------------
+
+def test_sweep_vs_reference(gdx, sweep):
+    for seed in range(1, 201):
+        und, dr = sweep_graphs(sweep, seed)
+        p = f"s{seed}_"
+        n = und.n
+        du = upload(gdx, und, with_rev=(seed % 2 == 0))  # odd seeds: reverse CSR built on GPU
+        if seed % 2:
+            assert_same_csr(du.download(), und, ("rev_offsets", "rev_srcs", "rev_eid"))
+        assert np.array_equal(du.sssp(seed % n), sweep[p + "sssp"]), seed
+        assert du.tc() == int(sweep[p + "tc"][0]), seed
+        assert rel_err(du.bc(list(range(n))), sweep[p + "bc"]) < 1e-9, seed
+        dd = upload(gdx, dr)
+        r, it = dd.pagerank(0.85, 1e-9, 110)
+        assert it == int(sweep[p + "pr_iter"][0]), seed
+        assert rel_err(r, sweep[p + "pr"]) < 1e-9, seed
+        du.close()
+        dd.close()
+
+
+# ---- GPU CSR builder == CsrGraph::buildFromEdges -------------------------------------
+
+@pytest.mark.parametrize("n,m,directed,weighted,seed", [
+    (1, 0, True, False, 1), (5, 0, False, False, 1), (50, 400, False, True, 2),
+    (300, 5000, True, True, 3), (1 << 12, 1 << 16, False, False, 4),
+    (1 << 14, 1 << 17, True, True, 5), (70000, 300000, False, True, 6)])
+def test_gpu_builder_bit_exact(gdx, port, n, m, directed, weighted, seed):
+    rng = np.random.default_rng(seed)
+    u, v = port.gen_rmat_edges(n, m, seed) if m else (np.zeros(0, np.int32),) * 2
+    w = rng.integers(0, 50, size=m).astype(np.int32) if weighted else None
+    exp = port.build_from_edges(n, u, v, w, directed)
+    dg = gdx.DeviceGraph.build_from_edges(n, u, v, w, directed)
+    assert (dg.n, dg.m, dg.directed) == (exp.n, exp.m, exp.directed)
+    assert_same_csr(dg.download(), exp)
+
+
+def test_gpu_builder_c1_reference_graph(gdx, port):
+    """C1 input exactly as the reference builds it: genRmatEdges(2^18, 2^22, 1)."""
+    u, v = port.gen_rmat_edges(1 << 18, 1 << 22, 1)
+    exp = port.build_from_edges(1 << 18, u, v, None, False)
+    assert exp.m == 7611081
+    dg = gdx.DeviceGraph.build_from_edges(1 << 18, u, v, None, False)
+    assert_same_csr(dg.download(), exp, ("offsets", "dests", "rev_offsets", "rev_srcs", "rev_eid"))
+
+
+# ---- SSSP ----------------------------------------------------------------------------
+
+def test_sssp_c1_bit_exact(gdx, port):
+    """Config 1: RMAT-18, ef 16, undirected, weights U[1,100] (withRandomWeights)."""
+    u, v = port.gen_rmat_edges(1 << 18, 1 << 22, 1)
+    g = port.with_random_weights(port.build_from_edges(1 << 18, u, v, None, False), 1, 100, 1)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 1, 12345, 262143):
+        st = {}
+        got = dg.sssp(src, stats=st)
+        exp = port.sssp(g, src)
+        assert np.array_equal(got, exp), src
+        if src == 0:
+            assert (exp < INF).sum() == 174054 and exp[exp < INF].max() == 209
+            assert st["rounds"] >= 2 and st["edges_visited"] >= g.m * 0.5
+
+
+def test_sssp_64bit_distances(gdx, port):
+    u, v = port.gen_rmat_edges(5000, 40000, 8)
+    g = port.build_from_edges(5000, u, v, None, True)
+    g.weights = np.random.default_rng(1).integers(1 << 28, 1 << 30, size=g.m).astype(np.int32)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 17):
+        assert np.array_equal(dg.sssp(src), port.sssp(g, src))
+
+
+def test_sssp_zero_weights_and_unreachable(gdx, port):
+    u, v = port.gen_uniform_edges(3000, 9000, 4)
+    g = port.build_from_edges(3000, u, v, None, True)
+    g.weights = (np.arange(g.m) % 3).astype(np.int32)  # many zero-weight edges
+    dg = gdx.DeviceGraph.from_csr(g)
+    got = dg.sssp(0)
+    assert np.array_equal(got, port.sssp(g, 0))
+    assert (got == INF).any()
+
+
+def test_sssp_device_output(gdx, port):
+    torch = pytest.importorskip("torch")
+    u, v = port.gen_rmat_edges(1 << 12, 1 << 15, 3)
+    g = port.with_random_weights(port.build_from_edges(1 << 12, u, v, None, False), 1, 100, 3)
+    dg = gdx.DeviceGraph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int64, device="cuda")
+    dg.sssp(5, out=out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), port.sssp(g, 5))
+
+
+# ---- PageRank ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("scale,directed", [(10, True), (16, True), (16, False), (18, True)])
+def test_pagerank_rmat(gdx, port, scale, directed):
+    n = 1 << scale
+    u, v = port.gen_rmat_edges(n, 16 * n, scale)
+    g = port.build_from_edges(n, u, v, None, directed)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for thr, mi in ((1e-6, 100), (1e-9, 110), (0.0, 5)):
+        exp, it = port.pr(g, 0.85, thr, mi)
+        got, rounds = dg.pagerank(0.85, thr, mi)
+        assert rounds == it, (thr, mi)
+        assert rel_err(got, exp) < 1e-9, (thr, mi)
+
+
+def test_pagerank_hub_rows_span_tiles(gdx, port):
+    """A star with in-degree >> tile size exercises the cross-tile slot path."""
+    n = 20000
+    u = np.arange(1, n, dtype=np.int32)
+    v = np.zeros(n - 1, np.int32)
+    u2, v2 = port.gen_uniform_edges(n, 5 * n, 9)
+    g = port.build_from_edges(n, np.concatenate([u, u2]), np.concatenate([v, v2]), None, True)
+    dg = gdx.DeviceGraph.from_csr(g)
+    exp, it = port.pr(g, 0.85, 1e-10, 200)
+    got, rounds = dg.pagerank(0.85, 1e-10, 200)
+    assert rounds == it and rel_err(got, exp) < 1e-9
+
+
+def test_pagerank_isolated_and_dangling(gdx, port):
+    g = port.build_from_edges(10, [0, 1, 2, 2], [1, 2, 0, 3], None, True)
+    exp, it = port.pr(g, 0.85, 1e-12, 500)
+    got, rounds = gdx.DeviceGraph.from_csr(g).pagerank(0.85, 1e-12, 500)
+    assert rounds == it and rel_err(got, exp) < 1e-12
+    assert abs(got.sum() - 1.0) < 1e-9
+
+
+# ---- Triangle counting ---------------------------------------------------------------
+
+@pytest.mark.parametrize("kind,scale,directed", [("uniform", 16, False), ("rmat", 14, False),
+                                                 ("rmat", 14, True), ("uniform", 18, True)])
+def test_tc(gdx, port, kind, scale, directed):
+    n = 1 << scale
+    u, v = (port.gen_uniform_edges if kind == "uniform" else port.gen_rmat_edges)(n, 8 * n, scale)
+    g = port.build_from_edges(n, u, v, None, directed)
+    dg = gdx.DeviceGraph.from_csr(g)
+    exp = port.tc(g)
+    assert dg.tc() == exp
+    mid = n // 3
+    assert dg.tc_range(0, mid) + dg.tc_range(mid, n) == exp
+    assert dg.tc_range(mid, n) == port.tc_range(g, mid, n)
+
+
+# ---- Betweenness centrality ------------------------------------------------------------
+
+def test_bc_rmat(gdx, port):
+    n = 1 << 12
+    u, v = port.gen_rmat_edges(n, 8 * n, 21)
+    for directed in (False, True):
+        g = port.build_from_edges(n, u, v, None, directed)
+        dg = gdx.DeviceGraph.from_csr(g)
+        srcs = [0, 1, 2, 5, 77, 1000, 4095, 1]  # duplicates are legal
+        assert rel_err(dg.bc(srcs), port.bc(g, srcs)) < 1e-9, directed
+
+
+def test_bc_grid_and_overflow(gdx, port):
+    gu, gv = port.gen_grid_ctr(100, 0.55, 3)
+    g = port.build_from_edges(100 * 100, gu, gv, None, False)
+    srcs = [0, 4242, 9999, 5050]
+    assert rel_err(gdx.DeviceGraph.from_csr(g).bc(srcs), port.bc(g, srcs)) < 1e-9
+    side = 600  # full grid: the reference's double sigma overflows
+    gu, gv = port.gen_grid_ctr(side, 2.0, 1)
+    g = port.build_from_edges(side * side, gu, gv, None, False)
+    got = gdx.DeviceGraph.from_csr(g).bc([0])
+    assert np.isfinite(got).all()
+    assert rel_err(got, port.bc(g, [0])) < 1e-6
+
+
+# ---- GPU generators == their CPU twin ---------------------------------------------------
+
+def test_generators_match_cpu_twin(gdx, port):
+    n, E = 1 << 14, 1 << 17
+    dg = gdx.DeviceGraph.generate("rmat", n, E, seed=5, directed=True)
+    u, v = port.gen_rmat_ctr(n, E, 5)
+    assert_same_csr(dg.download(), port.build_from_edges(n, u, v, None, True),
+                    ("offsets", "dests", "rev_offsets", "rev_srcs", "rev_eid"))
+    dg = gdx.DeviceGraph.generate("uniform", 5000, 40000, seed=6, directed=False,
+                                  weights=(1, 100))
+    u, v = port.gen_uniform_ctr(5000, 40000, 6)
+    exp = port.build_from_edges(5000, u, v, None, False)
+    exp.weights = port.hash_weights(exp, 1, 100, 6)
+    assert_same_csr(dg.download(), exp)
+    dg = gdx.DeviceGraph.generate("grid", 64, seed=7, keep=0.55, directed=False)
+    u, v = port.gen_grid_ctr(64, 0.55, 7)
+    assert_same_csr(dg.download(), port.build_from_edges(64 * 64, u, v, None, False),
+                    ("offsets", "dests", "rev_offsets", "rev_srcs", "rev_eid"))
