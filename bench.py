@@ -1,0 +1,467 @@
+#!/usr/bin/env python3
+"""bench.py -- GTEPS of the B200 backend on the BASELINE.json configurations.
+
+Headline (the `value` of the JSON line): config 2 of BASELINE.json --
+PageRank pull (d=0.85, tol 1e-6, maxIter 100) on an RMAT scale-24 graph
+(2^28 edge draws, ~268M directed edges), one gdx_pagerank call per step, graph
+resident in HBM.  The other configs are reported under "per_algorithm"
+(SSSP RMAT-18 C1, TC uniform 2^24 C3, BC 64 sources on a 4899^2 grid C4).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--algos pr,sssp,tc,bc] [--no-cpu-baseline]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL); the N ranks run
+independent replicas of the step, timing is the
+max over ranks.  `--impl reference` times the reference's own CPU path
+(oracle/_ref: interp::run in parallel mode on all host cores) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS per algorithm (SSSP/PR/TC/BC) at 1/2/4/8 B200; % of HBM roofline"
+FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+# ----------------------------------------------------------------------------- utils
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed `ncu --set full` summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+                for nm, val in zip(names, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, torch):
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self, torch):
+        if self.pg:
+            self.pg.barrier()
+        torch.cuda.synchronize()
+
+    def max(self, torch, x: float) -> float:
+        if not self.pg:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ------------------------------------------------------------------------ our arm
+
+def timed_steps(torch, dist, step, steps: int, warmup: int, flush):
+    """W warm-up steps, then K steps each preceded by an L2 flush; returns
+    (per-step ms list, bracketed total ms).  Device time via CUDA events on the
+    current stream (the library runs on it, see gdx_graph_set_stream)."""
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    results = []
+    dist.barrier(torch)
+    t0 = time.perf_counter()
+    for a, b in evs:
+        flush.zero_()
+        a.record()
+        results.append(step())
+        b.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3
+    dist.barrier(torch)
+    return [a.elapsed_time(b) for a, b in evs], wall, results
+
+
+def roofline(prof: dict, kernel: str, algo_bytes: float, pk: dict) -> dict:
+    ms, launches = prof.get(kernel, (0.0, 0))
+    achieved = algo_bytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"kernel": kernel, "bound": "hbm", "achieved": round(achieved, 1),
+            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+            "peak_source": pk["source"], "traffic": ncu_traffic(kernel),
+            "kernel_ms_avg": round(ms / max(launches, 1), 4), "launches": launches,
+            "algorithmic_bytes_per_launch": round(algo_bytes / max(launches, 1), 1)}
+
+
+def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
+    scale, draws = 24, 1 << 28
+    dg = gdx.DeviceGraph.generate("rmat", 1 << scale, draws, seed=1, directed=True,
+                                  device=dist.local)
+    n, m = dg.n, dg.m
+    dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    stats = {}
+
+    def step():
+        _, rounds = dg.pagerank(0.85, 1e-6, 100, out=out, stats=stats)
+        return rounds
+
+    dg.profile(True)
+    for _ in range(args.warmup):
+        step()
+    dg.profile_reset()
+    with Clocks(dist.local) as clk:
+        ms, wall, rounds = timed_steps(torch, dist, step, args.steps, 0, flush)
+    prof = dg.profile_read()
+    dg.profile(False)
+    total_ms = dist.max(torch, sum(ms))
+    edges = float(m) * sum(rounds)
+    res = {
+        "workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 tol=1e-6 maxIter=100",
+        "n": n, "m": m, "rounds": rounds[-1], "gteps": edges * dist.world / (total_ms * 1e-3) / 1e9,
+        "ms_per_step": total_ms / args.steps, "wall_ms": wall,
+        "roofline": roofline(prof, "pr_tiles", sum(rounds) * (12.0 * m + 32.0 * n), pk),
+        "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
+        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
+    }
+    # ---- e2e: host CSR arrays -> C ABI (upload) -> PR -> host rank --------------
+    h = dg.download()
+    pin = {k: torch.from_numpy(getattr(h, k)).pin_memory() for k in ("offsets", "rev_offsets", "rev_srcs")}
+    rank_host = torch.empty(n, dtype=torch.float64).pin_memory()
+
+    class View:
+        pass
+
+    v = View()
+    v.n, v.m, v.directed = n, m, True
+    v.offsets, v.rev_offsets, v.rev_srcs = pin["offsets"], pin["rev_offsets"], pin["rev_srcs"]
+    v.dests = v.weights = v.rev_eid = None
+
+    def e2e_step():
+        g2 = gdx.DeviceGraph.from_csr(v, device=dist.local)
+        _, r = g2.pagerank(0.85, 1e-6, 100, out=rank_host)
+        g2.close()
+        return r
+
+    dg.close()
+    e2e_step()
+    dist.barrier(torch)
+    t0 = time.perf_counter()
+    rr = [e2e_step() for _ in range(args.steps)]
+    e2e_s = dist.max(torch, time.perf_counter() - t0)
+    res["e2e"] = {"value": float(m) * sum(rr) * dist.world / e2e_s / 1e9, "unit": "GTEPS",
+                  "h2d_bytes_per_step": int(sum(t.numel() * 4 for t in pin.values())),
+                  "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3 / args.steps,
+                  "path": "gdx_graph_create(host CSR) + gdx_pagerank(host out) + destroy"}
+    if cpu_baseline:
+        res["cpu_baseline"] = cpu_pr_baseline(h)
+    return res
+
+
+def cpu_pr_baseline(h) -> dict:
+    from oracle import Port
+    port = Port()
+    cores = os.cpu_count() or 1
+    k = 2
+    t0 = time.perf_counter()
+    port.pr_rounds(h, 0.85, k, threads=cores)
+    t = time.perf_counter() - t0
+    return {"value": h.m * k / t / 1e9, "unit": "GTEPS", "cores": cores, "kind": "port",
+            "sample": f"oracle port (gdx_oracle.cpp orc_pr_rounds, pr.sp semantics) {k} rounds "
+                      f"of the same C2 graph on {cores} threads: {t:.2f}s"}
+
+
+def bench_sssp(torch, gdx, dist, args, pk) -> dict:
+    dg = gdx.DeviceGraph.generate("rmat", 1 << 18, 1 << 22, seed=1, directed=False,
+                                  weights=(1, 100), device=dist.local)
+    dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    out = torch.empty(dg.n, dtype=torch.int64, device="cuda")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    st_all = []
+
+    def step():
+        st = {}
+        dg.sssp(0, out=out, stats=st)
+        st_all.append(st)
+        return st
+
+    dg.profile(True)
+    for _ in range(args.warmup):
+        step()
+    dg.profile_reset()
+    st_all.clear()
+    ms, wall, sts = timed_steps(torch, dist, step, args.steps, 0, flush)
+    prof = dg.profile_read()
+    total = dist.max(torch, sum(ms))
+    res = {"workload": "C1 SSSP RMAT-18 ef16 undirected, weights U[1,100], src 0",
+           "n": dg.n, "m": dg.m, "rounds": sts[-1]["rounds"],
+           "edges_visited_over_m": sts[-1]["edges_visited"] / dg.m,
+           "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
+           "ms_per_step": total / args.steps,
+           "roofline": roofline(prof, "sssp_rounds", sum(s["algorithmic_bytes"] for s in sts), pk),
+           "gpu_launches": int(sum(v[1] for v in prof.values()))}
+    dg.close()
+    return res
+
+
+def bench_tc(torch, gdx, dist, args, pk) -> dict:
+    dg = gdx.DeviceGraph.generate("uniform", 1 << 24, 1 << 27, seed=1, directed=False,
+                                  device=dist.local)
+    dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    sts = []
+
+    def step():
+        st = {}
+        c = dg.tc(stats=st)
+        sts.append(st)
+        return c
+
+    dg.profile(True)
+    for _ in range(args.warmup):
+        step()
+    dg.profile_reset()
+    sts.clear()
+    ms, wall, counts = timed_steps(torch, dist, step, args.steps, 0, flush)
+    prof = dg.profile_read()
+    total = dist.max(torch, sum(ms))
+    res = {"workload": "C3 TC uniform 2^24 vertices, 2^27 draws, undirected",
+           "n": dg.n, "m": dg.m, "triangles": counts[-1],
+           "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
+           "ms_per_step": total / args.steps,
+           "roofline": roofline(prof, "tc", sum(s["algorithmic_bytes"] for s in sts), pk),
+           "gpu_launches": int(sum(v[1] for v in prof.values()))}
+    dg.close()
+    return res
+
+
+def bench_bc(torch, gdx, dist, args, pk) -> dict:
+    import numpy as np
+    side = 4899
+    dg = gdx.DeviceGraph.generate("grid", side, seed=1, keep=0.55, directed=False,
+                                  device=dist.local)
+    dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    h = dg.download()
+    deg = np.diff(h.offsets)
+    cand = np.flatnonzero(deg > 0)
+    rng = np.random.default_rng(1)
+    sources = sorted(rng.choice(cand, size=args.bc_sources, replace=False).tolist())
+    out = torch.empty(dg.n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    sts = []
+
+    def step():
+        st = {}
+        dg.bc(sources, out=out, stats=st)
+        sts.append(st)
+        return st
+
+    dg.profile(True)
+    for _ in range(max(1, args.warmup // 3)):
+        step()
+    dg.profile_reset()
+    sts.clear()
+    steps = max(1, args.steps // 2)
+    ms, wall, _ = timed_steps(torch, dist, step, steps, 0, flush)
+    prof = dg.profile_read()
+    total = dist.max(torch, sum(ms))
+    res = {"workload": f"C4 BC {len(sources)} sources, {side}^2 grid keep 0.55 undirected",
+           "n": dg.n, "m": dg.m, "levels": sts[-1]["rounds"], "steps": steps,
+           "gteps": dg.m * len(sources) * steps * dist.world / (total * 1e-3) / 1e9,
+           "ms_per_step": total / steps,
+           "roofline": roofline(prof, "bc_forward", sum(s["algorithmic_bytes"] for s in sts) / 2, pk),
+           "gpu_launches": int(sum(v[1] for v in prof.values()))}
+    dg.close()
+    return res
+
+
+def run_ours(args) -> None:
+    import torch
+
+    import paper_2401_02472_b200 as gdx
+    dist = Dist()
+    dist.init(torch)
+    pk = peaks()
+    algos = [a for a in args.algos.split(",") if a]
+    cpu = dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline
+    per = {}
+    head = bench_pr(torch, gdx, dist, args, pk, cpu)
+    for a in algos:
+        if a == "sssp":
+            per["sssp"] = bench_sssp(torch, gdx, dist, args, pk)
+        elif a == "tc":
+            per["tc"] = bench_tc(torch, gdx, dist, args, pk)
+        elif a == "bc":
+            per["bc"] = bench_bc(torch, gdx, dist, args, pk)
+    per["pr"] = {k: head[k] for k in ("workload", "gteps", "ms_per_step", "rounds", "roofline")}
+    line = {
+        "metric": METRIC, "value": round(head["gteps"], 3), "unit": "GTEPS",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(head["ms_per_step"], 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: counter-based RMAT generator (a,b,c,d=.57,.19,.19,.05), seed 1, built on GPU",
+        "config": {"workload": head["workload"], "graph": "rmat-24", "n": head["n"], "m": head["m"],
+                   "pr_rounds": head["rounds"], "damping": 0.85, "threshold": 1e-6, "max_iter": 100,
+                   "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "roofline": head["roofline"], "e2e": head["e2e"], "clocks": head["clocks"],
+        "gpu_launches": head["gpu_launches"], "kernels": head["kernels"],
+        "per_algorithm": per,
+    }
+    if "cpu_baseline" in head:
+        line["cpu_baseline"] = head["cpu_baseline"]
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args) -> None:
+    """The reference's own CPU path (oracle/_ref = reference sources compiled
+    unchanged): interp::run(ComputePR) in ExecMode::Parallel on all host
+    cores.  Rank 0 only; other ranks exit without work."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import Ref, ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    scale = args.ref_scale
+    u, v = ref.gen_rmat_edges(1 << scale, 16 << scale, 1)
+    g = ref.build(1 << scale, u, v, None, True)
+    times, rounds = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, it = g.interp_pr(0.85, 1e-6, 100, parallel=True, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            rounds.append(it)
+    total = sum(times)
+    value = g.m * sum(rounds) / total / 1e9
+    sample = (f"interp::run(ComputePR, d=0.85 tol=1e-6 maxIter=100) ExecMode::Parallel on {cores} "
+              f"threads, RMAT scale-{scale} (genRmatEdges, 2^{scale + 4} draws, directed, "
+              f"m={g.m}, {rounds[-1]} rounds) per step -- the reference's tree-walking executor "
+              f"cannot run RMAT-24 within the bench budget")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference genRmatEdges)",
+        "config": {"workload": "C2 PageRank pull RMAT (bounded CPU sample)", "graph": f"rmat-{scale}",
+                   "m": g.m},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algos", default="sssp,tc,bc")
+    ap.add_argument("--bc-sources", type=int, default=64)
+    ap.add_argument("--ref-scale", type=int, default=18)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
