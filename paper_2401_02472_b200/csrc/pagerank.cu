@@ -5,23 +5,26 @@
 // mass, a thread-per-vertex pull that re-reads the source's out-degree per
 // in-edge, and a copy-back kernel (tests/golden/pr/cuda/pr_cuda.cu:117-212).
 //
-// Here one round is one merge-path gather over the reverse CSR:
-//   * the (rows + in-edges) merge path is cut into fixed tiles of kTile items
-//     (perfect load balance regardless of in-degree skew);
-//   * a tile's rev_srcs are read coalesced and the precomputed
-//     contrib[u] = rank[u] / outdeg(u) values gathered into shared memory with
-//     kItems independent loads per thread;
-//   * each thread reduces its merge-path segment; a block-wide reduce-by-key
-//     scan stitches rows that cross threads; rows that cross tiles are summed
-//     through a compact per-row slot array and finished by a tiny fixup
-//     kernel;
-//   * the epilogue is fused: new rank, |change| >= threshold vote, next
-//     contrib, and the next round's dangling mass (one atomic per block);
+// Here one round is one merge-path gather over the reverse CSR (k_pr_gather):
+//   * the (rows + in-edges) merge path is cut into fixed tiles of
+//     kPrBlock * ITEMS items -- perfect load balance regardless of the
+//     in-degree skew (RMAT-24: 56% of rows empty, max in-degree 238,735);
+//   * per tile the row ends and rev_srcs are staged in shared memory with
+//     coalesced loads; each thread gathers the precomputed
+//     contrib[u] = rank[u] / outdeg(u) of its own segment into registers
+//     (ITEMS independent loads) and reduces it row by row;
+//   * rows are finished where they complete (fused epilogue: new rank,
+//     |change| >= threshold vote, next contrib, next round's dangling mass);
+//     a block-wide reduce-by-key scan carries partial sums across threads and
+//     rows crossing tiles are summed through a compact slot array and
+//     finished by k_pr_fixup;
 //   * rounds are enqueued in batches without host syncs; a round whose
 //     predecessor voted "settled" exits immediately on the device.
 // Term-wise arithmetic matches pr.sp (contrib is the same f64 quotient the
 // interpreter computes per in-edge); only the summation order differs.
 #include <cub/cub.cuh>
+
+#include <cstdlib>
 
 #include "gdx_internal.cuh"
 #include "plans.cuh"
@@ -39,10 +42,8 @@ struct PrArgs {
     const int32_t* __restrict__ offsets;
     const int32_t* __restrict__ rev_offsets;
     const int32_t* __restrict__ rev_srcs;
-    const int32_t* __restrict__ tile_row;
-    const int32_t* __restrict__ tile_edge;
-    const int32_t* __restrict__ tile_first_slot;
-    const int32_t* __restrict__ tile_carry_slot;
+    const int2* __restrict__ tile_coord;  // (row, edge) merge-path coordinate per tile boundary
+    const int2* __restrict__ tile_slots;  // (first-row slot, carry slot) per tile, -1 = none
     const int32_t* __restrict__ slot_row;
     double* slot_acc;
     double* rank0;
@@ -55,15 +56,6 @@ struct PrArgs {
     int32_t max_iter;
 };
 
-struct KV {
-    int32_t key;
-    double val;
-};
-struct KVOp {
-    __device__ KV operator()(const KV& a, const KV& b) const {
-        return b.key == a.key ? KV{b.key, a.val + b.val} : b;
-    }
-};
 
 __device__ inline bool round_skipped(const PrArgs& a, int round) {
     return round > 0 && *reinterpret_cast<const volatile int32_t*>(&a.flags[round - 1]) == 0;
@@ -96,7 +88,28 @@ __device__ inline void block_flush(const PrArgs& a, int round, double dang_local
     }
 }
 
-__global__ void __launch_bounds__(kPrBlock) k_pr_tiles(PrArgs a, int round) {
+struct KV {
+    int32_t key;
+    double val;
+};
+struct KVOp {
+    __device__ KV operator()(const KV& a, const KV& b) const {
+        return b.key == a.key ? KV{b.key, a.val + b.val} : b;
+    }
+};
+
+// One PageRank round over tiles of kPrBlock * ITEMS merge-path items.
+// Per tile: row ends and rev_srcs are staged in shared memory (coalesced);
+// each thread locates its merge-path segment, gathers exactly the contrib
+// values of its segment's in-edges into registers (ITEMS independent loads),
+// reduces them row by row and finishes every row it completes on the spot
+// (fused epilogue).  Only the first row a thread completes waits for the block
+// scan that carries partial sums across threads; rows crossing tile
+// boundaries go through slot_acc and k_pr_fixup.
+template <int ITEMS, int MINB>
+__global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int round) {
+    constexpr int TILE = kPrBlock * ITEMS;
+    typedef cub::BlockScan<KV, kPrBlock, cub::BLOCK_SCAN_RAKING> Scan;
     if (round_skipped(a, round)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.dangling[(round + 2) % 3] = 0.0;
     const double dang_in = *reinterpret_cast<const volatile double*>(&a.dangling[round % 3]);
@@ -105,81 +118,96 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_tiles(PrArgs a, int round) {
     double* __restrict__ rank_out = (round & 1) ? a.rank0 : a.rank1;
     double* __restrict__ contrib_out = (round & 1) ? a.contrib0 : a.contrib1;
 
-    __shared__ int32_t s_end[kTile + 1];
-    __shared__ double s_val[kTile];
-    __shared__ double s_sum[kTile];
-    typedef cub::BlockScan<KV, kPrBlock> Scan;
+    __shared__ int32_t s_end[TILE + 1];
+    __shared__ int32_t s_src[TILE];
     __shared__ typename Scan::TempStorage scan_tmp;
-
     const int tid = threadIdx.x;
     double dang_local = 0.0;
     int unsettled = 0;
-    for (int32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        const int32_t row0 = a.tile_row[t], e0 = a.tile_edge[t];
-        const int32_t nrows = a.tile_row[t + 1] - row0, nedges = a.tile_edge[t + 1] - e0;
+    int32_t t = blockIdx.x;
+    int2 c0 = make_int2(0, 0), c1 = c0, n0 = c0, n1 = c0;
+    if (t < a.ntiles) {
+        c0 = a.tile_coord[t];
+        c1 = a.tile_coord[t + 1];
+    }
+    for (; t < a.ntiles; t += gridDim.x) {
+        const int32_t tn = t + gridDim.x;
+        if (tn < a.ntiles) {  // prefetch the next tile's coordinates
+            n0 = a.tile_coord[tn];
+            n1 = a.tile_coord[tn + 1];
+        }
+        const int2 slots = a.tile_slots[t];
+        const int32_t row0 = c0.x, e0 = c0.y;
+        const int nrows = c1.x - row0, nedges = c1.y - e0;
         for (int i = tid; i <= nrows; i += kPrBlock) {
             const int32_t r = row0 + i;
             s_end[i] = r < a.n ? a.rev_offsets[r + 1] - e0 : INT32_MAX;
         }
-        int32_t src[kItems];
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
+        for (int k = 0; k < ITEMS; ++k) {
             const int i = tid + k * kPrBlock;
-            src[k] = i < nedges ? a.rev_srcs[e0 + i] : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-            const int i = tid + k * kPrBlock;
-            if (src[k] >= 0) s_val[i] = __ldg(&contrib[src[k]]);
+            if (i < nedges) s_src[i] = a.rev_srcs[e0 + i];
         }
         __syncthreads();
-
-        // merge-path coordinate of this thread's first item
         const int tile_items = nrows + nedges;
-        const int diag = min(tid * kItems, tile_items);
-        const int diag_end = min(diag + kItems, tile_items);
-        int lo = max(diag - nedges, 0), hi = min(diag, nrows);
-        while (lo < hi) {
-            const int p = (lo + hi) >> 1;
-            if (s_end[p] <= diag - p - 1)
-                lo = p + 1;
+        auto search = [&](int diag) {
+            int lo = max(diag - nedges, 0), hi = min(diag, nrows);
+            while (lo < hi) {
+                const int p = (lo + hi) >> 1;
+                if (s_end[p] <= diag - p - 1)
+                    lo = p + 1;
+                else
+                    hi = p;
+            }
+            return lo;
+        };
+        const int diag = min(tid * ITEMS, tile_items);
+        const int diag_end = min(diag + ITEMS, tile_items);
+        const int xs = search(diag), xe = search(diag_end);
+        const int ys = diag - xs, ye = diag_end - xe;
+        double v[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+            v[k] = ys + k < ye ? __ldg(&contrib[s_src[ys + k]]) : 0.0;
+        int x = xs;
+        int cur_end = s_end[x];
+        bool first = true;
+        double first_sum = 0.0, run = 0.0;
+        auto finish = [&](int row, double sum) {
+            if (row == 0 && slots.x >= 0)
+                atomicAdd(&a.slot_acc[slots.x], sum);  // row began in an earlier tile
             else
-                hi = p;
-        }
-        int x = lo, y = diag - lo;
-        const int start_row = x;
-        bool completed = false;
-        double run = 0.0;
-        for (int it = diag; it < diag_end; ++it) {
-            if (y < s_end[x]) {
-                run += s_val[y];
-                ++y;
+                pr_epilogue(a, round, row0 + row, sum, dang_in, rank_in, rank_out, contrib_out,
+                            dang_local, unsettled);
+        };
+        auto complete = [&]() {
+            if (first) {
+                first_sum = run;
+                first = false;
             } else {
-                s_sum[x] = run;
-                run = 0.0;
-                ++x;
-                completed = true;
+                finish(x, run);
+            }
+            run = 0.0;
+            ++x;
+            cur_end = s_end[x];
+        };
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            if (ys + k < ye) {
+                while (cur_end <= ys + k) complete();
+                run += v[k];
             }
         }
+        while (x < xe) complete();
         KV carry{x, run}, prefix, agg;
         Scan(scan_tmp).ExclusiveScan(carry, prefix, KVOp(), agg);
-        if (tid > 0 && completed && prefix.key == start_row) s_sum[start_row] += prefix.val;
-        __syncthreads();
-
-        const int32_t fslot = a.tile_first_slot[t];
-        for (int i = tid; i < nrows; i += kPrBlock) {
-            const double sum = s_sum[i];
-            if (i == 0 && fslot >= 0) {
-                atomicAdd(&a.slot_acc[fslot], sum);  // row began in an earlier tile
-                continue;
-            }
-            pr_epilogue(a, round, row0 + i, sum, dang_in, rank_in, rank_out, contrib_out,
-                        dang_local, unsettled);
+        if (!first) {
+            if (tid > 0 && prefix.key == xs) first_sum += prefix.val;
+            finish(xs, first_sum);
         }
-        if (tid == 0) {
-            const int32_t cs = a.tile_carry_slot[t];
-            if (cs >= 0) atomicAdd(&a.slot_acc[cs], agg.val);  // row continues in the next tile
-        }
+        if (tid == 0 && slots.y >= 0) atomicAdd(&a.slot_acc[slots.y], agg.val);
+        c0 = n0;
+        c1 = n1;
         __syncthreads();
     }
     block_flush(a, round, dang_local, unsettled);
@@ -221,13 +249,13 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_init(PrArgs a) {
 }
 
 // Merge-path coordinates of every tile boundary over (row ends, edge ids).
-__global__ void k_pr_tile_coords(int32_t n, int32_t m, int32_t ntiles,
-                                 const int32_t* __restrict__ rev_offsets, int32_t* tile_row,
-                                 int32_t* tile_edge, uint8_t* spanning) {
+__global__ void k_pr_tile_coords(int32_t n, int32_t m, int32_t ntiles, int32_t tile,
+                                 const int32_t* __restrict__ rev_offsets, int2* coord,
+                                 uint8_t* spanning) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t total = int64_t(n) + m;
-        const int64_t diag = t * kTile < total ? t * kTile : total;
+        const int64_t diag = t * tile < total ? t * tile : total;
         int64_t lo = diag - m > 0 ? diag - m : 0, hi = diag < n ? diag : n;
         while (lo < hi) {
             const int64_t p = (lo + hi) >> 1;
@@ -236,8 +264,7 @@ __global__ void k_pr_tile_coords(int32_t n, int32_t m, int32_t ntiles,
             else
                 hi = p;
         }
-        tile_row[t] = int32_t(lo);
-        tile_edge[t] = int32_t(diag - lo);
+        coord[t] = make_int2(int32_t(lo), int32_t(diag - lo));
         spanning[t] = t > 0 && t < ntiles && lo < n && (diag - lo) > rev_offsets[lo];
     }
 }
@@ -247,39 +274,44 @@ static void build_plan(gdx_graph* g) {
     cudaStream_t s = g->stream;
     const int32_t n = g->n, m = g->m;
     const int64_t total = int64_t(n) + m;
-    const int64_t nt = (total + kTile - 1) / kTile;
+    const char* var = std::getenv("GDX_PR_VARIANT");
+    P.variant = var ? std::atoi(var) : 7;  // 7: 8 items/thread (default), 8: 16
+    P.tile = P.variant == 8 ? kPrBlock * 16 : kTile;
+    const int64_t nt = (total + P.tile - 1) / P.tile;
     if (nt > INT32_MAX) fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph too large for one plan");
     P.ntiles = int32_t(nt);
-    P.tile_row.alloc(nt + 1);
-    P.tile_edge.alloc(nt + 1);
+    P.tile_coord.alloc(nt + 1);
     DevBuf<uint8_t> span(nt + 1);
     k_pr_tile_coords<<<blocks_for(nt + 1, 256, g->num_sms * 8), 256, 0, s>>>(
-        n, m, P.ntiles, g->rev_offsets.get(), P.tile_row.get(), P.tile_edge.get(), span.get());
+        n, m, P.ntiles, P.tile, g->rev_offsets.get(), P.tile_coord.get(), span.get());
     GDX_LAUNCH_CHECK();
-    std::vector<int32_t> row(nt + 1);
+    std::vector<int2> coord(nt + 1);
     std::vector<uint8_t> sp(nt + 1);
-    GDX_CUDA(cudaMemcpyAsync(row.data(), P.tile_row.get(), (nt + 1) * 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(coord.data(), P.tile_coord.get(), (nt + 1) * sizeof(int2),
+                             cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaMemcpyAsync(sp.data(), span.get(), nt + 1, cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
-    // One slot per distinct row crossing >= 1 tile boundary.
-    std::vector<int32_t> first(nt + 1, -1), carry(nt, -1), slot_row;
+    // One slot per distinct row crossing >= 1 tile boundary.  Tile t adds its
+    // first row's partial to slot .x when that row began in an earlier tile,
+    // and its trailing partial row to slot .y when the row continues.
+    std::vector<int32_t> first(nt + 1, -1), slot_row;
     int32_t last_row = -1;
     for (int64_t t = 0; t <= nt; ++t) {
         if (!sp[t]) continue;
-        if (row[t] != last_row) {
-            slot_row.push_back(row[t]);
-            last_row = row[t];
+        if (coord[t].x != last_row) {
+            slot_row.push_back(coord[t].x);
+            last_row = coord[t].x;
         }
         first[t] = int32_t(slot_row.size()) - 1;
     }
-    for (int64_t t = 0; t < nt; ++t) carry[t] = first[t + 1];
+    std::vector<int2> slots(nt);
+    for (int64_t t = 0; t < nt; ++t) slots[t] = make_int2(first[t], first[t + 1]);
     P.nslots = int32_t(slot_row.size());
-    P.tile_first_slot.alloc(nt + 1);
-    P.tile_carry_slot.alloc(nt);
+    P.tile_slots.alloc(nt);
     P.slot_row.alloc(slot_row.size());
     P.slot_acc.alloc(slot_row.size());
-    GDX_CUDA(cudaMemcpyAsync(P.tile_first_slot.get(), first.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, s));
-    GDX_CUDA(cudaMemcpyAsync(P.tile_carry_slot.get(), carry.data(), nt * 4, cudaMemcpyHostToDevice, s));
+    GDX_CUDA(cudaMemcpyAsync(P.tile_slots.get(), slots.data(), nt * sizeof(int2),
+                             cudaMemcpyHostToDevice, s));
     if (!slot_row.empty())
         GDX_CUDA(cudaMemcpyAsync(P.slot_row.get(), slot_row.data(), slot_row.size() * 4,
                                  cudaMemcpyHostToDevice, s));
@@ -290,7 +322,10 @@ static void build_plan(gdx_graph* g) {
     }
     P.dangling.alloc(3);
     int per_sm = 0;
-    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_tiles, kPrBlock, 0));
+    if (P.variant == 8)
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_gather<16, 3>, kPrBlock, 0));
+    else
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_gather<8, 5>, kPrBlock, 0));
     P.grid = std::max(1, per_sm) * g->num_sms;
     GDX_CUDA(cudaStreamSynchronize(s));
 }
@@ -330,10 +365,8 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         a.offsets = g->offsets.get();
         a.rev_offsets = g->rev_offsets.get();
         a.rev_srcs = g->rev_srcs.get();
-        a.tile_row = P.tile_row.get();
-        a.tile_edge = P.tile_edge.get();
-        a.tile_first_slot = P.tile_first_slot.get();
-        a.tile_carry_slot = P.tile_carry_slot.get();
+        a.tile_coord = P.tile_coord.get();
+        a.tile_slots = P.tile_slots.get();
         a.slot_row = P.slot_row.get();
         a.slot_acc = P.slot_acc.get();
         a.rank0 = P.rank[0].get();
@@ -362,7 +395,10 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             const int64_t lim = std::min(r + batch, limit);
             for (int64_t rr = r; rr < lim; ++rr) {
                 timed_launch(g, "pr_tiles", [&] {
-                    k_pr_tiles<<<P.grid, kPrBlock, 0, s>>>(a, int(rr));
+                    if (P.variant == 8)
+                        k_pr_gather<16, 3><<<P.grid, kPrBlock, 0, s>>>(a, int(rr));
+                    else
+                        k_pr_gather<8, 5><<<P.grid, kPrBlock, 0, s>>>(a, int(rr));
                 });
                 if (P.nslots > 0)
                     timed_launch(g, "pr_fixup", [&] {

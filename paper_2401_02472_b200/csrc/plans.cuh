@@ -16,9 +16,8 @@ gdx_graph* make_graph(int device);
 struct PrPlan {
     int32_t ntiles = 0;
     int32_t nslots = 0;
-    DevBuf<int32_t> tile_row, tile_edge;  // ntiles+1 merge-path coordinates
-    DevBuf<int32_t> tile_first_slot;      // slot of the tile's first row if it started earlier, else -1
-    DevBuf<int32_t> tile_carry_slot;      // slot receiving the tile's trailing partial row, else -1
+    DevBuf<int2> tile_coord;              // ntiles+1 merge-path (row, edge) coordinates
+    DevBuf<int2> tile_slots;              // per tile: (first-row slot, carry slot), -1 = none
     DevBuf<int32_t> slot_row;             // row of each spanning slot
     DevBuf<double> slot_acc;              // partial sums per slot (zeroed after use)
     DevBuf<double> rank[2], contrib[2];
@@ -26,6 +25,9 @@ struct PrPlan {
     DevBuf<int32_t> flags;                // per-round "unsettled" votes
     int32_t flags_cap = 0;
     int grid = 0;
+    int variant = 7;
+    int tile = 0;
+    size_t smem = 0;
 };
 
 // SSSP frontier workspace (sssp.cu).
