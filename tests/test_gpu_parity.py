@@ -280,3 +280,16 @@ def test_generators_match_cpu_twin(gdx, port):
     u, v = port.gen_grid_ctr(64, 0.55, 7)
     assert_same_csr(dg.download(), port.build_from_edges(64 * 64, u, v, None, False),
                     ("offsets", "dests", "rev_offsets", "rev_srcs", "rev_eid"))
+
+
+# ---- the C++ drop-in (include/gdx_graphdsl.hpp) against interp::run itself ----------------
+
+def test_cpp_dropin_against_interp(gdx):
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "gdx_dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/gdx_dropin_test not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "DROPIN PASS" in r.stdout, r.stdout + r.stderr
