@@ -24,6 +24,8 @@
 //     Where the reference's sigma is finite the quotients are identical.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "gdx_internal.cuh"
 #include "plans.cuh"
 
@@ -31,8 +33,8 @@ namespace cg = cooperative_groups;
 
 namespace gdx {
 
-constexpr int kBcBlock = 256;
-constexpr int kBcQueue = 4 * kBcBlock;
+// Block size is a template parameter: fewer, fatter blocks make the per-level
+// grid barrier cheaper (BC on high-diameter graphs is barrier-latency bound).
 
 enum { kTail = 0, kLevels = 1, kReached = 2, kFwdScan = 3, kBwdScan = 4, kDag = 5, kBcCtrs = 8 };
 
@@ -57,13 +59,25 @@ struct BcArgs {
 __device__ inline double2 xf_add(double2 a, double2 b) {
     if (a.x == 0.0) return b;
     if (b.x == 0.0) return a;
+    if (a.y == b.y) {  // common case: same binade exponent, exact renormalisation
+        const double s = a.x + b.x;
+        return s < 2.0 ? make_double2(s, a.y) : make_double2(s * 0.5, a.y + 1.0);
+    }
     const double e = fmax(a.y, b.y);
     const double s = ldexp(a.x, int(a.y - e)) + ldexp(b.x, int(b.y - e));
     const int k = ilogb(s);
     return make_double2(ldexp(s, -k), e + k);
 }
 
-__device__ inline double xf_ratio(double2 a, double2 b) { return ldexp(a.x / b.x, int(a.y - b.y)); }
+__device__ inline double xf_ratio(double2 a, double2 b) {
+    const double q = a.x / b.x;
+    return a.y == b.y ? q : ldexp(q, int(a.y - b.y));
+}
+
+// Neighbour lists are walked in chunks of kNb with every load of a chunk issued
+// before any is consumed (dests -> levels -> sigma/delta), so the per-item
+// critical path is a few dependent memory steps instead of one per neighbour.
+constexpr int kNb = 4;
 
 __device__ inline long long ld_volatile_ll(const long long* p) {
     return *reinterpret_cast<const volatile long long*>(p);
@@ -78,7 +92,9 @@ __global__ void k_bc_seed(BcArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.lvl_cnt[0] = a.S;
 }
 
+template <int kBcBlock>
 __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
+    constexpr int kBcQueue = 4 * kBcBlock;
     cg::grid_group grid = cg::this_grid();
     __shared__ uint64_t s_q[kBcQueue];
     __shared__ int s_qn;
@@ -101,32 +117,61 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
                 double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
                 const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
                 fscan += oe - ob;
-                for (int32_t e = ob; e < oe; ++e) {
-                    const int32_t w = a.dests[e];
-                    const int32_t lw = lev[w];
-                    if (a.undirected && L > 0 && lw == L - 1) {
-                        acc = xf_add(acc, a.sig[sb + w]);  // w is a parent of v
-                        ++dag;
-                    } else if (lw == -1 && atomicCAS(&lev[w], -1, L + 1) == -1) {
-                        const uint64_t x = (uint64_t(s) << 32) | uint32_t(w);
-                        const int pos = atomicAdd(&s_qn, 1);
-                        if (pos < kBcQueue) {
-                            s_q[pos] = x;
-                        } else {
-                            const long long p = atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], 1ull);
-                            a.log[end + p] = x;
+                auto push = [&](int32_t w) {
+                    const uint64_t x = (uint64_t(s) << 32) | uint32_t(w);
+                    const int pos = atomicAdd(&s_qn, 1);
+                    if (pos < kBcQueue) {
+                        s_q[pos] = x;
+                    } else {
+                        const long long p = atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], 1ull);
+                        a.log[end + p] = x;
+                    }
+                };
+                for (int32_t e = ob; e < oe; e += kNb) {
+                    int32_t w[kNb], lw[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) lw[k] = w[k] >= 0 ? lev[w[k]] : -2;
+                    double2 sg[kNb];
+                    bool par[kNb], got[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        par[k] = a.undirected && L > 0 && lw[k] == L - 1;
+                        sg[k] = par[k] ? a.sig[sb + w[k]] : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k)
+                        got[k] = lw[k] == -1 && atomicCAS(&lev[w[k]], -1, L + 1) == -1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        if (par[k]) {  // ascending parent order
+                            acc = xf_add(acc, sg[k]);
+                            ++dag;
                         }
+                        if (got[k]) push(w[k]);
                     }
                 }
                 if (!a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
                     fscan += ie - ib;
-                    for (int32_t e = ib; e < ie; ++e) {
-                        const int32_t p = a.in_srcs[e];
-                        if (lev[p] == L - 1) {
-                            acc = xf_add(acc, a.sig[sb + p]);
-                            ++dag;
-                        }
+                    for (int32_t e = ib; e < ie; e += kNb) {
+                        int32_t p[kNb];
+                        bool par[kNb];
+                        double2 sg[kNb];
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k) p[k] = e + k < ie ? a.in_srcs[e + k] : -1;
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k) par[k] = p[k] >= 0 && lev[p[k]] == L - 1;
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            sg[k] = par[k] ? a.sig[sb + p[k]] : make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            if (par[k]) {
+                                acc = xf_add(acc, sg[k]);
+                                ++dag;
+                            }
                     }
                 }
                 a.sig[sb + v] = acc;
@@ -159,6 +204,7 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
     }
 }
 
+template <int kBcBlock>
 __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
@@ -174,19 +220,30 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
             const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
             const int64_t sb = int64_t(s) * a.n;
             const int32_t* lev = a.level + sb;
+            const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
             const double2 sv = a.sig[sb + v];
             double d = 0.0;
-            const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
             bscan += oe - ob;
-            for (int32_t e = ob; e < oe; ++e) {
-                const int32_t w = a.dests[e];
-                if (lev[w] == L + 1) {
-                    const double2 sw = a.sig[sb + w];
-                    if (sw.x > 0.0) {
-                        d += xf_ratio(sv, sw) * (1.0 + a.delta[sb + w]);
+            for (int32_t e = ob; e < oe; e += kNb) {
+                int32_t w[kNb];
+                bool ch[kNb];
+                double2 sw[kNb];
+                double dw[kNb];
+#pragma unroll
+                for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+#pragma unroll
+                for (int k = 0; k < kNb; ++k) ch[k] = w[k] >= 0 && lev[w[k]] == L + 1;
+#pragma unroll
+                for (int k = 0; k < kNb; ++k) {
+                    sw[k] = ch[k] ? a.sig[sb + w[k]] : make_double2(1.0, 0.0);
+                    dw[k] = ch[k] ? a.delta[sb + w[k]] : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < kNb; ++k)
+                    if (ch[k] && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
+                        d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
                         ++dag;
                     }
-                }
             }
             a.delta[sb + v] = d;
             if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
@@ -256,8 +313,19 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             W.sources.ensure(size_t(W.batch));
             if (W.grid == 0) {
                 int a1 = 0, a2 = 0;
-                GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_bc_forward, kBcBlock, 0));
-                GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, k_bc_backward, kBcBlock, 0));
+                const char* bs = std::getenv("GDX_BC_BLOCK");
+                W.block = bs ? std::atoi(bs) : 256;
+                if (W.block != 512 && W.block != 1024) W.block = 256;
+                if (W.block == 256) {
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_bc_forward<256>, 256, 0));
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, k_bc_backward<256>, 256, 0));
+                } else if (W.block == 512) {
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_bc_forward<512>, 512, 0));
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, k_bc_backward<512>, 512, 0));
+                } else {
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_bc_forward<1024>, 1024, 0));
+                    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, k_bc_backward<1024>, 1024, 0));
+                }
                 const int per_sm = std::min(a1, a2);
                 if (per_sm < 1) fail(GDX_ERR_CUDA, "CudaError: bc kernels cannot be resident");
                 W.grid = per_sm * g->num_sms;
@@ -291,12 +359,14 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
                 timed_launch(g, "bc_seed", [&] { k_bc_seed<<<blocks_for(cnt, 256, 1024), 256, 0, s>>>(a); });
                 void* args[] = {&a};
                 timed_launch(g, "bc_forward", [&] {
-                    GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_bc_forward, dim3(W.grid),
-                                                         dim3(kBcBlock), args, 0, s));
+                    void* fn = W.block == 256 ? (void*)k_bc_forward<256>
+                               : W.block == 512 ? (void*)k_bc_forward<512> : (void*)k_bc_forward<1024>;
+                    GDX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(W.grid), dim3(W.block), args, 0, s));
                 });
                 timed_launch(g, "bc_backward", [&] {
-                    GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_bc_backward, dim3(W.grid),
-                                                         dim3(kBcBlock), args, 0, s));
+                    void* fn = W.block == 256 ? (void*)k_bc_backward<256>
+                               : W.block == 512 ? (void*)k_bc_backward<512> : (void*)k_bc_backward<1024>;
+                    GDX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(W.grid), dim3(W.block), args, 0, s));
                 });
                 launches += 3;
                 GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));

@@ -6,18 +6,18 @@
 // in-edge, and a copy-back kernel (tests/golden/pr/cuda/pr_cuda.cu:117-212).
 //
 // Here one round is one merge-path gather over the reverse CSR (k_pr_gather):
-//   * the (rows + in-edges) merge path is cut into fixed tiles of
-//     kPrBlock * ITEMS items -- perfect load balance regardless of the
-//     in-degree skew (RMAT-24: 56% of rows empty, max in-degree 238,735);
+//   * the (rows + in-edges) merge path is cut into fixed tiles of BLOCK * ITEMS
+//     items -- perfect load balance regardless of the in-degree skew
+//     (RMAT-24: 56% of rows empty, max in-degree 238,735);
 //   * per tile the row ends and rev_srcs are staged in shared memory with
 //     coalesced loads; each thread gathers the precomputed
 //     contrib[u] = rank[u] / outdeg(u) of its own segment into registers
 //     (ITEMS independent loads) and reduces it row by row;
-//   * rows are finished where they complete (fused epilogue: new rank,
-//     |change| >= threshold vote, next contrib, next round's dangling mass);
-//     a block-wide reduce-by-key scan carries partial sums across threads and
-//     rows crossing tiles are summed through a compact slot array and
-//     finished by k_pr_fixup;
+//   * a reduce-by-key scan carries partial sums across threads, the fused
+//     epilogue finishes the tile's rows in order (new rank, |change| >=
+//     threshold vote, next contrib, next round's dangling mass), and rows
+//     crossing tiles are summed through a compact slot array and finished by
+//     k_pr_fixup;
 //   * rounds are enqueued in batches without host syncs; a round whose
 //     predecessor voted "settled" exits immediately on the device.
 // Term-wise arithmetic matches pr.sp (contrib is the same f64 quotient the
@@ -32,8 +32,6 @@
 namespace gdx {
 
 constexpr int kPrBlock = 256;
-constexpr int kItems = 8;
-constexpr int kTile = kPrBlock * kItems;  // merge-path items per tile
 
 struct PrArgs {
     int32_t n;
@@ -77,8 +75,9 @@ __device__ inline void pr_epilogue(const PrArgs& a, int round, int32_t v, double
     if (od == 0) dang_local += nr;
 }
 
+template <int BLOCK = kPrBlock>
 __device__ inline void block_flush(const PrArgs& a, int round, double dang_local, int unsettled) {
-    typedef cub::BlockReduce<double, kPrBlock> R;
+    typedef cub::BlockReduce<double, BLOCK> R;
     __shared__ typename R::TempStorage tmp;
     double tot = R(tmp).Sum(dang_local);
     int any = __syncthreads_or(unsettled);
@@ -98,18 +97,19 @@ struct KVOp {
     }
 };
 
-// One PageRank round over tiles of kPrBlock * ITEMS merge-path items.
-// Per tile: row ends and rev_srcs are staged in shared memory (coalesced);
-// each thread locates its merge-path segment, gathers exactly the contrib
-// values of its segment's in-edges into registers (ITEMS independent loads),
-// reduces them row by row and finishes every row it completes on the spot
-// (fused epilogue).  Only the first row a thread completes waits for the block
-// scan that carries partial sums across threads; rows crossing tile
-// boundaries go through slot_acc and k_pr_fixup.
-template <int ITEMS, int MINB>
-__global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int round) {
-    constexpr int TILE = kPrBlock * ITEMS;
-    typedef cub::BlockScan<KV, kPrBlock, cub::BLOCK_SCAN_RAKING> Scan;
+// One PageRank round over tiles of BLOCK * ITEMS merge-path items.  Per tile:
+// row ends and rev_srcs are staged in shared memory (coalesced); each thread
+// locates its merge-path segment, gathers exactly the contrib values of its
+// segment's in-edges into registers (ITEMS independent loads) and reduces them
+// row by row into shared row sums; a block scan carries partial sums across
+// threads; the epilogue then finishes the tile's rows in order (coalesced).
+// Rows crossing tile boundaries go through slot_acc and k_pr_fixup.  Measured
+// on B200 (RMAT-24): one-warp blocks with 6 items/thread are fastest -- the
+// kernel is latency bound and small blocks never wait on a slow warp.
+template <int BLOCK, int ITEMS, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) k_pr_gather(PrArgs a, int round) {
+    constexpr int TILE = BLOCK * ITEMS;
+    typedef cub::BlockScan<KV, BLOCK, cub::BLOCK_SCAN_RAKING> Scan;
     if (round_skipped(a, round)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.dangling[(round + 2) % 3] = 0.0;
     const double dang_in = *reinterpret_cast<const volatile double*>(&a.dangling[round % 3]);
@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int roun
 
     __shared__ int32_t s_end[TILE + 1];
     __shared__ int32_t s_src[TILE];
+    __shared__ double s_sum[TILE];
     __shared__ typename Scan::TempStorage scan_tmp;
     const int tid = threadIdx.x;
     double dang_local = 0.0;
@@ -139,13 +140,13 @@ __global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int roun
         const int2 slots = a.tile_slots[t];
         const int32_t row0 = c0.x, e0 = c0.y;
         const int nrows = c1.x - row0, nedges = c1.y - e0;
-        for (int i = tid; i <= nrows; i += kPrBlock) {
+        for (int i = tid; i <= nrows; i += BLOCK) {
             const int32_t r = row0 + i;
             s_end[i] = r < a.n ? a.rev_offsets[r + 1] - e0 : INT32_MAX;
         }
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
-            const int i = tid + k * kPrBlock;
+            const int i = tid + k * BLOCK;
             if (i < nedges) s_src[i] = a.rev_srcs[e0 + i];
         }
         __syncthreads();
@@ -171,22 +172,11 @@ __global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int roun
             v[k] = ys + k < ye ? __ldg(&contrib[s_src[ys + k]]) : 0.0;
         int x = xs;
         int cur_end = s_end[x];
-        bool first = true;
-        double first_sum = 0.0, run = 0.0;
-        auto finish = [&](int row, double sum) {
-            if (row == 0 && slots.x >= 0)
-                atomicAdd(&a.slot_acc[slots.x], sum);  // row began in an earlier tile
-            else
-                pr_epilogue(a, round, row0 + row, sum, dang_in, rank_in, rank_out, contrib_out,
-                            dang_local, unsettled);
-        };
+        bool completed = false;
+        double run = 0.0;
         auto complete = [&]() {
-            if (first) {
-                first_sum = run;
-                first = false;
-            } else {
-                finish(x, run);
-            }
+            s_sum[x] = run;
+            completed = true;
             run = 0.0;
             ++x;
             cur_end = s_end[x];
@@ -201,16 +191,49 @@ __global__ void __launch_bounds__(kPrBlock, MINB) k_pr_gather(PrArgs a, int roun
         while (x < xe) complete();
         KV carry{x, run}, prefix, agg;
         Scan(scan_tmp).ExclusiveScan(carry, prefix, KVOp(), agg);
-        if (!first) {
-            if (tid > 0 && prefix.key == xs) first_sum += prefix.val;
-            finish(xs, first_sum);
+        if (completed && tid > 0 && prefix.key == xs) s_sum[xs] += prefix.val;
+        __syncthreads();
+        // coalesced epilogue over the tile's completed rows
+        for (int i = tid; i < nrows; i += BLOCK) {
+            const double sum = s_sum[i];
+            if (i == 0 && slots.x >= 0)
+                atomicAdd(&a.slot_acc[slots.x], sum);  // row began in an earlier tile
+            else
+                pr_epilogue(a, round, row0 + i, sum, dang_in, rank_in, rank_out, contrib_out,
+                            dang_local, unsettled);
         }
         if (tid == 0 && slots.y >= 0) atomicAdd(&a.slot_acc[slots.y], agg.val);
         c0 = n0;
         c1 = n1;
         __syncthreads();
     }
-    block_flush(a, round, dang_local, unsettled);
+    block_flush<BLOCK>(a, round, dang_local, unsettled);
+}
+
+// Tile shapes (block threads x items per thread); GDX_PR_VARIANT selects one
+// for A/B runs (tools/pr_variants.py), 40 is the default.
+struct PrVariant {
+    int id, block, items;
+    void* fn;
+};
+static const PrVariant kPrVariants[] = {
+    {40, 32, 6, (void*)k_pr_gather<32, 6, 32>},  // default: one warp per block, 192-item tiles
+    {41, 32, 8, (void*)k_pr_gather<32, 8, 32>},
+    {43, 32, 4, (void*)k_pr_gather<32, 4, 32>},
+    {44, 128, 6, (void*)k_pr_gather<128, 6, 8>},
+};
+static const PrVariant& pr_variant(int id) {
+    for (const auto& v : kPrVariants)
+        if (v.id == id) return v;
+    return kPrVariants[0];
+}
+static int pr_variant_tile(int id) {
+    const PrVariant& v = pr_variant(id);
+    return v.block * v.items;
+}
+static void k_pr_dispatch(int id, int grid, int block, cudaStream_t s, PrArgs& a, int round) {
+    void* args[] = {&a, &round};
+    GDX_CUDA(cudaLaunchKernel(pr_variant(id).fn, dim3(grid), dim3(block), args, 0, s));
 }
 
 // Rows that cross a tile boundary: their partial sums arrived via slot_acc.
@@ -275,8 +298,8 @@ static void build_plan(gdx_graph* g) {
     const int32_t n = g->n, m = g->m;
     const int64_t total = int64_t(n) + m;
     const char* var = std::getenv("GDX_PR_VARIANT");
-    P.variant = var ? std::atoi(var) : 7;  // 7: 8 items/thread (default), 8: 16
-    P.tile = P.variant == 8 ? kPrBlock * 16 : kTile;
+    P.variant = var ? std::atoi(var) : 40;  // see kPrVariants
+    P.tile = pr_variant_tile(P.variant);
     const int64_t nt = (total + P.tile - 1) / P.tile;
     if (nt > INT32_MAX) fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph too large for one plan");
     P.ntiles = int32_t(nt);
@@ -322,10 +345,9 @@ static void build_plan(gdx_graph* g) {
     }
     P.dangling.alloc(3);
     int per_sm = 0;
-    if (P.variant == 8)
-        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_gather<16, 3>, kPrBlock, 0));
-    else
-        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_gather<8, 5>, kPrBlock, 0));
+    const PrVariant& V = pr_variant(P.variant);
+    GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, V.fn, V.block, 0));
+    P.block = V.block;
     P.grid = std::max(1, per_sm) * g->num_sms;
     GDX_CUDA(cudaStreamSynchronize(s));
 }
@@ -395,10 +417,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             const int64_t lim = std::min(r + batch, limit);
             for (int64_t rr = r; rr < lim; ++rr) {
                 timed_launch(g, "pr_tiles", [&] {
-                    if (P.variant == 8)
-                        k_pr_gather<16, 3><<<P.grid, kPrBlock, 0, s>>>(a, int(rr));
-                    else
-                        k_pr_gather<8, 5><<<P.grid, kPrBlock, 0, s>>>(a, int(rr));
+                    k_pr_dispatch(P.variant, P.grid, P.block, s, a, int(rr));
                 });
                 if (P.nslots > 0)
                     timed_launch(g, "pr_fixup", [&] {

@@ -27,6 +27,7 @@ struct PrPlan {
     int grid = 0;
     int variant = 7;
     int tile = 0;
+    int block = 256;
     size_t smem = 0;
 };
 
@@ -36,6 +37,7 @@ struct SsspWork {
     DevBuf<int32_t> stamp;   // round at which a vertex was last enqueued
     DevBuf<int2> queue[2];   // work items (vertex, first edge)
     DevBuf<unsigned long long> ctrs;  // rotating counters + stats
+    DevBuf<unsigned long long> trace; // optional per-round trace (GDX_SSSP_TRACE)
     size_t qcap = 0;
     int grid = 0;
 };
@@ -59,6 +61,7 @@ struct BcWork {
     DevBuf<unsigned long long> ctrs;
     size_t log_cap = 0;
     int grid = 0;
+    int block = 0;
 };
 
 }  // namespace gdx

@@ -21,6 +21,9 @@
 // output is bit-identical to oracles::sssp and to interp::run.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "gdx_internal.cuh"
 #include "plans.cuh"
 
@@ -30,6 +33,7 @@ namespace gdx {
 
 constexpr int kSsspBlock = 256;
 constexpr int kChunk = 32;  // max edges per work item
+constexpr int kSsspQueue = 2048;  // block-local next-frontier staging (int2 items)
 
 // Counter layout in SsspWork::ctrs.
 enum { kQ = 0, kWork = 3, kRounds = 6, kVvis = 7, kEvis = 8, kUpd = 9, kCtrs = 16 };
@@ -45,6 +49,7 @@ struct SsspArgs {
     int2* q0;
     int2* q1;
     unsigned long long* ctr;
+    unsigned long long* trace;  // optional per-round (queue size, globaltimer ns)
 };
 
 __device__ inline unsigned long long ld_volatile(const unsigned long long* p) {
@@ -66,12 +71,16 @@ __global__ void k_sssp_init(SsspArgs<D> a, int32_t src, D inf) {
     }
 }
 
-template <class D>
+template <class D, int kIlp, bool kPre>
 __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const long long nwarps = (long long)gridDim.x * (kSsspBlock / 32);
+    const long long gwarp = ((long long)blockIdx.x * kSsspBlock + threadIdx.x) >> 5;
+    __shared__ int2 s_q[kSsspQueue];
+    __shared__ int s_qn;
+    __shared__ unsigned long long s_gpos;
     unsigned long long vvis = 0, evis = 0, upd = 0;
     int r = 0;
     for (;; ++r) {
@@ -83,15 +92,20 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
             a.ctr[kWork + clr] = 0;
         }
         const unsigned long long qn = ld_volatile(&a.ctr[kQ + cur]);
-        // Items per warp grab: small frontiers spread over all warps.
-        unsigned long long g = qn / (unsigned long long)(nwarps * 4);
-        const int G = g < 1 ? 1 : (g > 32 ? 32 : int(g));
-        while (true) {
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(&a.ctr[kWork + cur], (unsigned long long)G);
-            base = __shfl_sync(full, base, 0);
-            if (base >= qn) break;
-            const int cnt = int(min((unsigned long long)G, qn - base));
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 256) {
+            unsigned long long t;
+            t = clock64();
+            a.trace[2 * r] = qn;
+            a.trace[2 * r + 1] = t;
+        }
+        // Static split of the worklist over warps (no shared work counter: a
+        // single contended atomic per grab serialises at one L2 address).
+        const unsigned long long per = (qn + nwarps - 1) / nwarps;
+        const unsigned long long w0 = gwarp * per, w1 = min(qn, w0 + per);
+        if (threadIdx.x == 0) s_qn = 0;
+        __syncthreads();
+        for (unsigned long long base = w0; base < w1; base += 32) {
+            const int cnt = int(min(32ull, w1 - base));
             int v = 0, b = 0, len = 0;
             D dv = 0;
             if (lane < cnt) {
@@ -113,41 +127,51 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
             const int total = __shfl_sync(full, incl, 31);
             const int excl = incl - len;
             evis += len;
-            for (int j0 = 0; j0 < total; j0 += 32) {
-                const int j = j0 + lane;
-                // owner = largest k with excl_k <= j (items past cnt have excl == total)
-                int k = 0;
+            for (int j0 = 0; j0 < total; j0 += 32 * kIlp) {
+                // kIlp edges per lane, every load of the group issued together
+                int nbr[kIlp];
+                D cand[kIlp], cur_d[kIlp];
 #pragma unroll
-                for (int step = 16; step; step >>= 1) {
-                    int c = k + step;
-                    int ex = __shfl_sync(full, excl, c & 31);
-                    if (c < 32 && ex <= j) k = c;
-                }
-                const int ov = __shfl_sync(full, v, k);
-                const int ob = __shfl_sync(full, b, k);
-                const int oex = __shfl_sync(full, excl, k);
-                const D od = __shfl_sync(full, dv, k);
-                int pitems = 0, pv = 0;
-                if (j < total) {
-                    const int e = ob + (j - oex);
-                    const int nbr = a.dests[e];
-                    const D w = a.weights ? D(a.weights[e]) : D(1);
-                    const D cand = od + w;
-                    if (cand < a.dist[nbr]) {
-                        const D old = atomicMin(&a.dist[nbr], cand);
-                        if (cand < old) {
-                            ++upd;
-                            if (atomicExch(&a.stamp[nbr], r + 1) != r + 1) {
-                                int32_t d = a.offsets[nbr + 1] - a.offsets[nbr];
-                                pitems = (d + kChunk - 1) / kChunk;
-                                pv = nbr;
-                            }
-                        }
+                for (int k = 0; k < kIlp; ++k) {
+                    const int j = j0 + 32 * k + lane;
+                    int o = 0;  // owner = largest lane with excl <= j
+#pragma unroll
+                    for (int step = 16; step; step >>= 1) {
+                        int c = o + step;
+                        int ex = __shfl_sync(full, excl, c & 31);
+                        if (c < 32 && ex <= j) o = c;
                     }
+                    const int ob = __shfl_sync(full, b, o);
+                    const int oex = __shfl_sync(full, excl, o);
+                    const D od = __shfl_sync(full, dv, o);
+                    const int e = ob + (j - oex);
+                    nbr[k] = j < total ? a.dests[e] : -1;
+                    cand[k] = od + (j < total ? (a.weights ? D(a.weights[e]) : D(1)) : D(0));
                 }
-                (void)ov;
-                // warp-aggregated enqueue into the next round's worklist
-                int pincl = pitems;
+#pragma unroll
+                for (int k = 0; k < kIlp; ++k) cur_d[k] = kPre && nbr[k] >= 0 ? a.dist[nbr[k]] : D(0);
+                bool imp[kIlp];
+#pragma unroll
+                for (int k = 0; k < kIlp; ++k) {
+                    imp[k] = false;
+                    if (nbr[k] >= 0 && (!kPre || cand[k] < cur_d[k]))
+                        imp[k] = cand[k] < atomicMin(&a.dist[nbr[k]], cand[k]);
+                }
+                bool fresh[kIlp];
+#pragma unroll
+                for (int k = 0; k < kIlp; ++k) {
+                    upd += imp[k];
+                    fresh[k] = imp[k] && atomicExch(&a.stamp[nbr[k]], r + 1) != r + 1;
+                }
+                int deg[kIlp], mine = 0;
+#pragma unroll
+                for (int k = 0; k < kIlp; ++k) {
+                    deg[k] = fresh[k] ? a.offsets[nbr[k] + 1] - a.offsets[nbr[k]] : 0;
+                    mine += (deg[k] + kChunk - 1) / kChunk;
+                }
+                // warp-aggregated enqueue into the block's shared-memory queue
+                // (one global atomic per block per round; overflow goes direct)
+                int pincl = mine;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     int t = __shfl_up_sync(full, pincl, o);
@@ -155,17 +179,40 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
                 }
                 const int ptotal = __shfl_sync(full, pincl, 31);
                 if (ptotal) {
-                    unsigned long long pbase = 0;
-                    if (lane == 31) pbase = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)ptotal);
-                    pbase = __shfl_sync(full, pbase, 31);
-                    if (pitems) {
-                        const int32_t first = a.offsets[pv];
-                        unsigned long long at = pbase + (pincl - pitems);
-                        for (int t = 0; t < pitems; ++t) QN[at + t] = make_int2(pv, first + t * kChunk);
+                    int sb = 0;
+                    if (lane == 31) sb = atomicAdd(&s_qn, ptotal);
+                    sb = __shfl_sync(full, sb, 31);
+                    // positions >= kSsspQueue overflow straight to the global queue
+                    const int lo = max(sb, kSsspQueue);
+                    const int over = max(0, sb + ptotal - lo);
+                    unsigned long long gb = 0;
+                    if (lane == 31 && over > 0) gb = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)over);
+                    gb = __shfl_sync(full, gb, 31);
+                    int p = sb + (pincl - mine);
+#pragma unroll
+                    for (int k = 0; k < kIlp; ++k) {
+                        if (deg[k] > 0) {
+                            const int32_t first = a.offsets[nbr[k]];
+                            const int items = (deg[k] + kChunk - 1) / kChunk;
+                            for (int t = 0; t < items; ++t, ++p) {
+                                const int2 it = make_int2(nbr[k], first + t * kChunk);
+                                if (p < kSsspQueue)
+                                    s_q[p] = it;
+                                else
+                                    QN[gb + (p - lo)] = it;
+                            }
+                        }
                     }
                 }
             }
         }
+        // flush the block queue (s_qn may exceed the capacity: those went direct)
+        __syncthreads();
+        const int qb = min(s_qn, kSsspQueue);
+        if (threadIdx.x == 0 && qb > 0)
+            s_gpos = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)qb);
+        __syncthreads();
+        for (int i = threadIdx.x; i < qb; i += kSsspBlock) QN[s_gpos + i] = s_q[i];
         grid.sync();
         if (ld_volatile(&a.ctr[kQ + nxt]) == 0) break;
     }
@@ -207,10 +254,22 @@ static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
     a.q0 = w.queue[0].get();
     a.q1 = w.queue[1].get();
     a.ctr = w.ctrs.get();
+    static const bool trace = std::getenv("GDX_SSSP_TRACE") != nullptr;
+    a.trace = nullptr;
+    if (trace) {
+        w.trace.ensure(512);
+        a.trace = w.trace.get();
+    }
     const D inf = ~D(0);
+    const char* var = std::getenv("GDX_SSSP_VARIANT");
+    const int vsel = var ? std::atoi(var) : 0;
+    void* kfn = vsel == 1 ? (void*)k_sssp_rounds<D, 8, true>
+              : vsel == 2 ? (void*)k_sssp_rounds<D, 4, false>
+              : vsel == 3 ? (void*)k_sssp_rounds<D, 8, false>
+                          : (void*)k_sssp_rounds<D, 4, true>;
     if (w.grid == 0) {
         int per_sm = 0;
-        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sssp_rounds<D>, kSsspBlock, 0));
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSsspBlock, 0));
         if (per_sm < 1) fail(GDX_ERR_CUDA, "CudaError: sssp kernel cannot be resident");
         w.grid = per_sm * g->num_sms;
     }
@@ -220,7 +279,7 @@ static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
     });
     timed_launch(g, "sssp_rounds", [&] {
         void* args[] = {&a};
-        GDX_CUDA(cudaLaunchCooperativeKernel((void*)k_sssp_rounds<D>, dim3(w.grid), dim3(kSsspBlock),
+        GDX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(w.grid), dim3(kSsspBlock),
                                              args, 0, s));
     });
     // Widen into the caller's buffer (host or device).  Device output: write in
@@ -237,6 +296,13 @@ static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     GDX_CUDA(cudaMemcpyAsync(h, w.ctrs.get(), kCtrs * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
+    if (trace) {
+        std::vector<unsigned long long> t(512);
+        GDX_CUDA(cudaMemcpy(t.data(), a.trace, 512 * 8, cudaMemcpyDeviceToHost));
+        for (unsigned long long r = 0; r < h[kRounds] && r < 256; ++r)
+            fprintf(stderr, "sssp round %llu: queue %llu items, %.1f kcycles\n", r, t[2 * r],
+                    r + 1 < h[kRounds] ? double(t[2 * r + 3] - t[2 * r + 1]) * 1e-3 : 0.0);
+    }
     if (stats) {
         stats->rounds = int32_t(h[kRounds]);
         stats->launches = 3;

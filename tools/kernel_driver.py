@@ -8,6 +8,7 @@ and calls one entry point `--reps` times (no timing, no oracle).
 import argparse
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -22,17 +23,29 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--bc-sources", type=int, default=64)
     a = ap.parse_args()
+    _orig_generate = gdx.DeviceGraph.generate
+
+    def generate(*args, **kw):  # enable per-kernel event timing on every graph
+        g = _orig_generate(*args, **kw)
+        g.profile(True)
+        graphs.append(g)
+        return g
+
+    graphs = []
+    gdx.DeviceGraph.generate = generate
     if a.algo == "pr":
         g = gdx.DeviceGraph.generate("rmat", 1 << 24, 1 << 28, seed=1, directed=True)
         for _ in range(a.reps):
             print(g.pagerank(0.85, 1e-6, 100)[1])
+        graphs_pr = graphs  # noqa: F841
     elif a.algo == "sssp":
         g = gdx.DeviceGraph.generate("rmat", 1 << 18, 1 << 22, seed=1, directed=False,
                                      weights=(1, 100))
         for _ in range(a.reps):
             st = {}
+            t0 = time.perf_counter()
             g.sssp(0, stats=st)
-            print(st)
+            print(f"{(time.perf_counter() - t0) * 1e3:.3f} ms", st, flush=True)
     elif a.algo == "tc":
         g = gdx.DeviceGraph.generate("uniform", 1 << 24, 1 << 27, seed=1, directed=False)
         for _ in range(a.reps):
@@ -44,8 +57,14 @@ def main():
         src = sorted(np.random.default_rng(1).choice(cand, a.bc_sources, replace=False).tolist())
         for _ in range(a.reps):
             st = {}
+            t0 = time.perf_counter()
             g.bc(src, stats=st)
-            print(st)
+            print(f"{(time.perf_counter() - t0) * 1e3:.1f} ms", st, flush=True)
+
+
+    for g in graphs:
+        for k, (ms, n) in sorted(g.profile_read().items()):
+            print(f"kernel {k}: {ms / max(n, 1):.4f} ms avg over {n} launches")
 
 
 if __name__ == "__main__":
