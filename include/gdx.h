@@ -108,6 +108,15 @@ int gdx_graph_get_stream(gdx_graph* g, void** stream);
 int gdx_graph_build_from_edges(int32_t n, int64_t nedges, const int32_t* u, const int32_t* v,
                                const int32_t* w, int directed, int device, gdx_graph** out);
 
+/* Edge-list files.  Load = CsrGraph::loadEdgeList (csr.cpp:96-130): "u v [w]"
+ * lines, '#' comments, node count inferred as max id + 1 when node_count < 0;
+ * errors "ParseError: malformed edge line in <path>" etc.; built on the GPU.
+ * Write = writeEdgeList (csr.cpp:211-223): "# nodes N stored-edges M" header,
+ * one line per stored edge (directed) or per u <= v pair (undirected). */
+int gdx_graph_load_edge_list(const char* path, int directed, int32_t node_count, int device,
+                             gdx_graph** out);
+int gdx_graph_write_edge_list(gdx_graph* g, const char* path, int with_weights);
+
 /* Counter-based synthetic generators on the GPU.
  * kind: 0 = RMAT (a,b,c; d = 1-a-b-c), 1 = uniform, 2 = 2-D grid (side x side,
  * each lattice edge kept with probability keep).  The edge list is built into

@@ -70,6 +70,9 @@ SIGNATURES = {
     "gdx_graph_get_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "gdx_graph_build_from_edges": ([C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "gdx_graph_load_edge_list": ([C.c_char_p, C.c_int, C.c_int32, C.c_int,
+                                  C.POINTER(C.c_void_p)], C.c_int),
+    "gdx_graph_write_edge_list": ([C.c_void_p, C.c_char_p, C.c_int], C.c_int),
     "gdx_graph_generate": ([C.POINTER(GdxGenParams), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "gdx_graph_set_hash_weights": ([C.c_void_p, C.c_int32, C.c_int32, C.c_uint64], C.c_int),
     "gdx_sssp": ([C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),

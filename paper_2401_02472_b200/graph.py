@@ -125,6 +125,21 @@ class DeviceGraph:
         check(lib.gdx_graph_generate(C.byref(p), device, C.byref(h)))
         return cls(h, device)
 
+    @classmethod
+    def load_edge_list(cls, path: str, directed: bool = True, node_count: Optional[int] = None,
+                       device: int = 0) -> "DeviceGraph":
+        """CsrGraph::loadEdgeList (csr.cpp:96-130), built on the GPU."""
+        h = C.c_void_p()
+        check(_lib.load().gdx_graph_load_edge_list(
+            str(path).encode(), int(bool(directed)), -1 if node_count is None else int(node_count),
+            device, C.byref(h)))
+        return cls(h, device)
+
+    def write_edge_list(self, path: str, with_weights: bool = False) -> None:
+        """writeEdgeList (csr.cpp:211-223)."""
+        check(_lib.load().gdx_graph_write_edge_list(self.handle, str(path).encode(),
+                                                    int(bool(with_weights))))
+
     def set_hash_weights(self, lo: int, hi: int, seed: int) -> None:
         check(_lib.load().gdx_graph_set_hash_weights(self._h, lo, hi, seed))
 
