@@ -168,14 +168,20 @@ def timed_steps(torch, dist, step, steps: int, warmup: int, flush):
 def roofline(prof: dict, kernel: str, algo_bytes: float, pk: dict, work_launches=None) -> dict:
     """achieved = algorithmic bytes / summed device time of `kernel` (CUDA events
     around every launch, recorded by the library on the launching stream).
-    `work_launches` excludes launches that exit immediately (settled PR rounds)."""
-    ms, launches = prof.get(kernel, (0.0, 0))
+    `kernel` may be "a+b": kernels that together make one unit of work (a PR
+    round), timed and counted together.  `work_launches` excludes launches that
+    exit immediately (settled PR rounds)."""
+    parts = kernel.split("+")
+    ms = sum(prof.get(k, (0.0, 0))[0] for k in parts)
+    launches = prof.get(parts[0], (0.0, 0))[1]
     if work_launches:
         launches = work_launches
     achieved = algo_bytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    tr = [ncu_traffic(k) for k in parts]
+    traffic = sum(tr) if all(t is not None for t in tr) else None
     return {"kernel": kernel, "bound": "hbm", "achieved": round(achieved, 1),
             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "peak_source": pk["source"], "traffic": ncu_traffic(kernel),
+            "peak_source": pk["source"], "traffic": traffic,
             "kernel_ms_avg": round(ms / max(launches, 1), 4), "launches": launches,
             "algorithmic_bytes_per_launch": round(algo_bytes / max(launches, 1), 1)}
 
@@ -208,7 +214,7 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
         "workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 tol=1e-6 maxIter=100",
         "n": n, "m": m, "rounds": rounds[-1], "gteps": edges * dist.world / (total_ms * 1e-3) / 1e9,
         "ms_per_step": total_ms / args.steps, "wall_ms": wall,
-        "roofline": roofline(prof, "pr_tiles", sum(rounds) * (12.0 * m + 32.0 * n), pk,
+        "roofline": roofline(prof, "pr_edges+pr_vertices", sum(rounds) * (12.0 * m + 32.0 * n), pk,
                              work_launches=sum(rounds)),
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
@@ -236,7 +242,11 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
     e2e_step()
     dist.barrier(torch)
     t0 = time.perf_counter()
-    rr = [e2e_step() for _ in range(args.steps)]
+    rr = []
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        rr.append(e2e_step())
+        print(f"e2e step {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr)
     e2e_s = dist.max(torch, time.perf_counter() - t0)
     res["e2e"] = {"value": float(m) * sum(rr) * dist.world / e2e_s / 1e9, "unit": "GTEPS",
                   "h2d_bytes_per_step": int(sum(t.numel() * 4 for t in pin.values())),

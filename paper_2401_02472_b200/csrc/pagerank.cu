@@ -5,21 +5,24 @@
 // mass, a thread-per-vertex pull that re-reads the source's out-degree per
 // in-edge, and a copy-back kernel (tests/golden/pr/cuda/pr_cuda.cu:117-212).
 //
-// Here one round is one merge-path gather over the reverse CSR (k_pr_gather):
-//   * the (rows + in-edges) merge path is cut into fixed tiles of BLOCK * ITEMS
-//     items -- perfect load balance regardless of the in-degree skew
-//     (RMAT-24: 56% of rows empty, max in-degree 238,735);
-//   * per tile the row ends and rev_srcs are staged in shared memory with
-//     coalesced loads; each thread gathers the precomputed
-//     contrib[u] = rank[u] / outdeg(u) of its own segment into registers
-//     (ITEMS independent loads) and reduces it row by row;
-//   * a reduce-by-key scan carries partial sums across threads, the fused
-//     epilogue finishes the tile's rows in order (new rank, |change| >=
-//     threshold vote, next contrib, next round's dangling mass), and rows
-//     crossing tiles are summed through a compact slot array and finished by
-//     k_pr_fixup;
+// Here one round is two launches (variant 60, the default):
+//   * k_pr_edges: the reverse-CSR in-edges are cut into aligned groups of 8;
+//     a lane loads its group's rev_srcs with two 16 B vector loads and issues
+//     its 8 contrib[u] = rank[u] / outdeg(u) gathers back to back.  The row
+//     of the group's first edge comes from a precomputed index into the list
+//     of non-empty rows (RMAT-24: 56% of rows are empty), so there is no
+//     merge-path search and no shared memory; rows finish inside a lane, via a
+//     segmented warp-shuffle scan, or (rows spanning warps) by atomicAdd.
+//     Measured on B200 the gather is limited by the L1->L2 miss-request rate
+//     (ncu: l1tex__m_l1tex2xbar_req_cycles_active 87%), so the design keeps
+//     every other L1 request to ~1 per 8 edges;
+//   * k_pr_vertices: pr.sp:17-30 for every vertex with 16 B vector loads and
+//     stores (new rank, |change| >= threshold vote, next contrib, next
+//     round's dangling mass), at HBM speed;
 //   * rounds are enqueued in batches without host syncs; a round whose
 //     predecessor voted "settled" exits immediately on the device.
+// Variants 40-44 keep the earlier single-pass merge-path tile kernel
+// (k_pr_gather + k_pr_fixup) for A/B runs.
 // Term-wise arithmetic matches pr.sp (contrib is the same f64 quotient the
 // interpreter computes per in-edge); only the summation order differs.
 #include <cub/cub.cuh>
@@ -52,6 +55,12 @@ struct PrArgs {
     int32_t* flags;
     double damping, threshold, base, nd;
     int32_t max_iter;
+    // edge-aligned two-pass plan (k_pr_edges + k_pr_vertices)
+    int32_t m, nnz;
+    const int32_t* __restrict__ nz_row;   // vertex of the k-th row with in-edges
+    const int32_t* __restrict__ nz_end;   // rev_offsets[nz_row[k] + 1]
+    const int32_t* __restrict__ grp_row;  // nz row holding edge 8g
+    double* row_sum;                      // per vertex, zero between rounds
 };
 
 
@@ -210,17 +219,204 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_pr_gather(PrArgs a, int round) 
     block_flush<BLOCK>(a, round, dang_local, unsettled);
 }
 
+// ---------------------------------------------------------------------------
+// Edge-aligned two-pass round (variant 60).
+//
+// Pass A (k_pr_edges): the in-edge array is cut into aligned groups of 8; a
+// lane owns one group, loads its 8 rev_srcs with two 16 B vector loads and
+// issues its 8 contrib gathers back to back.  The row of the group's first
+// edge comes from a precomputed per-group index into the list of non-empty
+// rows, so there is no merge-path search and no shared memory at all: the
+// only L1 traffic besides the random gathers is ~1 wavefront per 8 edges.
+// Rows finish inside a lane (plain store of the row sum), across lanes of a
+// warp (segmented shuffle scan), or across warps (atomicAdd of the partial).
+// Pass B (k_pr_vertices) applies pr.sp:17-30 to every vertex with coalesced
+// loads, and clears row_sum for the next round.
+// ---------------------------------------------------------------------------
+constexpr int kEdgeGroup = 8;
+
+// One lane's 8-edge group g (all 32 lanes of the warp call this together
+// for 32 consecutive groups).
+__device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __restrict__ contrib,
+                                              int64_t g) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t e0 = g * kEdgeGroup;
+    const int cnt = e0 < a.m ? int((a.m - e0 < kEdgeGroup ? a.m - e0 : int64_t(kEdgeGroup))) : 0;
+    double v[kEdgeGroup];
+    {
+        const int4* p = reinterpret_cast<const int4*>(a.rev_srcs + (cnt ? e0 : 0));
+        const int4 q0 = __ldcs(p), q1 = __ldcs(p + 1);
+        const int32_t s[kEdgeGroup] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int k = 0; k < kEdgeGroup; ++k) v[k] = k < cnt ? __ldg(&contrib[s[k]]) : 0.0;
+    }
+    int32_t key = cnt ? a.grp_row[g] : INT32_MAX;
+    const int32_t first = key;
+    double run = 0.0, first_val = 0.0;
+    bool first_done = false;
+    if (cnt) {
+        int32_t end = a.nz_end[key];
+#pragma unroll
+        for (int k = 0; k < kEdgeGroup; ++k) {
+            if (k < cnt) {
+                while (end <= e0 + k) {  // row `key` ended before edge e0+k
+                    if (key == first) {
+                        first_val = run;
+                        first_done = true;
+                    } else {
+                        a.row_sum[a.nz_row[key]] = run;
+                    }
+                    run = 0.0;
+                    end = a.nz_end[++key];
+                }
+                run += v[k];
+            }
+        }
+        if (end <= e0 + cnt) {  // the last row ends exactly at the group's end
+            if (key == first) {
+                first_val = run;
+                first_done = true;
+            } else {
+                a.row_sum[a.nz_row[key]] = run;
+            }
+            run = 0.0;
+            ++key;
+        }
+    }
+    // segmented inclusive scan of (row, trailing partial) across the warp
+    double val = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t k2 = __shfl_up_sync(full, key, o);
+        const double v2 = __shfl_up_sync(full, val, o);
+        if (lane >= o && k2 == key) val += v2;
+    }
+    const int32_t pkey = __shfl_up_sync(full, key, 1);
+    const double pval = __shfl_up_sync(full, val, 1);
+    if (first_done) {
+        const double tot = first_val + (lane > 0 && pkey == first ? pval : 0.0);
+        const int64_t warp_e0 = (g & ~int64_t(31)) * kEdgeGroup;
+        const int32_t start = first > 0 ? a.nz_end[first - 1] : 0;
+        const int32_t row = a.nz_row[first];
+        if (start < warp_e0)
+            atomicAdd(&a.row_sum[row], tot);  // row began in an earlier warp's edges
+        else
+            a.row_sum[row] = tot;
+    }
+    // the warp's trailing row continues into the next warp's edges
+    if (lane == 31 && val != 0.0 && key < a.nnz) atomicAdd(&a.row_sum[a.nz_row[key]], val);
+}
+
+__global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
+    if (round_skipped(a, round)) return;
+    const double* __restrict__ contrib = (round & 1) ? a.contrib1 : a.contrib0;
+    pr_edge_group(a, contrib, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+}
+
+// Pass B: two vertices per thread (16 B vector loads/stores), two pairs in
+// flight per iteration.
+__device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, double dang_term,
+                                      const double* __restrict__ rank_in,
+                                      double* __restrict__ rank_out,
+                                      double* __restrict__ contrib_out, double& dang_local,
+                                      int& unsettled) {
+    if (v + 1 < a.n) {
+        const double2 sum = *reinterpret_cast<const double2*>(a.row_sum + v);
+        const double2 ri = *reinterpret_cast<const double2*>(rank_in + v);
+        const int32_t o0 = a.offsets[v], o1 = a.offsets[v + 1], o2 = a.offsets[v + 2];
+        if (sum.x != 0.0 || sum.y != 0.0)
+            *reinterpret_cast<double2*>(a.row_sum + v) = make_double2(0.0, 0.0);
+        const double nr0 = a.base + a.damping * (dang_term + sum.x);
+        const double nr1 = a.base + a.damping * (dang_term + sum.y);
+        double c0 = nr0 - ri.x, c1 = nr1 - ri.y;
+        if (c0 < 0.0) c0 = 0.0 - c0;
+        if (c1 < 0.0) c1 = 0.0 - c1;
+        if ((c0 >= a.threshold || c1 >= a.threshold) && round < a.max_iter) unsettled = 1;
+        *reinterpret_cast<double2*>(rank_out + v) = make_double2(nr0, nr1);
+        const int32_t d0 = o1 - o0, d1 = o2 - o1;
+        *reinterpret_cast<double2*>(contrib_out + v) =
+            make_double2(d0 > 0 ? nr0 / double(d0) : 0.0, d1 > 0 ? nr1 / double(d1) : 0.0);
+        if (d0 == 0) dang_local += nr0;
+        if (d1 == 0) dang_local += nr1;
+    } else if (v < a.n) {
+        const double sum = a.row_sum[v];
+        if (sum != 0.0) a.row_sum[v] = 0.0;
+        const double nr = a.base + a.damping * (dang_term + sum);
+        double c = nr - rank_in[v];
+        if (c < 0.0) c = 0.0 - c;
+        if (c >= a.threshold && round < a.max_iter) unsettled = 1;
+        rank_out[v] = nr;
+        const int32_t d = a.offsets[v + 1] - a.offsets[v];
+        contrib_out[v] = d > 0 ? nr / double(d) : 0.0;
+        if (d == 0) dang_local += nr;
+    }
+}
+
+__global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
+    if (round_skipped(a, round)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.dangling[(round + 2) % 3] = 0.0;
+    const double dang_in = *reinterpret_cast<const volatile double*>(&a.dangling[round % 3]);
+    const double dang_term = dang_in / a.nd;
+    const double* __restrict__ rank_in = (round & 1) ? a.rank1 : a.rank0;
+    double* __restrict__ rank_out = (round & 1) ? a.rank0 : a.rank1;
+    double* __restrict__ contrib_out = (round & 1) ? a.contrib0 : a.contrib1;
+    double dang_local = 0.0;
+    int unsettled = 0;
+    const int64_t stride = (int64_t)gridDim.x * kPrBlock * 2;
+    for (int64_t v = (blockIdx.x * (int64_t)kPrBlock + threadIdx.x) * 2; v < a.n; v += 2 * stride) {
+        pr_vertex_pair(a, round, v, dang_term, rank_in, rank_out, contrib_out, dang_local,
+                       unsettled);
+        pr_vertex_pair(a, round, v + stride, dang_term, rank_in, rank_out, contrib_out, dang_local,
+                       unsettled);
+    }
+    block_flush(a, round, dang_local, unsettled);
+}
+
+// Non-empty rows of the reverse CSR and the row of every 8-edge group.
+__global__ void k_pr_nz_flags(int32_t n, const int32_t* __restrict__ rev_offsets, int32_t* flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        flag[v] = rev_offsets[v + 1] > rev_offsets[v];
+}
+__global__ void k_pr_nz_fill(int32_t n, const int32_t* __restrict__ rev_offsets,
+                             const int32_t* __restrict__ pos, int32_t* nz_row, int32_t* nz_end) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        if (rev_offsets[v + 1] > rev_offsets[v]) {
+            nz_row[pos[v]] = int32_t(v);
+            nz_end[pos[v]] = rev_offsets[v + 1];
+        }
+}
+__global__ void k_pr_grp_rows(int64_t ngroups, int32_t nnz, const int32_t* __restrict__ nz_end,
+                              int32_t* grp_row) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = g * kEdgeGroup;
+        int32_t lo = 0, hi = nnz;  // first k with nz_end[k] > e
+        while (lo < hi) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (nz_end[mid] <= e)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        grp_row[g] = lo;
+    }
+}
+
 // Tile shapes (block threads x items per thread); GDX_PR_VARIANT selects one
-// for A/B runs (tools/pr_variants.py), 40 is the default.
+// for A/B runs (tools/pr_variants.py).  The default, 60, is the edge-aligned
+// two-pass round above; 40-44 are single-pass merge-path tile kernels.
 struct PrVariant {
-    int id, block, items;
+    int id, block, tile;
     void* fn;
 };
 static const PrVariant kPrVariants[] = {
-    {40, 32, 6, (void*)k_pr_gather<32, 6, 32>},  // default: one warp per block, 192-item tiles
-    {41, 32, 8, (void*)k_pr_gather<32, 8, 32>},
-    {43, 32, 4, (void*)k_pr_gather<32, 4, 32>},
-    {44, 128, 6, (void*)k_pr_gather<128, 6, 8>},
+    {40, 32, 192, (void*)k_pr_gather<32, 6, 32>},  // one warp per block, 192-item tiles
+    {41, 32, 256, (void*)k_pr_gather<32, 8, 32>},
+    {43, 32, 128, (void*)k_pr_gather<32, 4, 32>},
+    {44, 128, 768, (void*)k_pr_gather<128, 6, 8>},
 };
 static const PrVariant& pr_variant(int id) {
     for (const auto& v : kPrVariants)
@@ -228,8 +424,7 @@ static const PrVariant& pr_variant(int id) {
     return kPrVariants[0];
 }
 static int pr_variant_tile(int id) {
-    const PrVariant& v = pr_variant(id);
-    return v.block * v.items;
+    return pr_variant(id).tile;
 }
 static void k_pr_dispatch(int id, int grid, int block, cudaStream_t s, PrArgs& a, int round) {
     void* args[] = {&a, &round};
@@ -292,13 +487,56 @@ __global__ void k_pr_tile_coords(int32_t n, int32_t m, int32_t ntiles, int32_t t
     }
 }
 
+static void build_edge_plan(gdx_graph* g) {
+    auto& P = *g->pr;
+    cudaStream_t s = g->stream;
+    const int32_t n = g->n, m = g->m;
+    const int grid = blocks_for(n, 256, g->num_sms * 16);
+    DevBuf<int32_t> flag(n), pos(n);
+    DevBuf<int32_t> cnt(1);
+    k_pr_nz_flags<<<grid, 256, 0, s>>>(n, g->rev_offsets.get(), flag.get());
+    GDX_LAUNCH_CHECK();
+    size_t bytes = 0;
+    GDX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag.get(), pos.get(), n, s));
+    DevBuf<uint8_t> tmp(bytes);
+    GDX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, flag.get(), pos.get(), n, s));
+    int32_t last[2] = {0, 0};
+    if (n > 0) {
+        GDX_CUDA(cudaMemcpyAsync(&last[0], pos.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaMemcpyAsync(&last[1], flag.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    }
+    GDX_CUDA(cudaStreamSynchronize(s));
+    P.nnz = last[0] + last[1];
+    P.nz_row.alloc(size_t(P.nnz) + 1);
+    P.nz_end.alloc(size_t(P.nnz) + 1);
+    k_pr_nz_fill<<<grid, 256, 0, s>>>(n, g->rev_offsets.get(), pos.get(), P.nz_row.get(),
+                                      P.nz_end.get());
+    GDX_LAUNCH_CHECK();
+    const int64_t ngroups = (int64_t(m) + kEdgeGroup - 1) / kEdgeGroup;
+    P.grp_row.alloc(size_t(ngroups) + 1);
+    k_pr_grp_rows<<<blocks_for(ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
+        ngroups, P.nnz, P.nz_end.get(), P.grp_row.get());
+    GDX_LAUNCH_CHECK();
+    P.row_sum.alloc(n);
+    GDX_CUDA(cudaMemsetAsync(P.row_sum.get(), 0, P.row_sum.bytes(), s));
+    for (int i = 0; i < 2; ++i) {
+        P.rank[i].alloc(n);
+        P.contrib[i].alloc(n);
+    }
+    P.dangling.alloc(3);
+    P.block = 256;
+    P.grid = blocks_for(ngroups, 256, INT32_MAX);
+    GDX_CUDA(cudaStreamSynchronize(s));
+}
+
 static void build_plan(gdx_graph* g) {
     auto& P = *g->pr;
     cudaStream_t s = g->stream;
     const int32_t n = g->n, m = g->m;
     const int64_t total = int64_t(n) + m;
     const char* var = std::getenv("GDX_PR_VARIANT");
-    P.variant = var ? std::atoi(var) : 40;  // see kPrVariants
+    P.variant = var ? std::atoi(var) : 60;  // see kPrVariants
+    if (P.variant == 60) return build_edge_plan(g);
     P.tile = pr_variant_tile(P.variant);
     const int64_t nt = (total + P.tile - 1) / P.tile;
     if (nt > INT32_MAX) fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph too large for one plan");
@@ -402,6 +640,12 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         a.nd = double(g->n);
         a.base = (1.0 - damping) / a.nd;
         a.max_iter = max_iter;
+        a.m = g->m;
+        a.nnz = P.nnz;
+        a.nz_row = P.nz_row.get();
+        a.nz_end = P.nz_end.get();
+        a.grp_row = P.grp_row.get();
+        a.row_sum = P.row_sum.get();
 
         GDX_CUDA(cudaMemsetAsync(P.flags.get(), 0, size_t(limit) * 4, s));
         GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
@@ -416,6 +660,18 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         while (rounds < 0) {
             const int64_t lim = std::min(r + batch, limit);
             for (int64_t rr = r; rr < lim; ++rr) {
+                if (P.variant == 60) {
+                    if (g->m > 0)
+                        timed_launch(g, "pr_edges", [&] {
+                            k_pr_edges<<<P.grid, P.block, 0, s>>>(a, int(rr));
+                        });
+                    timed_launch(g, "pr_vertices", [&] {
+                        k_pr_vertices<<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0,
+                                        s>>>(a, int(rr));
+                    });
+                    launches += 1 + (g->m > 0);
+                    continue;
+                }
                 timed_launch(g, "pr_tiles", [&] {
                     k_pr_dispatch(P.variant, P.grid, P.block, s, a, int(rr));
                 });

@@ -23,6 +23,11 @@ struct PrPlan {
     DevBuf<double> rank[2], contrib[2];
     DevBuf<double> dangling;              // 3 rotating accumulators
     DevBuf<int32_t> flags;                // per-round "unsettled" votes
+    // edge-aligned two-pass plan (variant 60)
+    int32_t nnz = 0;
+    DevBuf<int32_t> nz_row, nz_end;       // non-empty rows of the reverse CSR and their ends
+    DevBuf<int32_t> grp_row;              // nz row holding edge 8g
+    DevBuf<double> row_sum;               // per-vertex gather sums (zero between rounds)
     int32_t flags_cap = 0;
     int grid = 0;
     int variant = 7;

@@ -44,11 +44,17 @@ def main():
     src2 = torch.from_numpy(newid[h.rev_srcs].astype(np.int32)).cuda()
     t = timeit(lambda: torch.index_select(contrib, 0, src2, out=out))
     print(f"index_select gather, sources relabelled by out-degree: {t:.3f} ms")
+    c32 = contrib.float()
+    o32 = torch.empty(m, dtype=torch.float32, device="cuda")
+    t = timeit(lambda: torch.index_select(c32, 0, src32, out=o32))
+    print(f"index_select gather of an f32 array (L2-resident 4n bytes): {t:.3f} ms")
+    t = timeit(lambda: torch.index_select(c32, 0, src2, out=o32))
+    print(f"index_select gather f32, relabelled: {t:.3f} ms")
     indeg = np.diff(h.rev_offsets)
     print(f"in-degree: zero={np.mean(indeg == 0):.3f} max={indeg.max()} ; out-degree zero={np.mean(outdeg == 0):.3f} max={outdeg.max()}")
     hot = np.bincount(h.rev_srcs, minlength=n)
     srt = np.sort(hot)[::-1]
-    for k in (1 << 16, 1 << 20, 1 << 22):
+    for k in (1 << 13, 1 << 14, 1 << 15, 1 << 16, 1 << 20, 1 << 22):
         print(f"top {k} sources cover {srt[:k].sum() / m:.3f} of gathers ({k * 8 / 2**20:.0f} MB of contrib)")
 
 

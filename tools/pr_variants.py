@@ -33,12 +33,13 @@ def main():
             r, rounds = g.pagerank(0.85, 1e-6, 100)
         wall = (time.perf_counter() - t0) / a.reps
         prof = g.profile_read()
-        ms, ln = prof["pr_tiles"]
+        ms = sum(v[0] for k, v in prof.items() if k != "pr_init")
         per_round = ms / (rounds * a.reps)
+        parts = " ".join(f"{k}={v[0] / (rounds * a.reps):.3f}" for k, v in prof.items() if k != "pr_init")
         gbs = (12.0 * g.m + 32.0 * g.n) / (per_round * 1e-3) / 1e9
         diff = 0.0 if ref is None else float(np.max(np.abs(r - ref) / np.abs(ref)))
         ref = r if ref is None else ref
-        print(f"variant {v}: rounds={rounds} pr_tiles {per_round:.3f} ms/round "
+        print(f"variant {v}: rounds={rounds} round kernels {per_round:.3f} ms/round [{parts}] "
               f"({gbs:.0f} GB/s algorithmic) wall {wall * 1e3:.1f} ms/run  maxrel vs first {diff:.2e}",
               flush=True)
         g.close()
