@@ -334,8 +334,10 @@ def bench_tc(torch, gdx, dist, args, pk) -> dict:
            "n": dg.n, "m": dg.m, "triangles": counts[-1],
            "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / args.steps,
-           "roofline": roofline(prof, "tc", sum(s["algorithmic_bytes"] for s in sts), pk),
-           "gpu_launches": int(sum(v[1] for v in prof.values()))}
+           "roofline": roofline(prof, "tc+tc_orient+tc_orient_fill",
+                                sum(s["algorithmic_bytes"] for s in sts), pk),
+           "gpu_launches": int(sum(v[1] for v in prof.values())),
+           "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()}}
     dg.close()
     return res
 

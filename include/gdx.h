@@ -149,7 +149,10 @@ int gdx_pagerank(gdx_graph* g, double damping, double threshold, int32_t max_ite
 
 /* ComputeTC: the tc.sp count (== its return value). */
 int gdx_tc(gdx_graph* g, int64_t* count_out, gdx_stats* stats);
-/* Same count restricted to middle vertices v in [v_begin, v_end) (sharding). */
+/* Partial count for sharding: the triangles whose owner vertex lies in
+ * [v_begin, v_end).  The owner is tc.sp's middle vertex on directed graphs and
+ * the smallest vertex on undirected ones (the oriented kernel, tc.cu); ranges
+ * that partition [0, n) sum to gdx_tc either way. */
 int gdx_tc_range(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_out,
                  gdx_stats* stats);
 

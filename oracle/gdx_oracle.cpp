@@ -531,6 +531,51 @@ int orc_tc(const orc_csr* g, int64_t* count, int nthreads) {
     return orc_tc_range(g, 0, g->n, count, nthreads);
 }
 
+// The partial-count contract of gdx_tc_range (include/gdx.h): directed graphs
+// keep tc.sp's middle vertex as the owner (orc_tc_range); on undirected graphs
+// a triangle a < b < c is owned by its smallest vertex a, counted as
+// |N+(a) ∩ N+(b)| with N+(x) = N(x) ∩ (x, inf) -- the GPU's oriented kernel.
+// Over [0, n) both equal orc_tc.
+int orc_tc_range_owner(const orc_csr* g, int32_t v_begin, int32_t v_end, int64_t* count,
+                       int nthreads) {
+    if (g->directed) return orc_tc_range(g, v_begin, v_end, count, nthreads);
+    v_begin = std::max(v_begin, 0);
+    v_end = std::min(v_end, g->n);
+    int T = clamp_threads(nthreads);
+    std::vector<int64_t> part(T, 0);
+    const int32_t* off = g->offsets;
+    const int32_t* dst = g->dests;
+    parallel_for(std::max<int64_t>(0, v_end - v_begin), T, 2048, [&](int t, int64_t b, int64_t e) {
+        int64_t local = 0;
+        for (int64_t i = b; i < e; ++i) {
+            const int32_t a = static_cast<int32_t>(v_begin + i);
+            const int32_t* ae = dst + off[a + 1];
+            for (const int32_t* p = std::upper_bound(dst + off[a], ae, a); p < ae; ++p) {
+                const int32_t bv = *p;  // a < bv
+                const int32_t* x = p + 1;
+                const int32_t* be = dst + off[bv + 1];
+                const int32_t* y = std::upper_bound(dst + off[bv], be, bv);
+                while (x < ae && y < be) {
+                    if (*x < *y)
+                        ++x;
+                    else if (*y < *x)
+                        ++y;
+                    else {
+                        ++local;
+                        ++x;
+                        ++y;
+                    }
+                }
+            }
+        }
+        part[t] += local;
+    });
+    int64_t s = 0;
+    for (int64_t p : part) s += p;
+    *count = s;
+    return 0;
+}
+
 // oracles.cpp:33-71 -- per source: BFS with path counting in queue order, then
 // dependency accumulation in reverse BFS order over children in ascending id
 // order.  Sources run concurrently; their dependency vectors are added into

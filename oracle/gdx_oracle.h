@@ -81,6 +81,8 @@ int orc_pr_rounds(const orc_csr* g, double damping, int32_t rounds, double* rank
 int orc_tc(const orc_csr* g, int64_t* count, int nthreads);
 /* Middle vertices restricted to [v_begin, v_end) -- for sharded checks. */
 int orc_tc_range(const orc_csr* g, int32_t v_begin, int32_t v_end, int64_t* count, int nthreads);
+int orc_tc_range_owner(const orc_csr* g, int32_t v_begin, int32_t v_end, int64_t* count,
+                       int nthreads);
 /* Brandes over a source set, oracles.cpp:33-71, with sigma carried as
  * (double mantissa, int exponent) so it never overflows.  Bit-identical to
  * oracles::bc wherever the reference's double sigma stays finite. */

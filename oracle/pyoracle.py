@@ -115,6 +115,7 @@ class Port:
         L.orc_pr_rounds.argtypes = [C.POINTER(_Csr), C.c_double, C.c_int32, _f64p, C.c_int]
         L.orc_tc.argtypes = [C.POINTER(_Csr), _i64p, C.c_int]
         L.orc_tc_range.argtypes = [C.POINTER(_Csr), C.c_int32, C.c_int32, _i64p, C.c_int]
+        L.orc_tc_range_owner.argtypes = [C.POINTER(_Csr), C.c_int32, C.c_int32, _i64p, C.c_int]
         L.orc_bc.argtypes = [C.POINTER(_Csr), _i32p, C.c_int32, _f64p, C.c_int]
         L.orc_bfs_levels.argtypes = [C.POINTER(_Csr), C.c_int32, _i32p]
 
@@ -215,6 +216,14 @@ class Port:
         return out.value
 
     def tc_range(self, g, v0, v1, threads=0) -> int:
+        """gdx_tc_range's partial count (owner: middle vertex if directed, smallest if not)."""
+        c, keep = _csr_of(g)
+        out = C.c_int64(0)
+        self._check(self.lib.orc_tc_range_owner(C.byref(c), v0, v1, C.byref(out), threads))
+        return out.value
+
+    def tc_range_middle(self, g, v0, v1, threads=0) -> int:
+        """tc.sp's middle-vertex partial count (any graph)."""
         c, keep = _csr_of(g)
         out = C.c_int64(0)
         self._check(self.lib.orc_tc_range(C.byref(c), v0, v1, C.byref(out), threads))

@@ -14,6 +14,10 @@
 // the warp); each lane intersects with a linear merge, or with galloping
 // binary searches when the two lists are very unequal (hub lists).  Counts are
 // warp-reduced and added with one 64-bit atomic per warp.
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+
 #include "gdx_internal.cuh"
 #include "plans.cuh"
 
@@ -148,6 +152,225 @@ __global__ void __launch_bounds__(kTcBlock) k_tc(int32_t v_begin, int32_t v_end,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Undirected graphs: oriented counting.  On a symmetric graph tc.sp's count
+// (u < v < w, v the middle vertex) is the number of triangles, which is also
+//     sum over v, sum over u in N+(v):  |N+(v) ∩ N+(u)|,   N+(x) = N(x) ∩ (x, inf)
+// (each triangle a < b < c is found once, at v = a, u = b, w = c).  This needs
+// no binary search in the random list N+(u) and only half the adjacency.
+//
+// k_tc_orient_count / k_tc_orient_fill build the oriented CSR (off+, adj+)
+// inside the call.  k_tc_oriented: a warp owns 32 consecutive vertices; their
+// N+ lists are one contiguous range of adj+, staged into the warp's shared
+// memory with coalesced loads.  The (v, u) pairs of the 32 lists are spread
+// over the lanes; a lane loads N+(u) with 16 B vector loads (one L1 wavefront
+// per 4 elements -- the gather is the kernel's bound) and merges it against
+// the tail of N+(v) after u in shared memory.  One 64-bit atomic per warp.
+// ---------------------------------------------------------------------------
+__global__ void k_tc_orient_count(int32_t n, const int32_t* __restrict__ offsets,
+                                  const int32_t* __restrict__ dests, int32_t* cnt,
+                                  int32_t* hs) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = offsets[v], e = offsets[v + 1];
+        const int32_t h = upper_bound_dev(dests, b, e, int32_t(v));
+        hs[v] = h;
+        cnt[v] = e - h;
+    }
+}
+
+__global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
+                                 const int32_t* __restrict__ hs,
+                                 const int32_t* __restrict__ off_plus, int32_t* adj_plus) {
+    // A warp fills the contiguous adj+ range of 32 consecutive vertices with
+    // coalesced stores; the source row of each output slot is found by a
+    // shuffle binary search over the 32 list starts.
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v0 = w * 32; v0 < n; v0 += nw * 32) {
+        const int64_t v = v0 + lane;
+        const int32_t src = v < n ? hs[v] : 0;
+        const int32_t dst = v < n ? off_plus[v] : INT32_MAX;
+        const int32_t d0 = __shfl_sync(full, dst, 0);
+        const int32_t d1 = v0 + 32 <= n ? off_plus[v0 + 32] : off_plus[n];
+        for (int32_t d = d0 + lane; d - lane < d1; d += 32) {
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int c = k + step;
+                const int32_t st = __shfl_sync(full, dst, c & 31);
+                if (c < 32 && st <= d) k = c;
+            }
+            const int32_t ks = __shfl_sync(full, src, k);
+            const int32_t kd = __shfl_sync(full, dst, k);
+            if (d < d1) adj_plus[d] = dests[ks + (d - kd)];
+        }
+    }
+}
+
+constexpr int kTcStage = 1024;  // ints of staged N+ lists per warp
+
+__global__ void __launch_bounds__(kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
+                                                          const int32_t* __restrict__ off_plus,
+                                                          const int32_t* __restrict__ adj,
+                                                          unsigned long long* acc) {
+    const unsigned full = 0xffffffffu;
+    __shared__ int32_t stage[kTcBlock / 32][kTcStage];
+    const int lane = threadIdx.x & 31;
+    int32_t* sA = stage[threadIdx.x >> 5];
+    const int64_t gwarp = (blockIdx.x * (int64_t)kTcBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * (kTcBlock / 32);
+    const int4* adj4 = reinterpret_cast<const int4*>(adj);
+    unsigned long long count = 0, scanned = 0;
+    for (int64_t v0 = v_begin + gwarp * 32; v0 < v_end; v0 += nwarps * 32) {
+        const int32_t v = int32_t(v0) + lane;
+        const bool valid = v < v_end;
+        const int32_t ob = valid ? off_plus[v] : 0;
+        const int32_t oe = valid ? off_plus[v + 1] : 0;
+        const int32_t r0 = __shfl_sync(full, ob, 0);
+        int32_t last_end = oe;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) last_end = max(last_end, __shfl_xor_sync(full, last_end, o));
+        const int32_t rlen = last_end - r0;
+        // stage the warp's lists (one contiguous range of adj+) when they fit
+        const bool staged = rlen <= kTcStage;
+        if (staged)
+            for (int32_t i = lane; i < rlen; i += 32) sA[i] = adj[r0 + i];
+        __syncwarp();
+        const int32_t* A = staged ? sA - r0 : adj;  // A[x] for x in [r0, last_end)
+        // pairs (v, i): u = N+(v)[i] for i < len-1 (the last u has no tail)
+        const int32_t np = max(oe - ob - 1, 0);
+        int incl = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(full, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(full, incl, 31);
+        const int excl = incl - np;
+        // The off+ range of the next pair's u is loaded while the current
+        // pair merges; the current pair's first three 16 B words of N+(u)
+        // are issued together (one L1 wavefront per 4 elements).
+        auto locate = [&](int j, int32_t& pu, int32_t& koe) {
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int c = k + step;
+                const int ex = __shfl_sync(full, excl, c & 31);
+                if (c < 32 && ex <= j) k = c;
+            }
+            const int32_t kob = __shfl_sync(full, ob, k);
+            koe = __shfl_sync(full, oe, k);
+            pu = kob + (j - __shfl_sync(full, excl, k));
+        };
+        int32_t pu = 0, koe = 0, bb = 0, be = 0;
+        locate(lane, pu, koe);
+        if (lane < total) {
+            const int32_t u = A[pu];
+            bb = off_plus[u];
+            be = off_plus[u + 1];
+        }
+        for (int j0 = 0; j0 < total; j0 += 32) {
+            const bool have = j0 + lane < total;
+            const int32_t cpu = pu, ckoe = koe, cbb = bb, cbe = be;
+            locate(j0 + 32 + lane, pu, koe);
+            if (j0 + 32 + lane < total) {
+                const int32_t u = A[pu];
+                bb = off_plus[u];
+                be = off_plus[u + 1];
+            }
+            if (!have || cbb >= cbe) continue;
+            const int32_t q0 = cbb & ~3;
+            int4 w[3];
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                w[t] = q0 + 4 * t < cbe ? adj4[(q0 >> 2) + t]
+                                        : make_int4(INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX);
+            int32_t p = cpu + 1;  // tail of N+(v) after u: A[p .. ckoe)
+            int32_t ap = A[p];
+            const int32_t a_last = A[ckoe - 1];
+            scanned += (ckoe - p) + (cbe - cbb) + 2;
+            unsigned long long c = 0;
+            bool done = false;
+#pragma unroll
+            for (int t = 0; t < 12; ++t) {
+                const int32_t idx = q0 + t;
+                const int32_t xv = (&w[t >> 2].x)[t & 3];
+                if (!done && idx >= cbb && idx < cbe) {
+                    while (ap < xv && ++p < ckoe) ap = A[p];
+                    if (p >= ckoe || xv > a_last)
+                        done = true;
+                    else if (ap == xv)
+                        ++c;
+                }
+            }
+            for (int32_t q = q0 + 12; !done && q < cbe; q += 4) {  // long lists
+                const int4 w4 = adj4[q >> 2];
+                const int32_t x[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (!done && q + t < cbe) {
+                        const int32_t xv = x[t];
+                        while (ap < xv && ++p < ckoe) ap = A[p];
+                        if (p >= ckoe || xv > a_last)
+                            done = true;
+                        else if (ap == xv)
+                            ++c;
+                    }
+                }
+            }
+            count += c;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        count += __shfl_xor_sync(full, count, o);
+        scanned += __shfl_xor_sync(full, scanned, o);
+    }
+    if (lane == 0) {
+        if (count) atomicAdd(&acc[0], count);
+        if (scanned) atomicAdd(&acc[1], scanned);
+    }
+}
+
+static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_stats* stats) {
+    cudaStream_t s = g->stream;
+    auto& P = *g->tc;
+    const int32_t n = g->n;
+    P.off_plus.ensure(size_t(n) + 1);
+    P.hi_start.ensure(size_t(n) + 1);
+    P.adj_plus.ensure(size_t(g->m) / 2 + size_t(n) + 8);
+    const int grid_v = blocks_for(n, 256, g->num_sms * 16);
+    timed_launch(g, "tc_orient", [&] {
+        k_tc_orient_count<<<grid_v, 256, 0, s>>>(n, g->offsets.get(), g->dests.get(),
+                                                 P.off_plus.get(), P.hi_start.get());
+    });
+    size_t bytes = 0;
+    GDX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, P.off_plus.get(), P.off_plus.get(),
+                                           n + 1, s));
+    P.scan_tmp.ensure(bytes);
+    // exclusive scan over n+1 entries: off_plus[n] = total (the count slot n is zeroed)
+    GDX_CUDA(cudaMemsetAsync(P.off_plus.get() + n, 0, 4, s));
+    GDX_CUDA(cub::DeviceScan::ExclusiveSum(P.scan_tmp.get(), bytes, P.off_plus.get(),
+                                           P.off_plus.get(), n + 1, s));
+    timed_launch(g, "tc_orient_fill", [&] {
+        k_tc_orient_fill<<<grid_v, 256, 0, s>>>(n, g->dests.get(), P.hi_start.get(),
+                                                P.off_plus.get(), P.adj_plus.get());
+    });
+    if (v_end > v_begin) {
+        const int64_t groups = (int64_t(v_end) - v_begin + 31) / 32;
+        const int grid = blocks_for(groups * 32, kTcBlock, g->num_sms * 16);
+        timed_launch(g, "tc", [&] {
+            k_tc_oriented<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, P.off_plus.get(),
+                                                    P.adj_plus.get(), P.acc.get());
+        });
+    }
+    if (stats) stats->launches = 2 + (v_end > v_begin);
+}
+
 static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_out,
                    gdx_stats* stats) {
     if (!g->dests.get() && g->m > 0)
@@ -160,7 +383,10 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
     GDX_CUDA(cudaMemsetAsync(P.acc.get(), 0, 2 * sizeof(unsigned long long), s));
     v_begin = std::max(v_begin, 0);
     v_end = std::min(v_end, g->n);
-    if (v_end > v_begin) {
+    const bool oriented = !g->directed && std::getenv("GDX_TC_MIDDLE") == nullptr;
+    if (oriented) {
+        run_tc_oriented(g, v_begin, v_end, stats);
+    } else if (v_end > v_begin) {
         const int64_t groups = (int64_t(v_end) - v_begin + 31) / 32;
         const int grid = blocks_for(groups * 32, kTcBlock, g->num_sms * 16);
         timed_launch(g, "tc", [&] {
@@ -174,14 +400,22 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
     *count_out = int64_t(h[0]);
     if (stats) {
         stats->rounds = 1;
-        stats->launches = v_end > v_begin ? 1 : 0;
+        if (!oriented) stats->launches = v_end > v_begin ? 1 : 0;
         stats->vertices_visited = int64_t(v_end) - v_begin;
         stats->edges_visited = int64_t(h[1]);
         stats->updates = int64_t(h[0]);
-        // offsets 4(n+1) + adjacency scan 4m + 4 per
-        // element of every intersected list.
+        // DESIGN.md "TC bytes".  Middle-vertex kernel: offsets 4(n+1) +
+        // adjacency scan 4m + 4 per element of every intersected list.
+        // Oriented kernel: orientation (offsets 4(n+1) read, dests 4m read,
+        // adj+ 2m + off+ 4(n+1) written) + N+ staging 2m + per pair the off+
+        // pair of u (8) and 4 per element of both merged lists.
         const double frac = g->n ? double(int64_t(v_end) - v_begin) / g->n : 0.0;
-        stats->algorithmic_bytes = frac * (4.0 * (g->n + 1) + 4.0 * g->m) + 4.0 * double(h[1]);
+        if (oriented)
+            stats->algorithmic_bytes = 8.0 * (g->n + 1) + 6.0 * g->m + frac * 2.0 * g->m +
+                                       4.0 * double(h[1]);
+        else
+            stats->algorithmic_bytes =
+                frac * (4.0 * (g->n + 1) + 4.0 * g->m) + 4.0 * double(h[1]);
     }
 }
 

@@ -45,8 +45,8 @@ def balanced_ranges(weights: np.ndarray, parts: int) -> list[tuple[int, int]]:
 
 
 def tc_ranges(offsets: np.ndarray, parts: int) -> list[tuple[int, int]]:
-    """Middle-vertex ranges for TC balanced by work ~ deg(v)^2 / 2 + deg(v)
-    (each of the ~deg/2 lower neighbours intersects two ~deg/2 lists)."""
+    """Owner-vertex ranges for TC (gdx_tc_range) balanced by work ~ deg(v)^2 / 2 +
+    deg(v) (each of ~deg/2 neighbours on one side intersects two ~deg/2 lists)."""
     deg = np.diff(np.asarray(offsets, dtype=np.int64)).astype(np.float64)
     return balanced_ranges(deg * deg / 2.0 + deg + 1.0, parts)
 
