@@ -193,9 +193,10 @@ int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* 
         if (weights) {
             if (g->weighted)
                 copy_out(g, weights, g->weights.get(), mb);
-            else {
+            else {  // unweighted: every weight is 1 (host or device destination)
+                std::vector<int32_t> ones(size_t(g->m), 1);
+                GDX_CUDA(cudaMemcpyAsync(weights, ones.data(), mb, cudaMemcpyDefault, g->stream));
                 GDX_CUDA(cudaStreamSynchronize(g->stream));
-                for (int32_t i = 0; i < g->m; ++i) weights[i] = 1;
             }
         }
         need(rev_offsets, g->rev_offsets, nb, "rev_offsets");

@@ -152,6 +152,19 @@ class DeviceGraph:
                                               "rev_srcs", "rev_eid")]))
         return HostCsr(n, m, self.directed, **a)
 
+    def device_arrays(self, names: Sequence[str]):
+        """Device (torch, int32) copies of the named CSR arrays, for on-device
+        checks at sizes where a host copy is impractical."""
+        import torch
+        n, m = self.n, self.m
+        order = ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")
+        out = {k: torch.empty(n + 1 if "offsets" in k else m, dtype=torch.int32,
+                              device=f"cuda:{self.device}") for k in names}
+        ptrs = [_ptr(out[k]) if k in out else None for k in order]
+        check(_lib.load().gdx_graph_download(self._h, *ptrs))
+        torch.cuda.synchronize(self.device)
+        return [out[k] for k in names]
+
     # ---- lifetime / streams ---------------------------------------------------
     def close(self) -> None:
         if self._h:
