@@ -15,8 +15,8 @@
 //     warp-aggregated atomicAdd on the next queue's tail;
 //   * rounds are separated by grid.sync(); the convergence test is "next
 //     queue empty" read on the device -- no host round trip per round.
-// Distances are 32-bit when n * max_weight fits (exact), else 64-bit; the
-// result is widened to int64 with INF = INT64_MAX/2 (oracles.hpp:12).  Any
+// Distances are 32-bit; a relaxation that would overflow them sets a flag and
+// the call reruns with 64-bit distances (exact either way); the result is widened to int64 with INF = INT64_MAX/2 (oracles.hpp:12).  Any
 // correct relaxation order yields the unique shortest-path distances, so the
 // output is bit-identical to oracles::sssp and to interp::run.
 #include <cooperative_groups.h>
@@ -36,7 +36,8 @@ constexpr int kChunk = 32;  // max edges per work item
 constexpr int kSsspQueue = 2048;  // block-local next-frontier staging (int2 items)
 
 // Counter layout in SsspWork::ctrs.
-enum { kQ = 0, kWork = 3, kRounds = 6, kVvis = 7, kEvis = 8, kUpd = 9, kCtrs = 16 };
+enum { kQ = 0, kWork = 3, kRounds = 6, kVvis = 7, kEvis = 8, kUpd = 9, kOvf = 10, kCtrs = 16 };
+constexpr int kWarpChunk = 256;  // queue items a warp reserves once its block's staging is full
 
 template <class D>
 struct SsspArgs {
@@ -50,6 +51,7 @@ struct SsspArgs {
     int2* q1;
     unsigned long long* ctr;
     unsigned long long* trace;  // optional per-round (queue size, globaltimer ns)
+    int stage_cap;              // block staging capacity (<= kSsspQueue; 0 in tests)
 };
 
 __device__ inline unsigned long long ld_volatile(const unsigned long long* p) {
@@ -82,6 +84,8 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
     __shared__ int s_qn;
     __shared__ unsigned long long s_gpos;
     unsigned long long vvis = 0, evis = 0, upd = 0;
+    unsigned long long wq_base = 0;  // this warp's overflow chunk in the next queue
+    int wq_left = 0;
     int r = 0;
     for (;; ++r) {
         const int cur = r % 3, nxt = (r + 1) % 3, clr = (r + 2) % 3;
@@ -112,11 +116,13 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
                 int2 it = Q[base + lane];
                 v = it.x;
                 b = it.y;
-                int32_t vb = a.offsets[v], ve = a.offsets[v + 1];
-                int32_t e = min(b + kChunk, ve);
-                len = e - b;
-                dv = a.dist[v];
-                vvis += (b == vb);
+                if (v >= 0) {  // v < 0: padding of a partly used warp chunk
+                    int32_t vb = a.offsets[v], ve = a.offsets[v + 1];
+                    int32_t e = min(b + kChunk, ve);
+                    len = e - b;
+                    dv = a.dist[v];
+                    vvis += (b == vb);
+                }
             }
             int incl = len;
 #pragma unroll
@@ -146,7 +152,14 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
                     const D od = __shfl_sync(full, dv, o);
                     const int e = ob + (j - oex);
                     nbr[k] = j < total ? a.dests[e] : -1;
-                    cand[k] = od + (j < total ? (a.weights ? D(a.weights[e]) : D(1)) : D(0));
+                    const D wt = j < total ? (a.weights ? D(a.weights[e]) : D(1)) : D(0);
+                    cand[k] = od + wt;
+                    if (sizeof(D) == 4 && j < total && od > D(0xFFFFFFFEu) - wt) {
+                        // 32-bit distances would overflow: flag it (the host
+                        // reruns with 64-bit distances) and drop the edge
+                        a.ctr[kOvf] = 1;
+                        nbr[k] = -1;
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < kIlp; ++k) cur_d[k] = kPre && nbr[k] >= 0 ? a.dist[nbr[k]] : D(0);
@@ -182,12 +195,19 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
                     int sb = 0;
                     if (lane == 31) sb = atomicAdd(&s_qn, ptotal);
                     sb = __shfl_sync(full, sb, 31);
-                    // positions >= kSsspQueue overflow straight to the global queue
-                    const int lo = max(sb, kSsspQueue);
+                    // positions >= kSsspQueue overflow into this warp's chunk of
+                    // the global queue (one global atomic per kWarpChunk items)
+                    const int lo = max(sb, a.stage_cap);
                     const int over = max(0, sb + ptotal - lo);
-                    unsigned long long gb = 0;
-                    if (lane == 31 && over > 0) gb = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)over);
-                    gb = __shfl_sync(full, gb, 31);
+                    if (over > wq_left) {
+                        // pad the rest of the old chunk, reserve a new one
+                        for (int t = lane; t < wq_left; t += 32) QN[wq_base + t] = make_int2(-1, 0);
+                        const int want = max(over, kWarpChunk);
+                        unsigned long long gb = 0;
+                        if (lane == 0) gb = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)want);
+                        wq_base = __shfl_sync(full, gb, 0);
+                        wq_left = want;
+                    }
                     int p = sb + (pincl - mine);
 #pragma unroll
                     for (int k = 0; k < kIlp; ++k) {
@@ -196,19 +216,24 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
                             const int items = (deg[k] + kChunk - 1) / kChunk;
                             for (int t = 0; t < items; ++t, ++p) {
                                 const int2 it = make_int2(nbr[k], first + t * kChunk);
-                                if (p < kSsspQueue)
+                                if (p < a.stage_cap)
                                     s_q[p] = it;
                                 else
-                                    QN[gb + (p - lo)] = it;
+                                    QN[wq_base + (p - lo)] = it;
                             }
                         }
                     }
+                    wq_base += over;
+                    wq_left -= over;
                 }
             }
         }
+        // pad this warp's partly used chunk
+        for (int t = lane; t < wq_left; t += 32) QN[wq_base + t] = make_int2(-1, 0);
+        wq_left = 0;
         // flush the block queue (s_qn may exceed the capacity: those went direct)
         __syncthreads();
-        const int qb = min(s_qn, kSsspQueue);
+        const int qb = min(s_qn, a.stage_cap);
         if (threadIdx.x == 0 && qb > 0)
             s_gpos = atomicAdd(&a.ctr[kQ + nxt], (unsigned long long)qb);
         __syncthreads();
@@ -240,8 +265,9 @@ __global__ void k_sssp_widen(int32_t n, const D* __restrict__ dist, D inf, int64
     }
 }
 
+// Returns true when 32-bit distances overflowed (the caller reruns with 64).
 template <class D>
-static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
     auto& w = *g->sssp;
     cudaStream_t s = g->stream;
     SsspArgs<D> a;
@@ -260,6 +286,10 @@ static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
         w.trace.ensure(512);
         a.trace = w.trace.get();
     }
+    // GDX_SSSP_STAGE (tests): block staging capacity, 0 = every push takes
+    // the warp-chunk path of large frontiers
+    const char* stage = std::getenv("GDX_SSSP_STAGE");
+    a.stage_cap = stage ? std::max(0, std::min(kSsspQueue, std::atoi(stage))) : kSsspQueue;
     const D inf = ~D(0);
     const char* var = std::getenv("GDX_SSSP_VARIANT");
     const int vsel = var ? std::atoi(var) : 0;
@@ -315,6 +345,7 @@ static void run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
         stats->algorithmic_bytes = (16.0 + sd) * h[kVvis] + (4.0 + sw + sd) * h[kEvis] +
                                    (12.0 + sd) * h[kUpd];
     }
+    return h[kOvf] != 0;
 }
 
 }  // namespace gdx
@@ -333,18 +364,20 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         DeviceGuard dg(g->device);
         if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
         auto& w = *g->sssp;
-        // every vertex enters a round's queue at most once: <= n + m/kChunk items
-        const size_t qcap = size_t(g->n) + size_t(g->m) / kChunk + 1;
+        // every vertex enters a round's queue at most once: <= n + m/kChunk
+        // items; warp overflow chunks at most double that, plus the padding of
+        // the last chunk of every warp
+        const size_t qcap = 2 * (size_t(g->n) + size_t(g->m) / kChunk + 1) +
+                            size_t(kWarpChunk) * 64 * size_t(g->num_sms);
         w.dist.ensure(size_t(g->n));
         w.stamp.ensure(size_t(g->n));
         // queue[1] doubles as the int64 staging buffer for host outputs
         w.queue[0].ensure(qcap);
         w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
         w.ctrs.ensure(kCtrs);
-        const bool narrow = int64_t(g->max_weight) * int64_t(g->n) < int64_t(0xFFFFFFFEll);
-        if (narrow)
-            run_sssp<unsigned int>(g, src, dist_out, stats);
-        else
-            run_sssp<unsigned long long>(g, src, dist_out, stats);
+        // 32-bit distances unless a relaxation overflows them (then 64-bit):
+        // the result is exact either way.
+        const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
+        if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
     });
 }

@@ -293,3 +293,16 @@ def test_cpp_dropin_against_interp(gdx):
         pytest.skip("oracle/_ref/gdx_dropin_test not built (needs /root/reference at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "DROPIN PASS" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("stage", ["0", "7"])
+def test_sssp_warp_chunk_queue(gdx, port, stage, monkeypatch):
+    """Large frontiers overflow the block staging into per-warp chunks of the
+    global queue (padded with sentinel items); force that path on C1-sized
+    graphs (GDX_SSSP_STAGE caps the staging) and check bit-exactness."""
+    monkeypatch.setenv("GDX_SSSP_STAGE", stage)
+    u, v = port.gen_rmat_edges(1 << 16, 1 << 20, 5)
+    g = port.with_random_weights(port.build_from_edges(1 << 16, u, v, None, False), 1, 100, 5)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 999):
+        assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
