@@ -96,7 +96,8 @@ int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* 
                        int32_t* rev_offsets, int32_t* rev_srcs, int32_t* rev_eid);
 /* The CUDA stream (cudaStream_t) all kernels of this handle run on.  Setting
  * it to a caller stream (e.g. torch.cuda.current_stream()) orders the calls
- * with the caller's work; NULL restores the handle's own stream. */
+ * with the caller's work; NULL restores the handle's own (non-blocking)
+ * stream; cudaStreamLegacy ((void*)1) selects the legacy default stream. */
 int gdx_graph_set_stream(gdx_graph* g, void* stream);
 int gdx_graph_get_stream(gdx_graph* g, void** stream);
 
@@ -159,6 +160,37 @@ int gdx_tc_range(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_ou
 /* ComputeBC: bc_out[n] f64, unnormalised, sources excluded, accumulated in
  * source-set order semantics (bc.sp:6-25). */
 int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out, gdx_stats* stats);
+
+/* ---- multi-GPU shards (one process per GPU) ----------------
+ * The caller owns the exchange (torch.distributed / NCCL in distributed.py);
+ * all buffer pointers below may be device or host memory unless noted.
+ *
+ * PageRank, destination-vertex ranges: the rank computes rows [v_begin, v_end)
+ * from the full contrib vector.  A round writes the slice's next contrib
+ * (contrib_slice[v - v_begin]) and partials[2] = {dangling mass of the slice's
+ * new ranks, unsettled vote 0/1}; the caller all-gathers the slices and
+ * all-reduces the partials (dangling_in of the next round = the summed
+ * dangling mass; the fixedPoint ends when no rank is unsettled).  Same
+ * arithmetic as gdx_pagerank (pr.sp:5-33) -- replaces the single-address
+ * dangling atomic and full-V launches of pr_cuda.cu:117-212. */
+int gdx_pr_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end);
+int gdx_pr_shard_init(gdx_graph* g, double* contrib_slice, double* partials /* device [2] */);
+int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, double threshold,
+                       int32_t max_iter, const double* dangling_in /* device [1] */,
+                       const double* contrib_in /* device [n] */,
+                       double* contrib_slice /* device */, double* partials /* device [2] */);
+int gdx_pr_shard_rank(gdx_graph* g, int32_t rounds, double* rank_slice);
+
+/* SSSP, vertex ranges: every rank keeps a full int64 replica of dist (device
+ * [n], INF = INT64_MAX/2) and prev (device [n], the value each own vertex had
+ * when last expanded).  frontier: queue the rank's vertices with dist < prev
+ * (prev := dist) and report how many improved (*count_out, host or device);
+ * relax: relax their out-edges into the local replica with atomicMin.  The
+ * caller MIN-all-reduces dist between rounds and stops when no rank reports
+ * an improvement (sssp.sp's fixedPoint; sssp_cuda.cu:117-199). */
+int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end);
+int gdx_sssp_shard_frontier(gdx_graph* g, int64_t* dist, int64_t* prev, int64_t* count_out);
+int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist);
 
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with

@@ -81,6 +81,14 @@ SIGNATURES = {
     "gdx_tc": ([C.c_void_p, i64p, C.POINTER(GdxStats)], C.c_int),
     "gdx_tc_range": ([C.c_void_p, C.c_int32, C.c_int32, i64p, C.POINTER(GdxStats)], C.c_int),
     "gdx_bc": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),
+    "gdx_pr_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32], C.c_int),
+    "gdx_pr_shard_init": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_pr_shard_round": ([C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_pr_shard_rank": ([C.c_void_p, C.c_int32, C.c_void_p], C.c_int),
+    "gdx_sssp_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32], C.c_int),
+    "gdx_sssp_shard_frontier": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_shard_relax": ([C.c_void_p, C.c_void_p], C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),

@@ -153,6 +153,7 @@ struct gdx_graph {
 
     gdx::Profiler prof;
     std::unique_ptr<gdx::PrPlan> pr;
+    std::unique_ptr<gdx::PrPlan> pr_shard;  // gdx_pr_shard_* (one rank's vertex range)
     std::unique_ptr<gdx::SsspWork> sssp;
     std::unique_ptr<gdx::TcPlan> tc;
     std::unique_ptr<gdx::BcWork> bc;

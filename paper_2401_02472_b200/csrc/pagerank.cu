@@ -61,11 +61,18 @@ struct PrArgs {
     const int32_t* __restrict__ nz_end;   // rev_offsets[nz_row[k] + 1]
     const int32_t* __restrict__ grp_row;  // nz row holding edge 8g
     double* row_sum;                      // per vertex, zero between rounds
+    // row range [v_begin, v_end) and its in-edges [e_begin, e_end) (the whole
+    // graph on one GPU; one rank's slice when sharded, gdx_pr_shard_*)
+    int32_t v_begin, v_end;
+    int64_t e_begin, e_end, e_base;       // e_base = e_begin rounded down to 8
+    int32_t shard;                        // 1: rounds never skip (the host decides)
+    double* contrib_slice;                // shard: contrib_out written at [v - v_begin]
 };
 
 
 __device__ inline bool round_skipped(const PrArgs& a, int round) {
-    return round > 0 && *reinterpret_cast<const volatile int32_t*>(&a.flags[round - 1]) == 0;
+    return !a.shard && round > 0 &&
+           *reinterpret_cast<const volatile int32_t*>(&a.flags[round - 1]) == 0;
 }
 
 // pr.sp:17-30 for one vertex, given sum = sum over in-neighbours of contrib.
@@ -241,25 +248,30 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
                                               int64_t g) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int64_t e0 = g * kEdgeGroup;
-    const int cnt = e0 < a.m ? int((a.m - e0 < kEdgeGroup ? a.m - e0 : int64_t(kEdgeGroup))) : 0;
+    const int64_t e0 = a.e_base + g * kEdgeGroup;
+    // valid slots k in [klo, khi): edges inside [e_begin, e_end)
+    const int64_t dlo = a.e_begin - e0, dhi = a.e_end - e0;
+    const int klo = dlo <= 0 ? 0 : dlo >= kEdgeGroup ? kEdgeGroup : int(dlo);
+    const int khi = dhi <= 0 ? 0 : dhi >= kEdgeGroup ? kEdgeGroup : int(dhi);
+    const bool any = khi > klo;
     double v[kEdgeGroup];
     {
-        const int4* p = reinterpret_cast<const int4*>(a.rev_srcs + (cnt ? e0 : 0));
+        const int4* p = reinterpret_cast<const int4*>(a.rev_srcs + (any ? e0 : 0));
         const int4 q0 = __ldcs(p), q1 = __ldcs(p + 1);
         const int32_t s[kEdgeGroup] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-        for (int k = 0; k < kEdgeGroup; ++k) v[k] = k < cnt ? __ldg(&contrib[s[k]]) : 0.0;
+        for (int k = 0; k < kEdgeGroup; ++k)
+            v[k] = k >= klo && k < khi ? __ldg(&contrib[s[k]]) : 0.0;
     }
-    int32_t key = cnt ? a.grp_row[g] : INT32_MAX;
+    int32_t key = any ? a.grp_row[g] : INT32_MAX;
     const int32_t first = key;
     double run = 0.0, first_val = 0.0;
     bool first_done = false;
-    if (cnt) {
+    if (any) {
         int32_t end = a.nz_end[key];
 #pragma unroll
         for (int k = 0; k < kEdgeGroup; ++k) {
-            if (k < cnt) {
+            if (k >= klo && k < khi) {
                 while (end <= e0 + k) {  // row `key` ended before edge e0+k
                     if (key == first) {
                         first_val = run;
@@ -273,7 +285,7 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
                 run += v[k];
             }
         }
-        if (end <= e0 + cnt) {  // the last row ends exactly at the group's end
+        if (end <= e0 + khi) {  // the last row ends exactly at the group's end
             if (key == first) {
                 first_val = run;
                 first_done = true;
@@ -296,8 +308,8 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
     const double pval = __shfl_up_sync(full, val, 1);
     if (first_done) {
         const double tot = first_val + (lane > 0 && pkey == first ? pval : 0.0);
-        const int64_t warp_e0 = (g & ~int64_t(31)) * kEdgeGroup;
-        const int32_t start = first > 0 ? a.nz_end[first - 1] : 0;
+        const int64_t warp_e0 = a.e_base + (g & ~int64_t(31)) * kEdgeGroup;
+        const int64_t start = first > 0 ? a.nz_end[first - 1] : a.e_begin;
         const int32_t row = a.nz_row[first];
         if (start < warp_e0)
             atomicAdd(&a.row_sum[row], tot);  // row began in an earlier warp's edges
@@ -315,13 +327,31 @@ __global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
 }
 
 // Pass B: two vertices per thread (16 B vector loads/stores), two pairs in
-// flight per iteration.
+// flight per iteration.  Pairs start at an even vertex; a pair that straddles
+// the range bounds (or the array end) takes the scalar path.
+__device__ inline void pr_vertex_one(const PrArgs& a, int round, int64_t v, double dang_term,
+                                     const double* __restrict__ rank_in,
+                                     double* __restrict__ rank_out,
+                                     double* __restrict__ contrib_out, double& dang_local,
+                                     int& unsettled) {
+    const double sum = a.row_sum[v];
+    if (sum != 0.0) a.row_sum[v] = 0.0;
+    const double nr = a.base + a.damping * (dang_term + sum);
+    double c = nr - rank_in[v];
+    if (c < 0.0) c = 0.0 - c;
+    if (c >= a.threshold && round < a.max_iter) unsettled = 1;
+    rank_out[v] = nr;
+    const int32_t d = a.offsets[v + 1] - a.offsets[v];
+    contrib_out[v] = d > 0 ? nr / double(d) : 0.0;
+    if (d == 0) dang_local += nr;
+}
+
 __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, double dang_term,
                                       const double* __restrict__ rank_in,
                                       double* __restrict__ rank_out,
                                       double* __restrict__ contrib_out, double& dang_local,
                                       int& unsettled) {
-    if (v + 1 < a.n) {
+    if (v >= a.v_begin && v + 1 < a.v_end && !a.shard) {
         const double2 sum = *reinterpret_cast<const double2*>(a.row_sum + v);
         const double2 ri = *reinterpret_cast<const double2*>(rank_in + v);
         const int32_t o0 = a.offsets[v], o1 = a.offsets[v + 1], o2 = a.offsets[v + 2];
@@ -339,17 +369,11 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
             make_double2(d0 > 0 ? nr0 / double(d0) : 0.0, d1 > 0 ? nr1 / double(d1) : 0.0);
         if (d0 == 0) dang_local += nr0;
         if (d1 == 0) dang_local += nr1;
-    } else if (v < a.n) {
-        const double sum = a.row_sum[v];
-        if (sum != 0.0) a.row_sum[v] = 0.0;
-        const double nr = a.base + a.damping * (dang_term + sum);
-        double c = nr - rank_in[v];
-        if (c < 0.0) c = 0.0 - c;
-        if (c >= a.threshold && round < a.max_iter) unsettled = 1;
-        rank_out[v] = nr;
-        const int32_t d = a.offsets[v + 1] - a.offsets[v];
-        contrib_out[v] = d > 0 ? nr / double(d) : 0.0;
-        if (d == 0) dang_local += nr;
+    } else {
+        for (int64_t x = v; x < v + 2; ++x)
+            if (x >= a.v_begin && x < a.v_end)
+                pr_vertex_one(a, round, x, dang_term, rank_in, rank_out, contrib_out, dang_local,
+                              unsettled);
     }
 }
 
@@ -360,39 +384,46 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
     const double dang_term = dang_in / a.nd;
     const double* __restrict__ rank_in = (round & 1) ? a.rank1 : a.rank0;
     double* __restrict__ rank_out = (round & 1) ? a.rank0 : a.rank1;
-    double* __restrict__ contrib_out = (round & 1) ? a.contrib0 : a.contrib1;
+    double* __restrict__ contrib_out =
+        a.shard ? a.contrib_slice - a.v_begin : ((round & 1) ? a.contrib0 : a.contrib1);
     double dang_local = 0.0;
     int unsettled = 0;
+    const int64_t v_al = a.v_begin & ~int64_t(1);
     const int64_t stride = (int64_t)gridDim.x * kPrBlock * 2;
-    for (int64_t v = (blockIdx.x * (int64_t)kPrBlock + threadIdx.x) * 2; v < a.n; v += 2 * stride) {
+    for (int64_t v = v_al + (blockIdx.x * (int64_t)kPrBlock + threadIdx.x) * 2; v < a.v_end;
+         v += 2 * stride) {
         pr_vertex_pair(a, round, v, dang_term, rank_in, rank_out, contrib_out, dang_local,
                        unsettled);
-        pr_vertex_pair(a, round, v + stride, dang_term, rank_in, rank_out, contrib_out, dang_local,
-                       unsettled);
+        if (v + stride < a.v_end)
+            pr_vertex_pair(a, round, v + stride, dang_term, rank_in, rank_out, contrib_out,
+                           dang_local, unsettled);
     }
     block_flush(a, round, dang_local, unsettled);
 }
 
 // Non-empty rows of the reverse CSR and the row of every 8-edge group.
-__global__ void k_pr_nz_flags(int32_t n, const int32_t* __restrict__ rev_offsets, int32_t* flag) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
-        flag[v] = rev_offsets[v + 1] > rev_offsets[v];
+__global__ void k_pr_nz_flags(int32_t v0, int32_t cnt, const int32_t* __restrict__ rev_offsets,
+                              int32_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = rev_offsets[v0 + i + 1] > rev_offsets[v0 + i];
 }
-__global__ void k_pr_nz_fill(int32_t n, const int32_t* __restrict__ rev_offsets,
+__global__ void k_pr_nz_fill(int32_t v0, int32_t cnt, const int32_t* __restrict__ rev_offsets,
                              const int32_t* __restrict__ pos, int32_t* nz_row, int32_t* nz_end) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = v0 + i;
         if (rev_offsets[v + 1] > rev_offsets[v]) {
-            nz_row[pos[v]] = int32_t(v);
-            nz_end[pos[v]] = rev_offsets[v + 1];
+            nz_row[pos[i]] = int32_t(v);
+            nz_end[pos[i]] = rev_offsets[v + 1];
         }
+    }
 }
-__global__ void k_pr_grp_rows(int64_t ngroups, int32_t nnz, const int32_t* __restrict__ nz_end,
-                              int32_t* grp_row) {
+__global__ void k_pr_grp_rows(int64_t ngroups, int64_t e_base, int64_t e_begin, int32_t nnz,
+                              const int32_t* __restrict__ nz_end, int32_t* grp_row) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
          g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = g * kEdgeGroup;
+        const int64_t e = max(e_base + g * kEdgeGroup, e_begin);
         int32_t lo = 0, hi = nnz;  // first k with nz_end[k] > e
         while (lo < hi) {
             const int32_t mid = (lo + hi) >> 1;
@@ -487,36 +518,49 @@ __global__ void k_pr_tile_coords(int32_t n, int32_t m, int32_t ntiles, int32_t t
     }
 }
 
-static void build_edge_plan(gdx_graph* g) {
-    auto& P = *g->pr;
+// Edge-aligned plan for the rows [v_begin, v_end) (the whole graph, or one
+// rank's slice under gdx_pr_shard_setup).
+static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_end) {
     cudaStream_t s = g->stream;
-    const int32_t n = g->n, m = g->m;
-    const int grid = blocks_for(n, 256, g->num_sms * 16);
-    DevBuf<int32_t> flag(n), pos(n);
-    DevBuf<int32_t> cnt(1);
-    k_pr_nz_flags<<<grid, 256, 0, s>>>(n, g->rev_offsets.get(), flag.get());
-    GDX_LAUNCH_CHECK();
-    size_t bytes = 0;
-    GDX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag.get(), pos.get(), n, s));
-    DevBuf<uint8_t> tmp(bytes);
-    GDX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, flag.get(), pos.get(), n, s));
+    const int32_t n = g->n;
+    const int32_t cnt = v_end - v_begin;
+    int32_t eb[2] = {0, 0};
+    GDX_CUDA(cudaMemcpyAsync(&eb[0], g->rev_offsets.get() + v_begin, 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(&eb[1], g->rev_offsets.get() + v_end, 4, cudaMemcpyDeviceToHost, s));
+    const int grid = blocks_for(std::max(cnt, 1), 256, g->num_sms * 16);
+    DevBuf<int32_t> flag(std::max(cnt, 1)), pos(std::max(cnt, 1));
     int32_t last[2] = {0, 0};
-    if (n > 0) {
-        GDX_CUDA(cudaMemcpyAsync(&last[0], pos.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
-        GDX_CUDA(cudaMemcpyAsync(&last[1], flag.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    if (cnt > 0) {
+        k_pr_nz_flags<<<grid, 256, 0, s>>>(v_begin, cnt, g->rev_offsets.get(), flag.get());
+        GDX_LAUNCH_CHECK();
+        size_t bytes = 0;
+        GDX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag.get(), pos.get(), cnt, s));
+        DevBuf<uint8_t> tmp(bytes);
+        GDX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, flag.get(), pos.get(), cnt, s));
+        GDX_CUDA(cudaMemcpyAsync(&last[0], pos.get() + cnt - 1, 4, cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaMemcpyAsync(&last[1], flag.get() + cnt - 1, 4, cudaMemcpyDeviceToHost, s));
     }
     GDX_CUDA(cudaStreamSynchronize(s));
+    P.v_begin = v_begin;
+    P.v_end = v_end;
+    P.e_begin = eb[0];
+    P.e_end = eb[1];
+    P.e_base = P.e_begin & ~int64_t(kEdgeGroup - 1);
     P.nnz = last[0] + last[1];
     P.nz_row.alloc(size_t(P.nnz) + 1);
     P.nz_end.alloc(size_t(P.nnz) + 1);
-    k_pr_nz_fill<<<grid, 256, 0, s>>>(n, g->rev_offsets.get(), pos.get(), P.nz_row.get(),
-                                      P.nz_end.get());
-    GDX_LAUNCH_CHECK();
-    const int64_t ngroups = (int64_t(m) + kEdgeGroup - 1) / kEdgeGroup;
-    P.grp_row.alloc(size_t(ngroups) + 1);
-    k_pr_grp_rows<<<blocks_for(ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
-        ngroups, P.nnz, P.nz_end.get(), P.grp_row.get());
-    GDX_LAUNCH_CHECK();
+    if (cnt > 0) {
+        k_pr_nz_fill<<<grid, 256, 0, s>>>(v_begin, cnt, g->rev_offsets.get(), pos.get(),
+                                          P.nz_row.get(), P.nz_end.get());
+        GDX_LAUNCH_CHECK();
+    }
+    P.ngroups = (P.e_end - P.e_base + kEdgeGroup - 1) / kEdgeGroup;
+    P.grp_row.alloc(size_t(P.ngroups) + 1);
+    if (P.ngroups > 0) {
+        k_pr_grp_rows<<<blocks_for(P.ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
+            P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz_end.get(), P.grp_row.get());
+        GDX_LAUNCH_CHECK();
+    }
     P.row_sum.alloc(n);
     GDX_CUDA(cudaMemsetAsync(P.row_sum.get(), 0, P.row_sum.bytes(), s));
     for (int i = 0; i < 2; ++i) {
@@ -525,7 +569,7 @@ static void build_edge_plan(gdx_graph* g) {
     }
     P.dangling.alloc(3);
     P.block = 256;
-    P.grid = blocks_for(ngroups, 256, INT32_MAX);
+    P.grid = blocks_for(std::max<int64_t>(P.ngroups, 1), 256, INT32_MAX);
     GDX_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -536,7 +580,7 @@ static void build_plan(gdx_graph* g) {
     const int64_t total = int64_t(n) + m;
     const char* var = std::getenv("GDX_PR_VARIANT");
     P.variant = var ? std::atoi(var) : 60;  // see kPrVariants
-    if (P.variant == 60) return build_edge_plan(g);
+    if (P.variant == 60) return build_edge_plan(g, P, 0, g->n);
     P.tile = pr_variant_tile(P.variant);
     const int64_t nt = (total + P.tile - 1) / P.tile;
     if (nt > INT32_MAX) fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph too large for one plan");
@@ -590,6 +634,70 @@ static void build_plan(gdx_graph* g) {
     GDX_CUDA(cudaStreamSynchronize(s));
 }
 
+static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshold,
+                        int32_t max_iter) {
+    PrArgs a;
+    a.n = g->n;
+    a.ntiles = P.ntiles;
+    a.nslots = P.nslots;
+    a.offsets = g->offsets.get();
+    a.rev_offsets = g->rev_offsets.get();
+    a.rev_srcs = g->rev_srcs.get();
+    a.tile_coord = P.tile_coord.get();
+    a.tile_slots = P.tile_slots.get();
+    a.slot_row = P.slot_row.get();
+    a.slot_acc = P.slot_acc.get();
+    a.rank0 = P.rank[0].get();
+    a.rank1 = P.rank[1].get();
+    a.contrib0 = P.contrib[0].get();
+    a.contrib1 = P.contrib[1].get();
+    a.dangling = P.dangling.get();
+    a.flags = P.flags.get();
+    a.damping = damping;
+    a.threshold = threshold;
+    a.nd = double(g->n);
+    a.base = (1.0 - damping) / a.nd;
+    a.max_iter = max_iter;
+    a.m = g->m;
+    a.nnz = P.nnz;
+    a.nz_row = P.nz_row.get();
+    a.nz_end = P.nz_end.get();
+    a.grp_row = P.grp_row.get();
+    a.row_sum = P.row_sum.get();
+    a.v_begin = P.shard ? P.v_begin : 0;
+    a.v_end = P.shard ? P.v_end : g->n;
+    a.e_begin = P.e_begin;
+    a.e_end = P.e_end;
+    a.e_base = P.e_base;
+    a.shard = P.shard ? 1 : 0;
+    a.contrib_slice = nullptr;
+    return a;
+}
+
+// Sharded rounds (gdx_pr_shard_*): rank = 1/n, contrib and the dangling mass
+// of the slice [v_begin, v_end).
+__global__ void __launch_bounds__(kPrBlock) k_pr_shard_init(PrArgs a, double* partials) {
+    double dang_local = 0.0;
+    const double r0 = 1.0 / a.nd;
+    for (int64_t v = a.v_begin + blockIdx.x * (int64_t)kPrBlock + threadIdx.x; v < a.v_end;
+         v += (int64_t)gridDim.x * kPrBlock) {
+        a.rank0[v] = r0;
+        const int32_t od = a.offsets[v + 1] - a.offsets[v];
+        a.contrib_slice[v - a.v_begin] = od > 0 ? r0 / double(od) : 0.0;
+        if (od == 0) dang_local += r0;
+    }
+    typedef cub::BlockReduce<double, kPrBlock> R;
+    __shared__ typename R::TempStorage tmp;
+    double tot = R(tmp).Sum(dang_local);
+    if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&partials[0], tot);
+}
+
+__global__ void k_pr_shard_partials(const double* dangling, const int32_t* flags, int round,
+                                    double* partials) {
+    partials[0] = dangling[(round + 1) % 3];
+    partials[1] = flags[round] ? 1.0 : 0.0;
+}
+
 }  // namespace gdx
 
 using namespace gdx;
@@ -618,34 +726,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             P.flags.alloc(size_t(limit));
             P.flags_cap = int32_t(limit);
         }
-        PrArgs a;
-        a.n = g->n;
-        a.ntiles = P.ntiles;
-        a.nslots = P.nslots;
-        a.offsets = g->offsets.get();
-        a.rev_offsets = g->rev_offsets.get();
-        a.rev_srcs = g->rev_srcs.get();
-        a.tile_coord = P.tile_coord.get();
-        a.tile_slots = P.tile_slots.get();
-        a.slot_row = P.slot_row.get();
-        a.slot_acc = P.slot_acc.get();
-        a.rank0 = P.rank[0].get();
-        a.rank1 = P.rank[1].get();
-        a.contrib0 = P.contrib[0].get();
-        a.contrib1 = P.contrib[1].get();
-        a.dangling = P.dangling.get();
-        a.flags = P.flags.get();
-        a.damping = damping;
-        a.threshold = threshold;
-        a.nd = double(g->n);
-        a.base = (1.0 - damping) / a.nd;
-        a.max_iter = max_iter;
-        a.m = g->m;
-        a.nnz = P.nnz;
-        a.nz_row = P.nz_row.get();
-        a.nz_end = P.nz_end.get();
-        a.grp_row = P.grp_row.get();
-        a.row_sum = P.row_sum.get();
+        PrArgs a = make_args(g, P, damping, threshold, max_iter);
 
         GDX_CUDA(cudaMemsetAsync(P.flags.get(), 0, size_t(limit) * 4, s));
         GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
@@ -661,7 +742,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             const int64_t lim = std::min(r + batch, limit);
             for (int64_t rr = r; rr < lim; ++rr) {
                 if (P.variant == 60) {
-                    if (g->m > 0)
+                    if (P.ngroups > 0)
                         timed_launch(g, "pr_edges", [&] {
                             k_pr_edges<<<P.grid, P.block, 0, s>>>(a, int(rr));
                         });
@@ -669,7 +750,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
                         k_pr_vertices<<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0,
                                         s>>>(a, int(rr));
                     });
-                    launches += 1 + (g->m > 0);
+                    launches += 1 + (P.ngroups > 0);
                     continue;
                 }
                 timed_launch(g, "pr_tiles", [&] {
@@ -712,5 +793,93 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             // rev_offsets 4n + offsets 4n + rank in 8n + rank out 8n + contrib out 8n.
             stats->algorithmic_bytes = double(rounds) * (12.0 * g->m + 32.0 * g->n);
         }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Sharded PageRank: one rank of a destination-vertex-range partition
+// (SURVEY.md §8(e)); the caller owns the exchange (all-gather of the contrib
+// slices, all-reduce of the partials) -- see distributed.py sharded_pr.
+// ---------------------------------------------------------------------------
+extern "C" int gdx_pr_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        if (v_begin < 0 || v_end > g->n || v_begin > v_end)
+            fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex range out of bounds");
+        if (!g->rev_offsets.get() || !g->rev_srcs.get())
+            fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
+        DeviceGuard dg(g->device);
+        g->pr_shard = std::make_unique<PrPlan>();
+        g->pr_shard->shard = true;
+        build_edge_plan(g, *g->pr_shard, v_begin, v_end);
+        g->pr_shard->partials.alloc(2);
+    });
+}
+
+extern "C" int gdx_pr_shard_init(gdx_graph* g, double* contrib_slice, double* partials) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        cudaStream_t s = g->stream;
+        PrArgs a = make_args(g, P, 0.85, 0.0, 0);
+        a.contrib_slice = contrib_slice;
+        GDX_CUDA(cudaMemsetAsync(partials, 0, 2 * sizeof(double), s));
+        GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
+        if (P.v_end > P.v_begin)
+            timed_launch(g, "pr_init", [&] {
+                k_pr_shard_init<<<blocks_for(P.v_end - P.v_begin, kPrBlock, g->num_sms * 8),
+                                  kPrBlock, 0, s>>>(a, partials);
+            });
+        GDX_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+extern "C" int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, double threshold,
+                                  int32_t max_iter, const double* dangling_in,
+                                  const double* contrib_in, double* contrib_slice,
+                                  double* partials) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        if (round < 0) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: negative round");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        cudaStream_t s = g->stream;
+        if (P.flags_cap < round + 1) {
+            const int32_t cap = std::max(round + 1, 2 * P.flags_cap);
+            DevBuf<int32_t> nf(cap);
+            P.flags = std::move(nf);
+            P.flags_cap = cap;
+        }
+        PrArgs a = make_args(g, P, damping, threshold, max_iter);
+        a.contrib0 = a.contrib1 = const_cast<double*>(contrib_in);
+        a.contrib_slice = contrib_slice;
+        GDX_CUDA(cudaMemcpyAsync(P.dangling.get() + round % 3, dangling_in, sizeof(double),
+                                 cudaMemcpyDefault, s));
+        GDX_CUDA(cudaMemsetAsync(P.flags.get() + round, 0, 4, s));
+        if (P.ngroups > 0)
+            timed_launch(g, "pr_edges", [&] {
+                k_pr_edges<<<P.grid, P.block, 0, s>>>(a, round);
+            });
+        timed_launch(g, "pr_vertices", [&] {
+            k_pr_vertices<<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
+                                       g->num_sms * 8),
+                            kPrBlock, 0, s>>>(a, round);
+        });
+        k_pr_shard_partials<<<1, 1, 0, s>>>(P.dangling.get(), P.flags.get(), round, partials);
+        GDX_LAUNCH_CHECK();
+    });
+}
+
+extern "C" int gdx_pr_shard_rank(gdx_graph* g, int32_t rounds, double* rank_slice) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard || !rank_slice)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        copy_out(g, rank_slice, P.rank[rounds & 1].get() + P.v_begin,
+                 size_t(P.v_end - P.v_begin) * sizeof(double));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
     });
 }

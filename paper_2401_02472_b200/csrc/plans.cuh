@@ -28,6 +28,10 @@ struct PrPlan {
     DevBuf<int32_t> nz_row, nz_end;       // non-empty rows of the reverse CSR and their ends
     DevBuf<int32_t> grp_row;              // nz row holding edge 8g
     DevBuf<double> row_sum;               // per-vertex gather sums (zero between rounds)
+    int32_t v_begin = 0, v_end = 0;       // row range of the plan
+    int64_t e_begin = 0, e_end = 0, e_base = 0, ngroups = 0;
+    bool shard = false;                   // built by gdx_pr_shard_setup
+    DevBuf<double> partials;              // shard: [dangling partial, unsettled]
     int32_t flags_cap = 0;
     int grid = 0;
     int variant = 7;
@@ -45,6 +49,11 @@ struct SsspWork {
     DevBuf<unsigned long long> trace; // optional per-round trace (GDX_SSSP_TRACE)
     size_t qcap = 0;
     int grid = 0;
+    // gdx_sssp_shard_*: this rank's vertex range and relaxation items
+    bool shard_ready = false;
+    int32_t shard_v0 = 0, shard_v1 = 0;
+    DevBuf<int2> shard_queue;
+    DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks]
 };
 
 // Triangle-counting workspace (tc.cu).

@@ -348,9 +348,136 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
     return h[kOvf] != 0;
 }
 
+// ---------------------------------------------------------------------------
+// Sharded SSSP (gdx_sssp_shard_*): one rank of a vertex-range partition.
+// Every rank keeps a full int64 replica of dist; a round relaxes the out-edges
+// of the rank's own vertices that improved since they were last expanded
+// (dist < prev), into the local replica, and the caller merges the replicas
+// with an element-wise MIN all-reduce (distributed.py sharded_sssp).
+// ---------------------------------------------------------------------------
+constexpr int kShardChunk = 128;  // edges per relaxation item
+
+__global__ void k_sssp_shard_frontier(int32_t v0, int32_t v1, const int32_t* __restrict__ offsets,
+                                      const long long* __restrict__ dist, long long* prev,
+                                      int2* queue, unsigned long long* ctr) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = v0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane);
+         base < v1; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = base + lane;
+        int items = 0;
+        int32_t b = 0;
+        if (v < v1) {
+            const long long d = dist[v];
+            if (d < prev[v]) {
+                prev[v] = d;
+                b = offsets[v];
+                const int32_t deg = offsets[v + 1] - b;
+                items = deg > 0 ? (deg + kShardChunk - 1) / kShardChunk : 0;
+                if (deg == 0) atomicAdd(&ctr[1], 1ull);  // improved but nothing to relax
+            }
+        }
+        int incl = items;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(full, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(full, incl, 31);
+        unsigned long long pos = 0;
+        if (lane == 31 && total) pos = atomicAdd(&ctr[0], (unsigned long long)total);
+        pos = __shfl_sync(full, pos, 31);
+        for (int t = 0; t < items; ++t)
+            queue[pos + incl - items + t] = make_int2(int32_t(v), b + t * kShardChunk);
+    }
+}
+
+__global__ void k_sssp_shard_relax(const int2* __restrict__ queue,
+                                   const unsigned long long* __restrict__ ctr,
+                                   const int32_t* __restrict__ offsets,
+                                   const int32_t* __restrict__ dests,
+                                   const int32_t* __restrict__ weights, long long* dist) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nq = ctr[0];
+    for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+         i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const int2 it = queue[i];
+        const long long dv = dist[it.x];
+        const int32_t e1 = min(it.y + kShardChunk, offsets[it.x + 1]);
+        for (int32_t e = it.y + lane; e < e1; e += 32) {
+            const int32_t u = dests[e];
+            const long long c = dv + (weights ? weights[e] : 1);
+            if (c < dist[u]) atomicMin(&dist[u], c);
+        }
+    }
+}
+
 }  // namespace gdx
 
 using namespace gdx;
+
+extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        if (v_begin < 0 || v_end > g->n || v_begin > v_end)
+            fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex range out of bounds");
+        if (!g->dests.get() && g->m > 0)
+            fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
+        DeviceGuard dg(g->device);
+        if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
+        auto& w = *g->sssp;
+        int32_t eb[2] = {0, 0};
+        GDX_CUDA(cudaMemcpy(&eb[0], g->offsets.get() + v_begin, 4, cudaMemcpyDeviceToHost));
+        GDX_CUDA(cudaMemcpy(&eb[1], g->offsets.get() + v_end, 4, cudaMemcpyDeviceToHost));
+        w.shard_v0 = v_begin;
+        w.shard_v1 = v_end;
+        w.shard_queue.ensure(size_t(v_end - v_begin) + size_t(eb[1] - eb[0]) / kShardChunk + 1);
+        w.shard_ctr.ensure(2);
+        w.shard_ready = true;
+    });
+}
+
+extern "C" int gdx_sssp_shard_frontier(gdx_graph* g, int64_t* dist, int64_t* prev,
+                                       int64_t* count_out) {
+    return guard_impl([&] {
+        if (!g || !g->sssp || !g->sssp->shard_ready)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        DeviceGuard dg(g->device);
+        auto& w = *g->sssp;
+        cudaStream_t s = g->stream;
+        GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get(), 0, 2 * sizeof(unsigned long long), s));
+        const int32_t cnt = w.shard_v1 - w.shard_v0;
+        if (cnt > 0)
+            timed_launch(g, "sssp_shard_frontier", [&] {
+                k_sssp_shard_frontier<<<blocks_for(cnt, 256, g->num_sms * 8), 256, 0, s>>>(
+                    w.shard_v0, w.shard_v1, g->offsets.get(),
+                    reinterpret_cast<const long long*>(dist), reinterpret_cast<long long*>(prev),
+                    w.shard_queue.get(), w.shard_ctr.get());
+            });
+        // count_out (device or host): queued items + improved sinks of this rank
+        unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+        GDX_CUDA(cudaMemcpyAsync(h, w.shard_ctr.get(), 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        const int64_t c = int64_t(h[0] + h[1]);
+        GDX_CUDA(cudaMemcpy(count_out, &c, sizeof(c), cudaMemcpyDefault));
+    });
+}
+
+extern "C" int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist) {
+    return guard_impl([&] {
+        if (!g || !g->sssp || !g->sssp->shard_ready)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        DeviceGuard dg(g->device);
+        auto& w = *g->sssp;
+        cudaStream_t s = g->stream;
+        timed_launch(g, "sssp_shard_relax", [&] {
+            k_sssp_shard_relax<<<g->num_sms * 16, 256, 0, s>>>(
+                w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
+                g->weighted ? g->weights.get() : nullptr, reinterpret_cast<long long*>(dist));
+        });
+    });
+}
 
 extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
     return guard_impl([&] {

@@ -10,6 +10,15 @@ SURVEY.md §8(e): each algorithm shards naturally --
   (source order preserved inside a block); every rank accumulates a partial
   ``bc`` and one f64 all-reduce of n sums them.  The cross-rank sum order
   differs from the reference's source order only by rounding (within 1e-6).
+* PR: destination-vertex ranges balanced by in-edges; every rank computes its
+  rows from the full contrib vector (``gdx_pr_shard_round``); per round one
+  all-gather of the contrib slices and one all-reduce of (dangling mass,
+  unsettled vote).  Same arithmetic and round count as ``gdx_pagerank``.
+* SSSP: vertex ranges balanced by out-edges; every rank keeps a replica of
+  dist, relaxes the out-edges of its own improved vertices
+  (``gdx_sssp_shard_*``), and one element-wise MIN all-reduce merges the
+  replicas per round; one SUM all-reduce of the improvement counts decides
+  the fixedPoint.  Distances are unique, so the result is bit-exact.
 
 ``torch.distributed`` carries the collectives: NCCL over NVLink on the GPU box,
 gloo on the CPU for the tests.  The per-rank compute is pluggable so the
@@ -72,21 +81,47 @@ def source_blocks(sources: Sequence[int], parts: int) -> list[list[int]]:
 # ---------------------------------------------------------------------------- executors
 
 class Executor(Protocol):
+    """Per-rank compute.  Tensors are torch tensors on the collective device
+    (CUDA under NCCL, CPU under gloo)."""
+
     def tc_range(self, v0: int, v1: int) -> int: ...
 
     def bc(self, sources: Sequence[int]) -> np.ndarray: ...
 
     def offsets(self) -> np.ndarray: ...
 
+    def rev_offsets(self) -> np.ndarray: ...
+
     def num_nodes(self) -> int: ...
+
+    # PageRank shard (gdx_pr_shard_*)
+    def pr_setup(self, v0: int, v1: int) -> None: ...
+
+    def pr_init(self, contrib_slice, partials) -> None: ...
+
+    def pr_round(self, rnd, damping, threshold, max_iter, dangling_in, contrib, contrib_slice,
+                 partials) -> None: ...
+
+    def pr_rank(self, rounds: int, rank_slice) -> None: ...
+
+    # SSSP shard (gdx_sssp_shard_*)
+    def sssp_setup(self, v0: int, v1: int) -> None: ...
+
+    def sssp_frontier(self, dist, prev) -> int: ...
+
+    def sssp_relax(self, dist) -> None: ...
 
 
 class DeviceExecutor:
     """Per-rank compute on this rank's GPU (libgdx.so)."""
 
     def __init__(self, graph):
+        import torch
         self.g = graph  # paper_2401_02472_b200.DeviceGraph on cuda:LOCAL_RANK
         self._off = None
+        # launch on torch's current stream so the library's kernels, NCCL
+        # collectives and torch copies are stream-ordered
+        graph.set_stream(torch.cuda.current_stream(graph.device).cuda_stream)
 
     def tc_range(self, v0, v1):
         return self.g.tc_range(v0, v1)
@@ -99,8 +134,49 @@ class DeviceExecutor:
             self._off = self.g.download().offsets
         return self._off
 
+    def rev_offsets(self):
+        if getattr(self, "_roff", None) is None:
+            (t,) = self.g.device_arrays(["rev_offsets"])
+            self._roff = t.cpu().numpy()
+        return self._roff
+
     def num_nodes(self):
         return self.g.n
+
+    def _staged(self, fn, *tensors):
+        """Run fn on device copies of CPU tensors (collectives over gloo, e.g.
+        several ranks sharing one GPU in the tests) and copy them back; CUDA
+        tensors (NCCL) are passed through untouched."""
+        dev = [t if t.is_cuda else t.to(f"cuda:{self.g.device}") for t in tensors]
+        out = fn(*dev)
+        for t, d in zip(tensors, dev):
+            if d is not t:
+                t.copy_(d.cpu())
+        return out
+
+    def pr_setup(self, v0, v1):
+        self.g.pr_shard_setup(v0, v1)
+
+    def pr_init(self, contrib_slice, partials):
+        self._staged(self.g.pr_shard_init, contrib_slice, partials)
+
+    def pr_round(self, rnd, damping, threshold, max_iter, dangling_in, contrib, contrib_slice,
+                 partials):
+        self._staged(lambda d, c, s, p: self.g.pr_shard_round(rnd, damping, threshold, max_iter,
+                                                              d, c, s, p),
+                     dangling_in, contrib, contrib_slice, partials)
+
+    def pr_rank(self, rounds, rank_slice):
+        self._staged(lambda r: self.g.pr_shard_rank(rounds, r), rank_slice)
+
+    def sssp_setup(self, v0, v1):
+        self.g.sssp_shard_setup(v0, v1)
+
+    def sssp_frontier(self, dist, prev):
+        return self._staged(self.g.sssp_shard_frontier, dist, prev)
+
+    def sssp_relax(self, dist):
+        self._staged(self.g.sssp_shard_relax, dist)
 
 
 # ---------------------------------------------------------------------------- sharded entry points
@@ -141,6 +217,101 @@ def sharded_bc(ex: Executor, sources: Sequence[int], group=None) -> np.ndarray:
     t = torch.from_numpy(np.ascontiguousarray(part, dtype=np.float64)).to(_device_for_collectives())
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.cpu().numpy()
+
+
+def _all_gather_slices(slice_buf, ranges, out, group=None):
+    """All-gather variable-length contiguous slices into `out` (padded equal
+    chunks through all_gather_into_tensor, then unpacked)."""
+    import torch
+    dist = _dist()
+    world = dist.get_world_size(group)
+    chunk = slice_buf.numel()
+    gathered = torch.empty(world * chunk, dtype=slice_buf.dtype, device=slice_buf.device)
+    dist.all_gather_into_tensor(gathered, slice_buf, group=group)
+    for r, (a, b) in enumerate(ranges):
+        if b > a:
+            out[a:b].copy_(gathered[r * chunk: r * chunk + (b - a)])
+
+
+def pr_ranges(rev_offsets: np.ndarray, parts: int) -> list[tuple[int, int]]:
+    """Destination-vertex ranges for PR balanced by (in-edges + vertices)."""
+    indeg = np.diff(np.asarray(rev_offsets, dtype=np.int64)).astype(np.float64)
+    return balanced_ranges(indeg + 1.0, parts)
+
+
+def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, group=None):
+    """ComputePR across ranks -> (rank f64[n] numpy, rounds).  Raises
+    GraphdslError("NonTermination") like gdx_pagerank when the interpreter's
+    fixedPoint cap 10n+100 is hit before max_iter+1 rounds."""
+    import torch
+    from ._lib import GraphdslError
+    dist = _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = _device_for_collectives()
+    n = ex.num_nodes()
+    if n == 0:
+        raise GraphdslError("RuntimeError", "RuntimeError: division by zero")
+    ranges = pr_ranges(ex.rev_offsets(), world)
+    v0, v1 = ranges[rank]
+    chunk = max(max(b - a for a, b in ranges), 1)
+    f64 = dict(dtype=torch.float64, device=dev)
+    contrib = [torch.zeros(n, **f64), torch.zeros(n, **f64)]
+    slice_buf = torch.zeros(chunk, **f64)
+    partials = torch.zeros(2, **f64)
+    ex.pr_setup(v0, v1)
+    ex.pr_init(slice_buf, partials)
+    _all_gather_slices(slice_buf, ranges, contrib[0], group)
+    dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+    dangling = partials[0:1].clone()
+    cap = 10 * n + 100
+    want = max_iter + 1 if max_iter >= 0 else 1
+    limit = min(want, cap)
+    rounds = limit
+    for r in range(limit):
+        ex.pr_round(r, damping, threshold, max_iter, dangling, contrib[r & 1], slice_buf, partials)
+        _all_gather_slices(slice_buf, ranges, contrib[(r + 1) & 1], group)
+        dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+        dangling.copy_(partials[0:1])
+        if float(partials[1].item()) == 0.0:
+            rounds = r + 1
+            break
+    else:
+        if limit < want:
+            raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} "
+                                "iterations without converging")
+    rank_slice = torch.zeros(chunk, **f64)
+    ex.pr_rank(rounds, rank_slice)
+    out = torch.zeros(n, **f64)
+    _all_gather_slices(rank_slice, ranges, out, group)
+    return out.cpu().numpy(), rounds
+
+
+def sharded_sssp(ex: Executor, src: int, group=None) -> np.ndarray:
+    """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact."""
+    import torch
+    from ._lib import GraphdslError
+    dist = _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = _device_for_collectives()
+    n = ex.num_nodes()
+    if not 0 <= src < n:
+        raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
+    v0, v1 = vertex_ranges(ex.offsets(), world)[rank]
+    ex.sssp_setup(v0, v1)
+    inf = (2**63 - 1) // 2
+    d = torch.full((n,), inf, dtype=torch.int64, device=dev)
+    prev = torch.full((n,), inf, dtype=torch.int64, device=dev)
+    d[src] = 0
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    cap = 10 * n + 100
+    for _ in range(cap + 1):
+        cnt.fill_(ex.sssp_frontier(d, prev))
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
+        if int(cnt.item()) == 0:
+            return d.cpu().numpy()
+        ex.sssp_relax(d)
+        dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
+    raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} iterations")
 
 
 def init_from_env(backend: Optional[str] = None) -> None:

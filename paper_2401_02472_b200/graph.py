@@ -190,6 +190,11 @@ class DeviceGraph:
         return self._h
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
+        """Launch on this CUDA stream (e.g. ``torch.cuda.current_stream().cuda_stream``).
+        None selects the handle's own stream; 0 (torch's default stream) maps to
+        cudaStreamLegacy so the library's work is ordered with torch's."""
+        if stream_ptr == 0:
+            stream_ptr = 1  # cudaStreamLegacy
         check(_lib.load().gdx_graph_set_stream(self.handle, stream_ptr))
 
     def stream(self) -> int:
@@ -250,6 +255,34 @@ class DeviceGraph:
         if stats is not None:
             stats.update(st.as_dict())
         return res
+
+    # ---- multi-GPU shards (distributed.py drives the exchange) ------------------
+    def pr_shard_setup(self, v_begin: int, v_end: int) -> None:
+        check(_lib.load().gdx_pr_shard_setup(self.handle, int(v_begin), int(v_end)))
+
+    def pr_shard_init(self, contrib_slice, partials) -> None:
+        check(_lib.load().gdx_pr_shard_init(self.handle, _ptr(contrib_slice), _ptr(partials)))
+
+    def pr_shard_round(self, rnd: int, damping: float, threshold: float, max_iter: int,
+                       dangling_in, contrib_in, contrib_slice, partials) -> None:
+        check(_lib.load().gdx_pr_shard_round(self.handle, int(rnd), float(damping),
+                                             float(threshold), int(max_iter), _ptr(dangling_in),
+                                             _ptr(contrib_in), _ptr(contrib_slice),
+                                             _ptr(partials)))
+
+    def pr_shard_rank(self, rounds: int, rank_slice) -> None:
+        check(_lib.load().gdx_pr_shard_rank(self.handle, int(rounds), _ptr(rank_slice)))
+
+    def sssp_shard_setup(self, v_begin: int, v_end: int) -> None:
+        check(_lib.load().gdx_sssp_shard_setup(self.handle, int(v_begin), int(v_end)))
+
+    def sssp_shard_frontier(self, dist, prev) -> int:
+        c = np.zeros(1, np.int64)
+        check(_lib.load().gdx_sssp_shard_frontier(self.handle, _ptr(dist), _ptr(prev), _ptr(c)))
+        return int(c[0])
+
+    def sssp_shard_relax(self, dist) -> None:
+        check(_lib.load().gdx_sssp_shard_relax(self.handle, _ptr(dist)))
 
     # ---- measurement -----------------------------------------------------------
     def profile(self, enable: bool = True) -> None:

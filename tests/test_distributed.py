@@ -8,6 +8,7 @@ import socket
 
 import numpy as np
 import pytest
+import torch
 import torch.multiprocessing as mp
 
 from conftest import ROOT
@@ -63,8 +64,62 @@ class OracleExecutor:
     def offsets(self):
         return self.g.offsets
 
+    def rev_offsets(self):
+        return self.g.rev_offsets
+
     def num_nodes(self):
         return self.g.n
+
+    # --- PR shard: numpy restatement of gdx_pr_shard_* (pr.sp:17-30 per row) ---
+    def pr_setup(self, v0, v1):
+        self.v0, self.v1 = v0, v1
+
+    def pr_init(self, contrib_slice, partials):
+        n, v0, v1 = self.g.n, self.v0, self.v1
+        r0 = 1.0 / n
+        od = np.diff(self.g.offsets)[v0:v1]
+        contrib_slice[:v1 - v0] = torch.from_numpy(np.where(od > 0, r0 / np.maximum(od, 1), 0.0))
+        partials[0] = r0 * float((od == 0).sum())
+        partials[1] = 0.0
+        self.rank = np.full(v1 - v0, r0)
+
+    def pr_round(self, rnd, damping, threshold, max_iter, dangling_in, contrib, contrib_slice,
+                 partials):
+        n, v0, v1 = self.g.n, self.v0, self.v1
+        c = contrib.numpy()
+        roff, src = self.g.rev_offsets, self.g.rev_srcs
+        sums = np.zeros(v1 - v0)
+        for i, v in enumerate(range(v0, v1)):
+            sums[i] = c[src[roff[v]:roff[v + 1]]].sum()
+        new = (1.0 - damping) / n + damping * (float(dangling_in[0]) / n + sums)
+        unsettled = bool(np.any(np.abs(new - self.rank) >= threshold)) and rnd < max_iter
+        od = np.diff(self.g.offsets)[v0:v1]
+        contrib_slice[:v1 - v0] = torch.from_numpy(np.where(od > 0, new / np.maximum(od, 1), 0.0))
+        partials[0] = float(new[od == 0].sum())
+        partials[1] = 1.0 if unsettled else 0.0
+        self.rank = new
+
+    def pr_rank(self, rounds, rank_slice):
+        rank_slice[:self.v1 - self.v0] = torch.from_numpy(self.rank)
+
+    # --- SSSP shard: numpy restatement of gdx_sssp_shard_* ---
+    def sssp_setup(self, v0, v1):
+        self.s0, self.s1 = v0, v1
+
+    def sssp_frontier(self, dist, prev):
+        d, p = dist.numpy(), prev.numpy()
+        own = np.arange(self.s0, self.s1)
+        self.front = own[d[own] < p[own]]
+        p[self.front] = d[self.front]
+        return len(self.front)
+
+    def sssp_relax(self, dist):
+        d = dist.numpy()
+        off, dst = self.g.offsets, self.g.dests
+        w = self.g.weights if self.g.weights is not None else np.ones(self.g.m, np.int32)
+        for v in self.front:
+            e = slice(off[v], off[v + 1])
+            np.minimum.at(d, dst[e], d[v] + w[e].astype(np.int64))
 
 
 def _worker(rank, world, port, q):
@@ -103,3 +158,52 @@ def test_sharded_tc_bc_gloo_world2():
     assert tc == tc_exp
     scale = np.maximum(np.maximum(np.abs(bc), np.abs(bc_exp)), 1e-12)
     assert float(np.max(np.abs(bc - bc_exp) / scale)) < 1e-12
+
+
+def _worker_pr_sssp(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+    from oracle import Port
+    D.init_from_env("gloo")
+    p = Port()
+    n = 1 << 10
+    u, v = p.gen_rmat_edges(n, 8 * n, 9)
+    gd = p.build_from_edges(n, u, v, None, True)
+    rank_v, rounds = D.sharded_pr(OracleExecutor(gd), 0.85, 1e-9, 110)
+    gu = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1, 100, 9)
+    d0 = D.sharded_sssp(OracleExecutor(gu), 0)
+    d5 = D.sharded_sssp(OracleExecutor(gu), 5)
+    if rank == 0:
+        exp_r, exp_rounds = p.pr(gd, 0.85, 1e-9, 110)
+        q.put((rank_v, rounds, exp_r, exp_rounds, d0, p.sssp(gu, 0), d5, p.sssp(gu, 5)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pr_sssp_gloo(world):
+    """Vertex-range PR (all-gather of contrib slices + all-reduce of the
+    partials) and SSSP (MIN all-reduce of the dist replicas) against the
+    single-process oracle: same PR rounds, PR within 1e-12, SSSP bit-exact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker_pr_sssp, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    r, rounds, er, erounds, d0, e0, d5, e5 = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert rounds == erounds
+    assert float(np.max(np.abs(r - er) / np.abs(er))) < 1e-12
+    assert np.array_equal(d0, e0) and np.array_equal(d5, e5)
+
+
+def test_pr_ranges_balance_in_edges():
+    roff = np.array([0, 50, 50, 51, 52, 100], np.int64)
+    r = D.pr_ranges(roff, 2)
+    assert r[0][0] == 0 and r[-1][1] == 5 and r[0][1] == r[1][0]

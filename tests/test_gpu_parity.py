@@ -10,7 +10,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import G, known_graph, rel_err, reverse_of, sweep_graphs
+from conftest import G, ROOT, known_graph, rel_err, reverse_of, sweep_graphs
 
 pytestmark = pytest.mark.gpu
 INF = (2**63 - 1) // 2
@@ -306,3 +306,54 @@ def test_sssp_warp_chunk_queue(gdx, port, stage, monkeypatch):
     dg = gdx.DeviceGraph.from_csr(g)
     for src in (0, 999):
         assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
+
+
+# ---- multi-GPU shards through the real kernels ------------------------------------------
+
+def _gpu_shard_worker(rank, world, port, q):
+    import os
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0")
+    import torch.distributed as tdist
+    import paper_2401_02472_b200 as G
+    from paper_2401_02472_b200 import distributed as D
+    from oracle import Port
+    # every rank shares cuda:0, so the collectives go over gloo (CPU-staged);
+    # on the GPU box's multi-GPU runs the same code uses NCCL on device tensors
+    D.init_from_env("gloo")
+    p = Port()
+    n = 1 << 12
+    u, v = p.gen_rmat_edges(n, 16 * n, 21)
+    gd = p.build_from_edges(n, u, v, None, True)
+    gu = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1, 100, 21)
+    r, rounds = D.sharded_pr(D.DeviceExecutor(G.DeviceGraph.from_csr(gd)), 0.85, 1e-9, 110)
+    d = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gu)), 7)
+    if rank == 0:
+        er, erounds = p.pr(gd, 0.85, 1e-9, 110)
+        q.put((r, rounds, er, erounds, d, p.sssp(gu, 7)))
+    tdist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_pr_sssp_device(gdx, world):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    r, rounds, er, erounds, d, ed = q.get(timeout=500)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert rounds == erounds
+    assert rel_err(r, er) < 1e-12
+    assert np.array_equal(d, ed)
