@@ -11,9 +11,9 @@ SSSP RMAT-26 C5 with ~2.1e9 stored edges, checked by an on-device certificate).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--algos sssp,tc,bc,sssp26] [--no-cpu-baseline]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL); the N ranks run
-independent replicas of the step, timing is the
-max over ranks.  `--impl reference` times the reference's own CPU path
+N > 1 is launched by torchrun (one rank per GPU, NCCL): PageRank (headline),
+TC, BC and C5 SSSP run partitioned across the ranks (distributed.py; strong
+scaling -- the graph is fixed), timing is the max over ranks.  `--impl reference` times the reference's own CPU path
 (oracle/_ref: interp::run in parallel mode on all host cores) on a bounded
 sample of the same workload.
 """
@@ -117,9 +117,9 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
 
-    def init(self, torch):
+    def init(self, torch, force: bool = False):
         torch.cuda.set_device(self.local)
-        if self.world > 1:
+        if self.world > 1 or force:
             import torch.distributed as dist
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
@@ -416,17 +416,170 @@ def bench_bc(torch, gdx, dist, args, pk) -> dict:
     return res
 
 
+# --------------------------------------------------------------- sharded (N > 1) arm
+
+def _shard_roofline(prof, kernels, algo_bytes, pk, launches):
+    r = roofline(prof, kernels, algo_bytes, pk, work_launches=launches)
+    r["scope"] = "rank 0's kernels and rank 0's share of the algorithmic bytes"
+    return r
+
+
+def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
+    """C2 PageRank partitioned over the ranks by destination-vertex ranges
+    (distributed.sharded_pr): per round one NCCL all-gather of the contrib
+    slices and one all-reduce of (dangling, unsettled).  Strong scaling: the
+    graph is fixed, every rank computes its rows."""
+    from paper_2401_02472_b200 import distributed as D
+    dg = gdx.DeviceGraph.generate("rmat", 1 << 24, 1 << 28, seed=1, directed=True,
+                                  device=dist.local)
+    n, m = dg.n, dg.m
+    ex = D.DeviceExecutor(dg)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def step():
+        _, rounds = D.sharded_pr(ex, 0.85, 1e-6, 100, to_host=False)
+        return rounds
+
+    dg.profile(True)
+    for _ in range(args.warmup):
+        step()
+    dg.profile_reset()
+    with Clocks(dist.local) as clk:
+        ms, wall, rounds = timed_steps(torch, dist, step, args.steps, 0, flush)
+    prof = dg.profile_read()
+    dg.profile(False)
+    total_ms = dist.max(torch, sum(ms))
+    ranges = D.pr_ranges(ex.rev_offsets(), dist.world)
+    roff = ex.rev_offsets()
+    v0, v1 = ranges[dist.rank]
+    e_r = int(roff[v1]) - int(roff[v0])
+    res = {
+        "workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 tol=1e-6 maxIter=100",
+        "n": n, "m": m, "rounds": rounds[-1],
+        "gteps": float(m) * sum(rounds) / (total_ms * 1e-3) / 1e9,
+        "ms_per_step": total_ms / args.steps, "wall_ms": wall,
+        "roofline": _shard_roofline(prof, "pr_edges+pr_vertices",
+                                    sum(rounds) * (12.0 * e_r + 32.0 * (v1 - v0)), pk, sum(rounds)),
+        "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
+        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
+        "partition": {"ranges": ranges, "rank0_edges": e_r},
+    }
+    # e2e: every rank uploads the host CSR through the C ABI, runs the sharded
+    # fixedPoint and gathers the full rank vector to the host
+    h = dg.download()
+    pin = {k: torch.from_numpy(getattr(h, k)).pin_memory() for k in ("offsets", "rev_offsets", "rev_srcs")}
+
+    class View:
+        pass
+
+    v = View()
+    v.n, v.m, v.directed = n, m, True
+    v.offsets, v.rev_offsets, v.rev_srcs = pin["offsets"], pin["rev_offsets"], pin["rev_srcs"]
+    v.dests = v.weights = v.rev_eid = None
+
+    def e2e_step():
+        g2 = gdx.DeviceGraph.from_csr(v, device=dist.local)
+        _, r = D.sharded_pr(D.DeviceExecutor(g2), 0.85, 1e-6, 100, to_host=True)
+        g2.close()
+        return r
+
+    dg.close()
+    e2e_step()
+    dist.barrier(torch)
+    t0 = time.perf_counter()
+    rr = [e2e_step() for _ in range(args.steps)]
+    e2e_s = dist.max(torch, time.perf_counter() - t0)
+    res["e2e"] = {"value": float(m) * sum(rr) / e2e_s / 1e9, "unit": "GTEPS",
+                  "h2d_bytes_per_step": int(sum(t.numel() * 4 for t in pin.values())),
+                  "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3 / args.steps,
+                  "path": "per rank: gdx_graph_create(host CSR) + sharded_pr (NCCL) + host rank"}
+    return res
+
+
+def bench_sharded_other(torch, gdx, dist, args, pk, algo: str) -> dict:
+    """C3 TC (owner-vertex ranges + one all-reduce), C4 BC (source blocks + one
+    all-reduce of bc), C5 SSSP (vertex ranges, MIN all-reduce per round)."""
+    import numpy as np
+    from paper_2401_02472_b200 import distributed as D
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    if algo == "tc":
+        dg = gdx.DeviceGraph.generate("uniform", 1 << 24, 1 << 27, seed=1, directed=False,
+                                      device=dist.local)
+        ex = D.DeviceExecutor(dg)
+        ex.offsets()
+
+        def step():
+            return D.sharded_tc(ex)
+        units, name, kern = float(dg.m), "C3 TC uniform 2^24 vertices, 2^27 draws, undirected", \
+            "tc+tc_orient+tc_orient_fill"
+    elif algo == "bc":
+        side = 4899
+        dg = gdx.DeviceGraph.generate("grid", side, seed=1, keep=0.55, directed=False,
+                                      device=dist.local)
+        ex = D.DeviceExecutor(dg)
+        deg = np.diff(ex.offsets())
+        rng = np.random.default_rng(1)
+        sources = sorted(rng.choice(np.flatnonzero(deg > 0), size=args.bc_sources,
+                                    replace=False).tolist())
+
+        def step():
+            return D.sharded_bc(ex, sources)
+        units, name, kern = float(dg.m) * len(sources), \
+            f"C4 BC {len(sources)} sources, {side}^2 grid keep 0.55 undirected", "bc_forward"
+    else:  # sssp26
+        dg = gdx.DeviceGraph.generate("rmat", 1 << 26, 1 << 30, seed=1, directed=False,
+                                      weights=(1, 100), device=dist.local)
+        ex = D.DeviceExecutor(dg)
+        ex.offsets()
+        st = {}
+
+        def step():
+            return D.sharded_sssp(ex, 0, to_host=False, stats=st)
+        units, name, kern = float(dg.m), \
+            "C5 SSSP RMAT-26 ef16 undirected, weights U[1,100], src 0", "sssp_shard_relax"
+    dg.profile(True)
+    for _ in range(1 if algo != "tc" else args.warmup):
+        step()
+    dg.profile_reset()
+    steps = max(1, args.steps // 2) if algo == "bc" else args.steps
+    ms, wall, outs = timed_steps(torch, dist, step, steps, 0, flush)
+    prof = dg.profile_read()
+    total = dist.max(torch, sum(ms))
+    res = {"workload": name, "n": dg.n, "m": dg.m, "steps": steps,
+           "gteps": units * steps / (total * 1e-3) / 1e9, "ms_per_step": total / steps,
+           "parallelism": f"sharded x{dist.world}", "scaling": "strong",
+           "gpu_launches": int(sum(v[1] for v in prof.values())),
+           "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()}}
+    if algo == "tc":
+        res["triangles"] = outs[-1]
+    if algo == "sssp26":
+        res["rounds"] = st.get("rounds")
+        res["certificate_ok"] = sssp_certificate(torch, dg, outs[-1])
+    dg.close()
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args) -> None:
     import torch
 
     import paper_2401_02472_b200 as gdx
     dist = Dist()
-    dist.init(torch)
+    dist.init(torch, force=args.sharded)
     pk = peaks()
     algos = [a for a in args.algos.split(",") if a]
     cpu = dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline
     per = {}
-    head = bench_pr(torch, gdx, dist, args, pk, cpu)
+    sharded = dist.world > 1 or args.sharded
+    if sharded:
+        head = bench_pr_sharded(torch, gdx, dist, args, pk)
+        for a in algos:
+            if a in ("tc", "bc", "sssp26"):
+                per["sssp_c5" if a == "sssp26" else a] = bench_sharded_other(torch, gdx, dist,
+                                                                             args, pk, a)
+        algos = []  # C1 SSSP is a single-GPU config
+    else:
+        head = bench_pr(torch, gdx, dist, args, pk, cpu)
     for a in algos:
         if a == "sssp":
             per["sssp"] = bench_sssp(torch, gdx, dist, args, pk)
@@ -441,11 +594,12 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": round(head["gteps"], 3), "unit": "GTEPS",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(head["ms_per_step"], 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: counter-based RMAT generator (a,b,c,d=.57,.19,.19,.05), seed 1, built on GPU",
         "config": {"workload": head["workload"], "graph": "rmat-24", "n": head["n"], "m": head["m"],
                    "pr_rounds": head["rounds"], "damping": 0.85, "threshold": 1e-6, "max_iter": 100,
-                   "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
+                   "parallelism": (f"vertex-range shards x{dist.world} (NCCL all-gather of contrib "
+                                   "slices + all-reduce per round)") if sharded else "single",
                    "l2": "flushed (512 MB write) before every timed step"},
         "roofline": head["roofline"], "e2e": head["e2e"], "clocks": head["clocks"],
         "gpu_launches": head["gpu_launches"], "kernels": head["kernels"],
@@ -514,6 +668,8 @@ def main() -> None:
     ap.add_argument("--bc-sources", type=int, default=64)
     ap.add_argument("--ref-scale", type=int, default=18)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU sharded path even at N=1 (torchrun, NCCL)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

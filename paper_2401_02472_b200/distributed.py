@@ -155,7 +155,9 @@ class DeviceExecutor:
         return out
 
     def pr_setup(self, v0, v1):
-        self.g.pr_shard_setup(v0, v1)
+        if getattr(self, "_pr_range", None) != (v0, v1):  # the plan is cached per range
+            self.g.pr_shard_setup(v0, v1)
+            self._pr_range = (v0, v1)
 
     def pr_init(self, contrib_slice, partials):
         self._staged(self.g.pr_shard_init, contrib_slice, partials)
@@ -170,7 +172,9 @@ class DeviceExecutor:
         self._staged(lambda r: self.g.pr_shard_rank(rounds, r), rank_slice)
 
     def sssp_setup(self, v0, v1):
-        self.g.sssp_shard_setup(v0, v1)
+        if getattr(self, "_sssp_range", None) != (v0, v1):
+            self.g.sssp_shard_setup(v0, v1)
+            self._sssp_range = (v0, v1)
 
     def sssp_frontier(self, dist, prev):
         return self._staged(self.g.sssp_shard_frontier, dist, prev)
@@ -186,6 +190,21 @@ def _dist():
     return dist
 
 
+def _cached_ranges(ex, kind: str, world: int, make):
+    """Partitions are a pure function of the graph: computed once per executor."""
+    cache = getattr(ex, "_range_cache", None)
+    if cache is None:
+        cache = {}
+        try:
+            ex._range_cache = cache
+        except AttributeError:
+            return make()
+    key = (kind, world)
+    if key not in cache:
+        cache[key] = make()
+    return cache[key]
+
+
 def _device_for_collectives():
     import torch
     import torch.distributed as dist
@@ -199,7 +218,7 @@ def sharded_tc(ex: Executor, group=None) -> int:
     import torch
     dist = _dist()
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    v0, v1 = tc_ranges(ex.offsets(), world)[rank]
+    v0, v1 = _cached_ranges(ex, "tc", world, lambda: tc_ranges(ex.offsets(), world))[rank]
     local = ex.tc_range(v0, v1)
     t = torch.tensor([local], dtype=torch.int64, device=_device_for_collectives())
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
@@ -239,8 +258,10 @@ def pr_ranges(rev_offsets: np.ndarray, parts: int) -> list[tuple[int, int]]:
     return balanced_ranges(indeg + 1.0, parts)
 
 
-def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, group=None):
-    """ComputePR across ranks -> (rank f64[n] numpy, rounds).  Raises
+def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, group=None,
+               to_host: bool = True):
+    """ComputePR across ranks -> (rank f64[n], rounds): numpy, or the
+    collective-device tensor when ``to_host`` is False.  Raises
     GraphdslError("NonTermination") like gdx_pagerank when the interpreter's
     fixedPoint cap 10n+100 is hit before max_iter+1 rounds."""
     import torch
@@ -251,7 +272,7 @@ def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, gr
     n = ex.num_nodes()
     if n == 0:
         raise GraphdslError("RuntimeError", "RuntimeError: division by zero")
-    ranges = pr_ranges(ex.rev_offsets(), world)
+    ranges = _cached_ranges(ex, "pr", world, lambda: pr_ranges(ex.rev_offsets(), world))
     v0, v1 = ranges[rank]
     chunk = max(max(b - a for a, b in ranges), 1)
     f64 = dict(dtype=torch.float64, device=dev)
@@ -283,11 +304,12 @@ def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, gr
     ex.pr_rank(rounds, rank_slice)
     out = torch.zeros(n, **f64)
     _all_gather_slices(rank_slice, ranges, out, group)
-    return out.cpu().numpy(), rounds
+    return (out.cpu().numpy() if to_host else out), rounds
 
 
-def sharded_sssp(ex: Executor, src: int, group=None) -> np.ndarray:
-    """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact."""
+def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats=None):
+    """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact;
+    numpy, or the collective-device tensor when ``to_host`` is False."""
     import torch
     from ._lib import GraphdslError
     dist = _dist()
@@ -296,7 +318,7 @@ def sharded_sssp(ex: Executor, src: int, group=None) -> np.ndarray:
     n = ex.num_nodes()
     if not 0 <= src < n:
         raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
-    v0, v1 = vertex_ranges(ex.offsets(), world)[rank]
+    v0, v1 = _cached_ranges(ex, "sssp", world, lambda: vertex_ranges(ex.offsets(), world))[rank]
     ex.sssp_setup(v0, v1)
     inf = (2**63 - 1) // 2
     d = torch.full((n,), inf, dtype=torch.int64, device=dev)
@@ -308,7 +330,9 @@ def sharded_sssp(ex: Executor, src: int, group=None) -> np.ndarray:
         cnt.fill_(ex.sssp_frontier(d, prev))
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
         if int(cnt.item()) == 0:
-            return d.cpu().numpy()
+            if stats is not None:
+                stats["rounds"] = _ + 1
+            return d.cpu().numpy() if to_host else d
         ex.sssp_relax(d)
         dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
     raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} iterations")
