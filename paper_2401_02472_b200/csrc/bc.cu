@@ -261,6 +261,267 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-per-source mode (high-diameter graphs, many sources).  A road-like grid
+// has ~10^4 BFS levels of a few thousand vertices: the grid-wide kernels above
+// spend ~25 us per level in grid.sync and cross-CTA queue atomics.  Here one
+// 1024-thread CTA runs a whole source (forward and backward) with
+// __syncthreads() as the level barrier and a shared-memory queue tail; the
+// CTAs of the grid take different sources, so up to #SM sources run
+// concurrently with no grid-wide synchronisation at all.  Same arithmetic and
+// summation orders as the grid kernels.
+// ---------------------------------------------------------------------------
+constexpr int kBcCta = 1024;
+
+struct BcCtaArgs {
+    int32_t n;
+    int32_t nsrc;
+    bool undirected;
+    const int32_t* __restrict__ offsets;
+    const int32_t* __restrict__ dests;
+    const int32_t* __restrict__ in_offsets;
+    const int32_t* __restrict__ in_srcs;
+    const int32_t* __restrict__ sources;
+    int32_t* level;    // [grid][n], -1 = undiscovered (restored after each source)
+    double2* sig;      // [grid][n]
+    double* delta;     // [grid][n]
+    int32_t* log;      // [grid][n]   discovery order, levels contiguous
+    int32_t* loff;     // [grid][n+2] level boundaries in log
+    double* bc;
+    unsigned long long* ctr;
+};
+
+// CS CTAs (a thread-block cluster) share one source: the level barrier is a
+// cluster barrier and the queue tail lives in CTA 0's shared memory (DSMEM
+// atomics), so a source's levels are spread over CS * 1024 threads.
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(BcCtaArgs a) {
+    __shared__ int s_next_local[2];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = int(cluster.block_rank());
+    int* s_next = cluster.map_shared_rank(s_next_local, 0);
+    const int tid = crank * kBcCta + int(threadIdx.x);
+    const int ltid = threadIdx.x;
+    constexpr int kStride = CS * kBcCta;
+    const int64_t slot = blockIdx.x / CS;
+    const int32_t nslots = gridDim.x / CS;
+    int32_t* lev = a.level + slot * a.n;
+    double2* sig = a.sig + slot * a.n;
+    double* delta = a.delta + slot * a.n;
+    int32_t* log = a.log + slot * a.n;
+    int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
+    unsigned long long reached = 0, fscan = 0, bscan = 0, dag = 0, levels_max = 0;
+    for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
+        const int32_t src = a.sources[si];
+        if (tid == 0) {
+            lev[src] = 0;
+            log[0] = src;
+            loff[0] = 0;
+            s_next[0] = s_next[1] = 0;
+        }
+        cluster.sync();
+        // ---- forward: iterateInBFS ----
+        int beg = 0, end = 1, L = 0;
+        for (;; ++L) {
+            for (int i = beg + tid; i < end; i += kStride) {
+                const int32_t v = log[i];
+                double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
+                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+                fscan += oe - ob;
+                for (int32_t e = ob; e < oe; e += kNb) {
+                    int32_t w[kNb], lw[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) lw[k] = w[k] >= 0 ? lev[w[k]] : -2;
+                    double2 sg[kNb];
+                    bool par[kNb], got[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        par[k] = a.undirected && L > 0 && lw[k] == L - 1;
+                        sg[k] = par[k] ? sig[w[k]] : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k)
+                        got[k] = lw[k] == -1 && atomicCAS(&lev[w[k]], -1, L + 1) == -1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        if (par[k]) {  // ascending parent order
+                            acc = xf_add(acc, sg[k]);
+                            ++dag;
+                        }
+                        if (got[k]) log[end + atomicAdd(&s_next[L & 1], 1)] = w[k];
+                    }
+                }
+                if (!a.undirected && L > 0) {
+                    const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
+                    fscan += ie - ib;
+                    for (int32_t e = ib; e < ie; e += kNb) {
+                        int32_t p[kNb];
+                        bool par[kNb];
+                        double2 sg[kNb];
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k) p[k] = e + k < ie ? a.in_srcs[e + k] : -1;
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k) par[k] = p[k] >= 0 && lev[p[k]] == L - 1;
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            sg[k] = par[k] ? sig[p[k]] : make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            if (par[k]) {
+                                acc = xf_add(acc, sg[k]);
+                                ++dag;
+                            }
+                    }
+                }
+                sig[v] = acc;
+            }
+            cluster.sync();
+            const int next = s_next[L & 1];
+            if (tid == 0) {
+                s_next[(L + 1) & 1] = 0;
+                loff[L + 1] = end;
+            }
+            cluster.sync();
+            if (next == 0) break;
+            beg = end;
+            end += next;
+        }
+        const int levels = L + 1;  // loff[0..levels] bound the levels in log
+        if (tid == 0) {
+            reached += end;
+            levels_max = max(levels_max, (unsigned long long)levels);
+        }
+        // ---- backward: iterateInReverse ----
+        for (int Lb = levels - 1; Lb >= 0; --Lb) {
+            const int b0 = loff[Lb], b1 = loff[Lb + 1];
+            for (int i = b0 + tid; i < b1; i += kStride) {
+                const int32_t v = log[i];
+                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+                const double2 sv = sig[v];
+                double d = 0.0;
+                bscan += oe - ob;
+                for (int32_t e = ob; e < oe; e += kNb) {
+                    int32_t w[kNb];
+                    bool ch[kNb];
+                    double2 sw[kNb];
+                    double dw[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) ch[k] = w[k] >= 0 && lev[w[k]] == Lb + 1;
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        sw[k] = ch[k] ? sig[w[k]] : make_double2(1.0, 0.0);
+                        dw[k] = ch[k] ? delta[w[k]] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k)
+                        if (ch[k] && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
+                            d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
+                            ++dag;
+                        }
+                }
+                delta[v] = d;
+                if (v != src) atomicAdd(&a.bc[v], d);
+            }
+            cluster.sync();
+        }
+        // restore `level` for the slot's next source
+        for (int i = tid; i < end; i += kStride) lev[log[i]] = -1;
+        cluster.sync();
+    }
+    for (int o = 16; o; o >>= 1) {
+        fscan += __shfl_xor_sync(0xffffffffu, fscan, o);
+        bscan += __shfl_xor_sync(0xffffffffu, bscan, o);
+        dag += __shfl_xor_sync(0xffffffffu, dag, o);
+    }
+    if ((ltid & 31) == 0) {
+        atomicAdd(&a.ctr[kFwdScan], fscan);
+        atomicAdd(&a.ctr[kBwdScan], bscan);
+        atomicAdd(&a.ctr[kDag], dag);
+    }
+    if (tid == 0) {
+        atomicAdd(&a.ctr[kReached], reached);
+        atomicMax(&a.ctr[kLevels], levels_max);
+    }
+}
+
+static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
+                       unsigned long long* totals, int& launches, int& max_levels) {
+    auto& W = *g->bc;
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    const int32_t nsrc = int32_t(hsrc.size());
+    // cluster size: spread each source over CS SMs while there are SMs to spare
+    const char* csv = std::getenv("GDX_BC_CLUSTER");
+    int CS = 1;
+    if (csv)
+        CS = std::atoi(csv);
+    else
+        while (CS < 4 && int64_t(2 * CS) * std::min<int32_t>(nsrc, g->num_sms) <= g->num_sms) CS *= 2;
+    if (CS != 1 && CS != 2 && CS != 4) CS = 1;
+    const int slots = std::max(1, std::min<int32_t>(nsrc, g->num_sms / CS));
+    const int grid = slots * CS;
+    if (W.cta_grid < slots) {
+        W.level.release();
+        W.sig.release();
+        W.delta.release();
+        W.log.release();
+        W.cta_log.release();
+        W.cta_loff.release();
+        W.batch = 0;
+        W.level.alloc(size_t(slots) * n);
+        W.sig.alloc(size_t(slots) * n * 2);
+        W.delta.alloc(size_t(slots) * n);
+        W.cta_log.alloc(size_t(slots) * n);
+        W.cta_loff.alloc(size_t(slots) * (n + 2));
+        W.cta_grid = slots;
+        GDX_CUDA(cudaMemsetAsync(W.level.get(), 0xff, W.level.bytes(), s));
+    }
+    W.sources.ensure(size_t(nsrc));
+    GDX_CUDA(cudaMemcpyAsync(W.sources.get(), hsrc.data(), size_t(nsrc) * 4,
+                             cudaMemcpyHostToDevice, s));
+    GDX_CUDA(cudaMemsetAsync(W.ctrs.get(), 0, kBcCtrs * 8, s));
+    BcCtaArgs a;
+    a.n = g->n;
+    a.nsrc = nsrc;
+    a.undirected = !g->directed;
+    a.offsets = g->offsets.get();
+    a.dests = g->dests.get();
+    a.in_offsets = g->rev_offsets.get();
+    a.in_srcs = g->rev_srcs.get();
+    a.sources = W.sources.get();
+    a.level = W.level.get();
+    a.sig = reinterpret_cast<double2*>(W.sig.get());
+    a.delta = W.delta.get();
+    a.log = W.cta_log.get();
+    a.loff = W.cta_loff.get();
+    a.bc = W.bc.get();
+    a.ctr = W.ctrs.get();
+    if (g->directed && (!a.in_offsets || !a.in_srcs))
+        fail(GDX_ERR_UNSUPPORTED, "Unsupported: directed BC needs the reverse CSR");
+    timed_launch(g, "bc_cta", [&] {
+        if (CS == 4)
+            k_bc_cta<4><<<grid, kBcCta, 0, s>>>(a);
+        else if (CS == 2)
+            k_bc_cta<2><<<grid, kBcCta, 0, s>>>(a);
+        else
+            k_bc_cta<1><<<grid, kBcCta, 0, s>>>(a);
+    });
+    ++launches;
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    totals[kReached] += h[kReached];
+    totals[kFwdScan] += h[kFwdScan];
+    totals[kBwdScan] += h[kBwdScan];
+    totals[kDag] += h[kDag];
+    max_levels = std::max<int>(max_levels, int(h[kLevels]));
+}
+
 }  // namespace gdx
 
 using namespace gdx;
@@ -289,7 +550,23 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         GDX_CUDA(cudaMemsetAsync(W.bc.get(), 0, n * sizeof(double), s));
         unsigned long long totals[kBcCtrs] = {};
         int launches = 0, max_levels = 0;
-        if (nsrc > 0) {
+        // CTA-per-source mode when there are enough sources to fill the GPU
+        // with independent BFS trees (GDX_BC_MODE=grid|cta overrides).
+        const char* mode = std::getenv("GDX_BC_MODE");
+        const bool cta_mode = mode ? std::string(mode) == "cta"
+                                   : nsrc >= std::max(16, g->num_sms / 4);
+        if (nsrc > 0 && cta_mode) {
+            run_bc_cta(g, hsrc, totals, launches, max_levels);
+        } else if (nsrc > 0) {
+            if (W.cta_grid > 0) {  // switch back from CTA mode: its buffers are sized differently
+                W.level.release();
+                W.sig.release();
+                W.delta.release();
+                W.cta_log.release();
+                W.cta_loff.release();
+                W.cta_grid = 0;
+                W.batch = 0;
+            }
             // batch size: 36 bytes per (source, vertex) of state + log
             size_t free_b = 0, tot_b = 0;
             GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));

@@ -79,6 +79,10 @@ struct BcWork {
     size_t log_cap = 0;
     int grid = 0;
     int block = 0;
+    // CTA-per-source mode (k_bc_cta): one state slot per CTA
+    int32_t cta_grid = 0;
+    DevBuf<int32_t> cta_log;    // [cta_grid][n]
+    DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
 };
 
 }  // namespace gdx

@@ -239,7 +239,19 @@ def test_tc(gdx, port, kind, scale, directed):
 
 # ---- Betweenness centrality ------------------------------------------------------------
 
-def test_bc_rmat(gdx, port):
+@pytest.fixture(params=["grid", "cta", "cta1", "cta2"])
+def bc_mode(request, monkeypatch):
+    """Both BC executions: grid-wide level-synchronous kernels, and one CTA
+    cluster per source (the default once there are >= max(16, #SM/4) sources)
+    with the cluster size picked from the SM count, or forced to 1 / 2."""
+    mode = request.param
+    monkeypatch.setenv("GDX_BC_MODE", "grid" if mode == "grid" else "cta")
+    if mode in ("cta1", "cta2"):
+        monkeypatch.setenv("GDX_BC_CLUSTER", mode[-1])
+    return mode
+
+
+def test_bc_rmat(gdx, port, bc_mode):
     n = 1 << 12
     u, v = port.gen_rmat_edges(n, 8 * n, 21)
     for directed in (False, True):
@@ -249,7 +261,7 @@ def test_bc_rmat(gdx, port):
         assert rel_err(dg.bc(srcs), port.bc(g, srcs)) < 1e-9, directed
 
 
-def test_bc_grid_and_overflow(gdx, port):
+def test_bc_grid_and_overflow(gdx, port, bc_mode):
     gu, gv = port.gen_grid_ctr(100, 0.55, 3)
     g = port.build_from_edges(100 * 100, gu, gv, None, False)
     srcs = [0, 4242, 9999, 5050]
@@ -260,6 +272,19 @@ def test_bc_grid_and_overflow(gdx, port):
     got = gdx.DeviceGraph.from_csr(g).bc([0])
     assert np.isfinite(got).all()
     assert rel_err(got, port.bc(g, [0])) < 1e-6
+
+
+def test_bc_many_sources_slot_reuse(gdx, port):
+    """More sources than CTAs: the default picks CTA mode and every CTA slot is
+    reused for several sources (its level array restored in between)."""
+    gu, gv = port.gen_grid_ctr(60, 0.6, 5)
+    g = port.build_from_edges(3600, gu, gv, None, False)
+    srcs = list(range(0, 3600, 11))  # 328 sources > #SM
+    dg = gdx.DeviceGraph.from_csr(g)
+    st = {}
+    got = dg.bc(srcs, stats=st)
+    assert st["launches"] == 1  # one k_bc_cta launch
+    assert rel_err(got, port.bc(g, srcs)) < 1e-9
 
 
 # ---- GPU generators == their CPU twin ---------------------------------------------------
