@@ -43,6 +43,7 @@ struct PrPlan {
 // SSSP frontier workspace (sssp.cu).
 struct SsspWork {
     DevBuf<uint64_t> dist;   // 32- or 64-bit distances (reinterpreted)
+    DevBuf<uint64_t> prev;   // frontier-scan mode: distance at the last expansion
     DevBuf<int32_t> stamp;   // round at which a vertex was last enqueued
     DevBuf<int2> queue[2];   // work items (vertex, first edge)
     DevBuf<unsigned long long> ctrs;  // rotating counters + stats
@@ -53,7 +54,7 @@ struct SsspWork {
     bool shard_ready = false;
     int32_t shard_v0 = 0, shard_v1 = 0;
     DevBuf<int2> shard_queue;
-    DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks]
+    DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges]
 };
 
 // Triangle-counting workspace (tc.cu).

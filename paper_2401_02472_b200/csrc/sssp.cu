@@ -357,59 +357,199 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
 // ---------------------------------------------------------------------------
 constexpr int kShardChunk = 128;  // edges per relaxation item
 
-__global__ void k_sssp_shard_frontier(int32_t v0, int32_t v1, const int32_t* __restrict__ offsets,
-                                      const long long* __restrict__ dist, long long* prev,
-                                      int2* queue, unsigned long long* ctr) {
+// Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
+// distance dropped since they were last expanded (dist < prev; prev := dist).
+// One global atomic per block-chunk of 2048 vertices.
+template <class D>
+__global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t v1,
+                                                           const int32_t* __restrict__ offsets,
+                                                           const D* __restrict__ dist, D* prev,
+                                                           int2* queue,
+                                                           unsigned long long* ctr) {
+    constexpr int kPer = 8;  // vertices per thread per chunk
     const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = v0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane);
-         base < v1; base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = base + lane;
-        int items = 0;
-        int32_t b = 0;
-        if (v < v1) {
-            const long long d = dist[v];
-            if (d < prev[v]) {
-                prev[v] = d;
-                b = offsets[v];
-                const int32_t deg = offsets[v + 1] - b;
-                items = deg > 0 ? (deg + kShardChunk - 1) / kShardChunk : 0;
-                if (deg == 0) atomicAdd(&ctr[1], 1ull);  // improved but nothing to relax
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int s_warp[8];
+    __shared__ unsigned long long s_base;
+    for (int64_t c0 = v0 + int64_t(blockIdx.x) * 256 * kPer; c0 < v1;
+         c0 += int64_t(gridDim.x) * 256 * kPer) {
+        int items[kPer], first[kPer];
+        int mine = 0, sinks = 0;
+        unsigned long long vis = 0, edg = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            items[k] = 0;
+            first[k] = 0;
+            if (v < v1) {
+                const D d = dist[v];
+                if (d < prev[v]) {
+                    prev[v] = d;
+                    const int32_t b = offsets[v], deg = offsets[v + 1] - b;
+                    first[k] = b;
+                    items[k] = (deg + kShardChunk - 1) / kShardChunk;
+                    sinks += deg == 0;
+                    ++vis;
+                    edg += deg;
+                }
             }
+            mine += items[k];
         }
-        int incl = items;
+        if (sinks) atomicAdd(&ctr[1], (unsigned long long)sinks);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            vis += __shfl_xor_sync(full, vis, o);
+            edg += __shfl_xor_sync(full, edg, o);
+        }
+        if (lane == 0 && vis) {
+            atomicAdd(&ctr[3], vis);
+            atomicAdd(&ctr[4], edg);
+        }
+        int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(full, incl, o);
             if (lane >= o) incl += t;
         }
-        const int total = __shfl_sync(full, incl, 31);
-        unsigned long long pos = 0;
-        if (lane == 31 && total) pos = atomicAdd(&ctr[0], (unsigned long long)total);
-        pos = __shfl_sync(full, pos, 31);
-        for (int t = 0; t < items; ++t)
-            queue[pos + incl - items + t] = make_int2(int32_t(v), b + t * kShardChunk);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; ++w) {
+                const int x = s_warp[w];
+                s_warp[w] = tot;
+                tot += x;
+            }
+            s_base = tot ? atomicAdd(&ctr[0], (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        unsigned long long pos = s_base + s_warp[warp] + incl - mine;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int32_t v = int32_t(c0 + int64_t(k) * 256 + threadIdx.x);
+            for (int t = 0; t < items[k]; ++t) queue[pos++] = make_int2(v, first[k] + t * kShardChunk);
+        }
+        __syncthreads();
     }
 }
 
-__global__ void k_sssp_shard_relax(const int2* __restrict__ queue,
-                                   const unsigned long long* __restrict__ ctr,
-                                   const int32_t* __restrict__ offsets,
-                                   const int32_t* __restrict__ dests,
-                                   const int32_t* __restrict__ weights, long long* dist) {
-    const int lane = threadIdx.x & 31;
+// Relaxation: one warp per item (<= kShardChunk out-edges of one vertex), lanes
+// over the edges; 32-bit distances flag an overflow (ctr[2]) instead of
+// wrapping -- the caller then reruns with 64-bit distances.
+template <class D, int LPI>
+__global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict__ queue,
+                                                        const unsigned long long* __restrict__ ctr,
+                                                        const int32_t* __restrict__ offsets,
+                                                        const int32_t* __restrict__ dests,
+                                                        const int32_t* __restrict__ weights,
+                                                        D* dist, unsigned long long* ovf) {
+    // LPI lanes per item: lane groups of LPI take one item each
+    const int sub = threadIdx.x & (LPI - 1);
     const unsigned long long nq = ctr[0];
-    for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
-         i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+    for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
+         i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
         const int2 it = queue[i];
-        const long long dv = dist[it.x];
+        const D dv = dist[it.x];
         const int32_t e1 = min(it.y + kShardChunk, offsets[it.x + 1]);
-        for (int32_t e = it.y + lane; e < e1; e += 32) {
+        for (int32_t e = it.y + sub; e < e1; e += LPI) {
             const int32_t u = dests[e];
-            const long long c = dv + (weights ? weights[e] : 1);
+            const D w = weights ? D(weights[e]) : D(1);
+            if (sizeof(D) == 4 && dv > D(0xFFFFFFFEu) - w) {
+                *ovf = 1;
+                continue;
+            }
+            const D c = dv + w;
             if (c < dist[u]) atomicMin(&dist[u], c);
         }
     }
+}
+
+template <class D>
+__global__ void k_sssp_scan_init(int32_t n, int32_t src, D inf, D* dist, D* prev) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        dist[i] = i == src ? D(0) : inf;
+        prev[i] = inf;
+    }
+}
+
+// Large graphs: rounds of (frontier scan, relaxation) with one host read of
+// the item count per round (the round count is ~ the weighted BFS depth, so
+// the host round trips are negligible next to the ~ms rounds).  Returns true
+// when 32-bit distances overflowed.
+template <class D>
+static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    auto& w = *g->sssp;
+    cudaStream_t s = g->stream;
+    const int32_t n = g->n;
+    D* dist = reinterpret_cast<D*>(w.dist.get());
+    D* prev = reinterpret_cast<D*>(w.prev.get());
+    const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
+    const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
+    w.shard_queue.ensure(items_cap);
+    w.shard_ctr.ensure(5);
+    unsigned long long* ctr = w.shard_ctr.get();
+    DevBuf<unsigned long long> ovf(1);
+    GDX_CUDA(cudaMemsetAsync(ovf.get(), 0, 8, s));
+    timed_launch(g, "sssp_init", [&] {
+        k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, src, inf, dist,
+                                                                              prev);
+    });
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+    unsigned long long vvis = 0, evis = 0;
+    int rounds = 0, launches = 1;
+    const int fgrid = blocks_for(n, 256 * 8, g->num_sms * 8);
+    const char* lv = std::getenv("GDX_SSSP_LPI");
+    const int lpi = lv ? std::atoi(lv) : 32;  // lanes per relaxation item
+    for (;; ++rounds) {
+        GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
+        timed_launch(g, "sssp_frontier", [&] {
+            k_sssp_scan_frontier<D><<<fgrid, 256, 0, s>>>(0, n, g->offsets.get(), dist, prev,
+                                                          w.shard_queue.get(), ctr);
+        });
+        GDX_CUDA(cudaMemcpyAsync(h, ctr, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        ++launches;
+        vvis += h[3];
+        evis += h[4];
+        if (h[0] == 0) break;
+        timed_launch(g, "sssp_relax", [&] {
+            auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
+                    : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
+            fn<<<g->num_sms * 16, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
+                                               g->dests.get(),
+                                               g->weighted ? g->weights.get() : nullptr, dist,
+                                               ovf.get());
+        });
+        ++launches;
+    }
+    cudaPointerAttributes pa;
+    bool dev_out = cudaPointerGetAttributes(&pa, dist_out) == cudaSuccess &&
+                   pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    if (!dev_out) w.queue[1].ensure(size_t(n));
+    int64_t* target = dev_out ? dist_out : reinterpret_cast<int64_t*>(w.queue[1].get());
+    timed_launch(g, "sssp_widen", [&] {
+        k_sssp_widen<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, dist, inf, target);
+    });
+    if (!dev_out) copy_out(g, dist_out, target, size_t(n) * sizeof(int64_t));
+    GDX_CUDA(cudaMemcpyAsync(h, ovf.get(), 8, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    const bool overflow = h[0] != 0;
+    if (stats) {
+        stats->rounds = rounds;
+        stats->launches = launches + 1;
+        stats->vertices_visited = int64_t(vvis);
+        stats->edges_visited = int64_t(evis);
+        stats->updates = 0;
+        // per round: frontier scan dist + prev (2 sizeof(D) n); per frontier
+        // vertex: offsets pair 8 + prev write + item 8 + dist[v]; per edge:
+        // dest 4 + weight 4 + dist[nbr]
+        const double sd = sizeof(D), sw = g->weighted ? 4.0 : 0.0;
+        stats->algorithmic_bytes = (rounds + 1) * 2.0 * sd * n + (16.0 + 2 * sd) * vvis +
+                                   (4.0 + sw + sd) * evis;
+    }
+    return overflow;
 }
 
 }  // namespace gdx
@@ -432,7 +572,7 @@ extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end
         w.shard_v0 = v_begin;
         w.shard_v1 = v_end;
         w.shard_queue.ensure(size_t(v_end - v_begin) + size_t(eb[1] - eb[0]) / kShardChunk + 1);
-        w.shard_ctr.ensure(2);
+        w.shard_ctr.ensure(5);
         w.shard_ready = true;
     });
 }
@@ -445,14 +585,16 @@ extern "C" int gdx_sssp_shard_frontier(gdx_graph* g, int64_t* dist, int64_t* pre
         DeviceGuard dg(g->device);
         auto& w = *g->sssp;
         cudaStream_t s = g->stream;
-        GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get(), 0, 2 * sizeof(unsigned long long), s));
+        GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get(), 0, 5 * sizeof(unsigned long long), s));
         const int32_t cnt = w.shard_v1 - w.shard_v0;
         if (cnt > 0)
             timed_launch(g, "sssp_shard_frontier", [&] {
-                k_sssp_shard_frontier<<<blocks_for(cnt, 256, g->num_sms * 8), 256, 0, s>>>(
-                    w.shard_v0, w.shard_v1, g->offsets.get(),
-                    reinterpret_cast<const long long*>(dist), reinterpret_cast<long long*>(prev),
-                    w.shard_queue.get(), w.shard_ctr.get());
+                k_sssp_scan_frontier<unsigned long long>
+                    <<<blocks_for(cnt, 256 * 8, g->num_sms * 8), 256, 0, s>>>(
+                        w.shard_v0, w.shard_v1, g->offsets.get(),
+                        reinterpret_cast<const unsigned long long*>(dist),
+                        reinterpret_cast<unsigned long long*>(prev), w.shard_queue.get(),
+                        w.shard_ctr.get());
             });
         // count_out (device or host): queued items + improved sinks of this rank
         unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
@@ -472,9 +614,10 @@ extern "C" int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist) {
         auto& w = *g->sssp;
         cudaStream_t s = g->stream;
         timed_launch(g, "sssp_shard_relax", [&] {
-            k_sssp_shard_relax<<<g->num_sms * 16, 256, 0, s>>>(
+            k_sssp_scan_relax<unsigned long long, 32><<<g->num_sms * 16, 256, 0, s>>>(
                 w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
-                g->weighted ? g->weights.get() : nullptr, reinterpret_cast<long long*>(dist));
+                g->weighted ? g->weights.get() : nullptr,
+                reinterpret_cast<unsigned long long*>(dist), w.shard_ctr.get() + 2);
         });
     });
 }
@@ -503,8 +646,18 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
         w.ctrs.ensure(kCtrs);
         // 32-bit distances unless a relaxation overflows them (then 64-bit):
-        // the result is exact either way.
-        const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
-        if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
+        // the result is exact either way.  Large graphs use frontier-scan
+        // rounds (bandwidth-bound), small ones the persistent kernel
+        // (latency-bound); GDX_SSSP_MODE=scan|persistent overrides.
+        const char* mode = std::getenv("GDX_SSSP_MODE");
+        const bool scan = mode ? std::string(mode) == "scan" : g->m >= (int64_t(1) << 25);
+        if (scan) {
+            w.prev.ensure(size_t(g->n));
+            if (run_sssp_scan<unsigned int>(g, src, dist_out, stats))
+                run_sssp_scan<unsigned long long>(g, src, dist_out, stats);
+        } else {
+            const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
+            if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
+        }
     });
 }

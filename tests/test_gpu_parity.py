@@ -155,7 +155,21 @@ def test_sssp_c1_bit_exact(gdx, port):
             assert st["rounds"] >= 2 and st["edges_visited"] >= g.m * 0.5
 
 
-def test_sssp_64bit_distances(gdx, port):
+@pytest.mark.parametrize("mode", ["persistent", "scan"])
+def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
+    """Both SSSP executions (persistent cooperative kernel for small graphs,
+    frontier-scan rounds for large ones) are bit-exact on config 1."""
+    monkeypatch.setenv("GDX_SSSP_MODE", mode)
+    u, v = port.gen_rmat_edges(1 << 18, 1 << 22, 1)
+    g = port.with_random_weights(port.build_from_edges(1 << 18, u, v, None, False), 1, 100, 1)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 262143):
+        assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
+
+
+@pytest.mark.parametrize("mode", ["persistent", "scan"])
+def test_sssp_64bit_distances(gdx, port, mode, monkeypatch):
+    monkeypatch.setenv("GDX_SSSP_MODE", mode)
     u, v = port.gen_rmat_edges(5000, 40000, 8)
     g = port.build_from_edges(5000, u, v, None, True)
     g.weights = np.random.default_rng(1).integers(1 << 28, 1 << 30, size=g.m).astype(np.int32)
