@@ -178,11 +178,12 @@ def roofline(prof: dict, kernel: str, algo_bytes: float, pk: dict, work_launches
     if work_launches:
         launches = work_launches
     achieved = algo_bytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-    tr = [ncu_traffic(k) for k in parts]
-    traffic = sum(tr) if all(t is not None for t in tr) else None
+    tr = {k: ncu_traffic(k) for k in parts}
+    known = [k for k, t in tr.items() if t is not None]
+    traffic = sum(tr[k] for k in known) if known else None
     return {"kernel": kernel, "bound": "hbm", "achieved": round(achieved, 1),
             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "peak_source": pk["source"], "traffic": traffic,
+            "peak_source": pk["source"], "traffic": traffic, "traffic_kernels": known,
             "kernel_ms_avg": round(ms / max(launches, 1), 4), "launches": launches,
             "algorithmic_bytes_per_launch": round(algo_bytes / max(launches, 1), 1)}
 
@@ -411,7 +412,9 @@ def bench_bc(torch, gdx, dist, args, pk) -> dict:
            "n": dg.n, "m": dg.m, "levels": sts[-1]["rounds"], "steps": steps,
            "gteps": dg.m * len(sources) * steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / steps,
-           "roofline": roofline(prof, "bc_forward", sum(s["algorithmic_bytes"] for s in sts) / 2, pk),
+           "roofline": roofline(prof, "bc_cta" if "bc_cta" in prof else "bc_forward",
+                                sum(s["algorithmic_bytes"] for s in sts)
+                                / (1 if "bc_cta" in prof else 2), pk),
            "gpu_launches": int(sum(v[1] for v in prof.values()))}
     dg.close()
     return res

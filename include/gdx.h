@@ -90,6 +90,10 @@ int gdx_device_count(int* count);
 /* ---- graph lifetime ------------------------------------------------------ */
 int gdx_graph_create(const gdx_csr_view* view, int device, gdx_graph** out);
 int gdx_graph_destroy(gdx_graph* g);
+/* Device memory of destroyed graphs and released workspaces is cached by the
+ * library (size-matched reuse, like a caching allocator; capped at 48 GiB) so
+ * create/destroy cycles avoid cudaMalloc/cudaFree.  Returns it to the driver. */
+int gdx_pool_trim(int64_t* released_bytes);
 int gdx_graph_info(const gdx_graph* g, int32_t* n, int32_t* m, int32_t* directed);
 /* Copies the device CSR back; any pointer may be NULL to skip that array. */
 int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* weights,

@@ -64,6 +64,7 @@ SIGNATURES = {
     "gdx_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "gdx_graph_create": ([C.POINTER(GdxCsrView), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "gdx_graph_destroy": ([C.c_void_p], C.c_int),
+    "gdx_pool_trim": ([i64p], C.c_int),
     "gdx_graph_info": ([C.c_void_p, i32p, i32p, i32p], C.c_int),
     "gdx_graph_download": ([C.c_void_p] + [C.c_void_p] * 6, C.c_int),
     "gdx_graph_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),

@@ -3,6 +3,9 @@
 // sssp.cu / pagerank.cu / tc.cu / bc.cu; construction in build.cu.
 #include <cstring>
 
+#include <map>
+#include <mutex>
+
 #include "gdx_internal.cuh"
 #include "plans.cuh"
 
@@ -16,11 +19,114 @@ gdx_graph::~gdx_graph() {
     sssp.reset();
     tc.reset();
     bc.reset();
-    if (pinned) cudaFreeHost(pinned);
+    if (pinned) gdx::pinned_free(pinned);
     if (own_stream) cudaStreamDestroy(own_stream);
 }
 
 namespace gdx {
+
+// ---- device memory pool ------------------------------------------------------
+namespace {
+struct Pool {
+    std::mutex mu;
+    std::multimap<size_t, std::pair<int, void*>> free;  // bytes -> (device, ptr)
+    size_t cached = 0;
+};
+Pool& pool() {
+    static Pool* p = new Pool;  // leaked on purpose: outlives static destructors
+    return *p;
+}
+constexpr size_t kPoolCap = size_t(48) << 30;  // cached bytes kept per process
+}  // namespace
+
+void* pool_alloc(size_t bytes, size_t* got) {
+    int dev = 0;
+    GDX_CUDA(cudaGetDevice(&dev));
+    auto& P = pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        const size_t hi = bytes + bytes / 4 + (size_t(2) << 20);
+        for (auto it = P.free.lower_bound(bytes); it != P.free.end() && it->first <= hi; ++it)
+            if (it->second.first == dev) {
+                void* p = it->second.second;
+                *got = it->first;
+                P.cached -= it->first;
+                P.free.erase(it);
+                return p;
+            }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        pool_trim();
+        e = cudaMalloc(&p, bytes);
+    }
+    GDX_CUDA(e);
+    *got = bytes;
+    return p;
+}
+
+void pool_free(void* p, size_t bytes) {
+    if (!p) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceSynchronize();  // no kernel may still use the block (cudaFree's guarantee)
+    auto& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.cached + bytes > kPoolCap) {
+        cudaFree(p);
+        return;
+    }
+    P.free.emplace(bytes, std::make_pair(dev, p));
+    P.cached += bytes;
+}
+
+// 4 KB pinned host scratch blocks of graph handles (cudaFreeHost would
+// synchronise the device on every graph destroy).
+namespace {
+std::mutex g_pinned_mu;
+std::vector<void*>& pinned_free_list() {
+    static auto* v = new std::vector<void*>;
+    return *v;
+}
+}  // namespace
+
+void* pinned_alloc() {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        auto& v = pinned_free_list();
+        if (!v.empty()) {
+            void* p = v.back();
+            v.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    GDX_CUDA(cudaMallocHost(&p, 4096));
+    return p;
+}
+
+void pinned_free(void* p) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    pinned_free_list().push_back(p);
+}
+
+size_t pool_trim() {
+    auto& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    size_t n = P.cached;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : P.free) {
+        cudaSetDevice(kv.second.first);
+        cudaFree(kv.second.second);
+    }
+    cudaSetDevice(cur);
+    P.free.clear();
+    P.cached = 0;
+    return n;
+}
 
 int guard_impl(const std::function<void()>& f) {
     try {
@@ -49,7 +155,7 @@ static void new_handle(gdx_graph* g, int device) {
     GDX_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
     GDX_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
     g->stream = g->own_stream;
-    GDX_CUDA(cudaMallocHost(&g->pinned, 4096));
+    g->pinned = static_cast<int64_t*>(pinned_alloc());
 }
 
 gdx_graph* make_graph(int device) {
@@ -155,6 +261,13 @@ int gdx_graph_create(const gdx_csr_view* v, int device, gdx_graph** out) {
         finalize_graph(g.get());
         GDX_CUDA(cudaStreamSynchronize(s));
         *out = g.release();
+    });
+}
+
+int gdx_pool_trim(int64_t* released_bytes) {
+    return guard_impl([&] {
+        const size_t n = pool_trim();
+        if (released_bytes) *released_bytes = int64_t(n);
     });
 }
 

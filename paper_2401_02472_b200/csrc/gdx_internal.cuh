@@ -48,21 +48,33 @@ struct DeviceGuard {
     }
 };
 
+// Device memory pool (api.cu): freed blocks are kept per device and handed
+// back to allocations of similar size, so repeated graph create/destroy
+// cycles (the C-ABI e2e path) do not pay cudaMalloc/cudaFree.  pool_free
+// synchronises the device first (the guarantee cudaFree gives), and an
+// allocation that fails releases the cache and retries.
+void* pool_alloc(size_t bytes, size_t* got);
+void pool_free(void* p, size_t bytes);
+size_t pool_trim();
+void* pinned_alloc();
+void pinned_free(void* p);
+
 // Owning device buffer.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    size_t cap = 0;  // bytes of the underlying block
     DevBuf() = default;
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) { o.p = nullptr, o.n = 0, o.cap = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
         if (this != &o) {
             release();
-            p = o.p, n = o.n;
-            o.p = nullptr, o.n = 0;
+            p = o.p, n = o.n, cap = o.cap;
+            o.p = nullptr, o.n = 0, o.cap = 0;
         }
         return *this;
     }
@@ -70,8 +82,8 @@ struct DevBuf {
     void alloc(size_t count) {
         release();
         if (count == 0) count = 1;
-        // +64 B tail: TMA bulk copies round segment ends up to 16 B.
-        GDX_CUDA(cudaMalloc(&p, count * sizeof(T) + 64));
+        // +64 B tail: vector loads round segment ends up to 16 B.
+        p = static_cast<T*>(pool_alloc(count * sizeof(T) + 64, &cap));
         n = count;
     }
     // Grow-only allocation (workspaces cached on the graph handle).
@@ -79,9 +91,10 @@ struct DevBuf {
         if (count > n || p == nullptr) alloc(count);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, cap);
         p = nullptr;
         n = 0;
+        cap = 0;
     }
     T* get() const { return p; }
     size_t bytes() const { return n * sizeof(T); }

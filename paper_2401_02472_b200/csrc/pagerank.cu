@@ -244,13 +244,18 @@ constexpr int kEdgeGroup = 8;
 
 // One lane's 8-edge group g (all 32 lanes of the warp call this together
 // for 32 consecutive groups).
+// R = true: a row range [v_begin, v_end) (sharded); false: the whole graph
+// (compile-time zero bases -- keeps the single-GPU kernel at 32 registers).
+template <bool R>
 __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __restrict__ contrib,
                                               int64_t g) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int64_t e0 = a.e_base + g * kEdgeGroup;
+    const int64_t e_base = R ? a.e_base : 0, e_begin = R ? a.e_begin : 0;
+    const int64_t e_end = R ? a.e_end : int64_t(a.m);
+    const int64_t e0 = e_base + g * kEdgeGroup;
     // valid slots k in [klo, khi): edges inside [e_begin, e_end)
-    const int64_t dlo = a.e_begin - e0, dhi = a.e_end - e0;
+    const int64_t dlo = e_begin - e0, dhi = e_end - e0;
     const int klo = dlo <= 0 ? 0 : dlo >= kEdgeGroup ? kEdgeGroup : int(dlo);
     const int khi = dhi <= 0 ? 0 : dhi >= kEdgeGroup ? kEdgeGroup : int(dhi);
     const bool any = khi > klo;
@@ -308,8 +313,8 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
     const double pval = __shfl_up_sync(full, val, 1);
     if (first_done) {
         const double tot = first_val + (lane > 0 && pkey == first ? pval : 0.0);
-        const int64_t warp_e0 = a.e_base + (g & ~int64_t(31)) * kEdgeGroup;
-        const int64_t start = first > 0 ? a.nz_end[first - 1] : a.e_begin;
+        const int64_t warp_e0 = e_base + (g & ~int64_t(31)) * kEdgeGroup;
+        const int64_t start = first > 0 ? a.nz_end[first - 1] : e_begin;
         const int32_t row = a.nz_row[first];
         if (start < warp_e0)
             atomicAdd(&a.row_sum[row], tot);  // row began in an earlier warp's edges
@@ -320,10 +325,11 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
     if (lane == 31 && val != 0.0 && key < a.nnz) atomicAdd(&a.row_sum[a.nz_row[key]], val);
 }
 
+template <bool R>
 __global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
     if (round_skipped(a, round)) return;
     const double* __restrict__ contrib = (round & 1) ? a.contrib1 : a.contrib0;
-    pr_edge_group(a, contrib, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    pr_edge_group<R>(a, contrib, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
 }
 
 // Pass B: two vertices per thread (16 B vector loads/stores), two pairs in
@@ -346,12 +352,14 @@ __device__ inline void pr_vertex_one(const PrArgs& a, int round, int64_t v, doub
     if (d == 0) dang_local += nr;
 }
 
+template <bool R>
 __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, double dang_term,
                                       const double* __restrict__ rank_in,
                                       double* __restrict__ rank_out,
                                       double* __restrict__ contrib_out, double& dang_local,
                                       int& unsettled) {
-    if (v >= a.v_begin && v + 1 < a.v_end && !a.shard) {
+    const int64_t vb = R ? a.v_begin : 0, ve = R ? a.v_end : a.n;
+    if (!R && v + 1 < ve) {
         const double2 sum = *reinterpret_cast<const double2*>(a.row_sum + v);
         const double2 ri = *reinterpret_cast<const double2*>(rank_in + v);
         const int32_t o0 = a.offsets[v], o1 = a.offsets[v + 1], o2 = a.offsets[v + 2];
@@ -371,12 +379,13 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
         if (d1 == 0) dang_local += nr1;
     } else {
         for (int64_t x = v; x < v + 2; ++x)
-            if (x >= a.v_begin && x < a.v_end)
+            if (x >= vb && x < ve)
                 pr_vertex_one(a, round, x, dang_term, rank_in, rank_out, contrib_out, dang_local,
                               unsettled);
     }
 }
 
+template <bool R>
 __global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
     if (round_skipped(a, round)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.dangling[(round + 2) % 3] = 0.0;
@@ -385,18 +394,19 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
     const double* __restrict__ rank_in = (round & 1) ? a.rank1 : a.rank0;
     double* __restrict__ rank_out = (round & 1) ? a.rank0 : a.rank1;
     double* __restrict__ contrib_out =
-        a.shard ? a.contrib_slice - a.v_begin : ((round & 1) ? a.contrib0 : a.contrib1);
+        R ? a.contrib_slice - a.v_begin : ((round & 1) ? a.contrib0 : a.contrib1);
     double dang_local = 0.0;
     int unsettled = 0;
-    const int64_t v_al = a.v_begin & ~int64_t(1);
+    const int64_t v_al = R ? a.v_begin & ~int64_t(1) : 0;
+    const int64_t ve = R ? a.v_end : a.n;
     const int64_t stride = (int64_t)gridDim.x * kPrBlock * 2;
-    for (int64_t v = v_al + (blockIdx.x * (int64_t)kPrBlock + threadIdx.x) * 2; v < a.v_end;
+    for (int64_t v = v_al + (blockIdx.x * (int64_t)kPrBlock + threadIdx.x) * 2; v < ve;
          v += 2 * stride) {
-        pr_vertex_pair(a, round, v, dang_term, rank_in, rank_out, contrib_out, dang_local,
-                       unsettled);
-        if (v + stride < a.v_end)
-            pr_vertex_pair(a, round, v + stride, dang_term, rank_in, rank_out, contrib_out,
-                           dang_local, unsettled);
+        pr_vertex_pair<R>(a, round, v, dang_term, rank_in, rank_out, contrib_out, dang_local,
+                          unsettled);
+        if (v + stride < ve)
+            pr_vertex_pair<R>(a, round, v + stride, dang_term, rank_in, rank_out, contrib_out,
+                              dang_local, unsettled);
     }
     block_flush(a, round, dang_local, unsettled);
 }
@@ -744,10 +754,10 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
                 if (P.variant == 60) {
                     if (P.ngroups > 0)
                         timed_launch(g, "pr_edges", [&] {
-                            k_pr_edges<<<P.grid, P.block, 0, s>>>(a, int(rr));
+                            k_pr_edges<false><<<P.grid, P.block, 0, s>>>(a, int(rr));
                         });
                     timed_launch(g, "pr_vertices", [&] {
-                        k_pr_vertices<<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0,
+                        k_pr_vertices<false><<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0,
                                         s>>>(a, int(rr));
                     });
                     launches += 1 + (P.ngroups > 0);
@@ -860,10 +870,10 @@ extern "C" int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, d
         GDX_CUDA(cudaMemsetAsync(P.flags.get() + round, 0, 4, s));
         if (P.ngroups > 0)
             timed_launch(g, "pr_edges", [&] {
-                k_pr_edges<<<P.grid, P.block, 0, s>>>(a, round);
+                k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round);
             });
         timed_launch(g, "pr_vertices", [&] {
-            k_pr_vertices<<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
+            k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
                                        g->num_sms * 8),
                             kPrBlock, 0, s>>>(a, round);
         });

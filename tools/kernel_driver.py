@@ -19,7 +19,7 @@ import paper_2401_02472_b200 as gdx  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--algo", default="pr", choices=["pr", "sssp", "tc", "bc"])
+    ap.add_argument("--algo", default="pr", choices=["pr", "sssp", "sssp26", "tc", "bc"])
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--bc-sources", type=int, default=64)
     a = ap.parse_args()
@@ -38,8 +38,9 @@ def main():
         for _ in range(a.reps):
             print(g.pagerank(0.85, 1e-6, 100)[1])
         graphs_pr = graphs  # noqa: F841
-    elif a.algo == "sssp":
-        g = gdx.DeviceGraph.generate("rmat", 1 << 18, 1 << 22, seed=1, directed=False,
+    elif a.algo in ("sssp", "sssp26"):
+        sc = 18 if a.algo == "sssp" else 26
+        g = gdx.DeviceGraph.generate("rmat", 1 << sc, 16 << sc, seed=1, directed=False,
                                      weights=(1, 100))
         for _ in range(a.reps):
             st = {}
