@@ -445,22 +445,31 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
                                                         D* dist, unsigned long long* ovf) {
     // LPI lanes per item: lane groups of LPI take one item each
     const int sub = threadIdx.x & (LPI - 1);
+    constexpr int kU = kShardChunk / LPI;  // edges per lane per item, all loads issued together
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
         const int2 it = queue[i];
         const D dv = dist[it.x];
         const int32_t e1 = min(it.y + kShardChunk, offsets[it.x + 1]);
-        for (int32_t e = it.y + sub; e < e1; e += LPI) {
-            const int32_t u = dests[e];
-            const D w = weights ? D(weights[e]) : D(1);
-            if (sizeof(D) == 4 && dv > D(0xFFFFFFFEu) - w) {
+        int32_t u[kU];
+        D c[kU], du[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const int32_t e = it.y + sub + k * LPI;
+            u[k] = e < e1 ? dests[e] : -1;
+            const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
+            c[k] = dv + w;
+            if (sizeof(D) == 4 && u[k] >= 0 && dv > D(0xFFFFFFFEu) - w) {
                 *ovf = 1;
-                continue;
+                u[k] = -1;
             }
-            const D c = dv + w;
-            if (c < dist[u]) atomicMin(&dist[u], c);
         }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) du[k] = u[k] >= 0 ? dist[u[k]] : D(0);
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+            if (u[k] >= 0 && c[k] < du[k]) atomicMin(&dist[u[k]], c[k]);
     }
 }
 
@@ -500,7 +509,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     int rounds = 0, launches = 1;
     const int fgrid = blocks_for(n, 256 * 8, g->num_sms * 8);
     const char* lv = std::getenv("GDX_SSSP_LPI");
-    const int lpi = lv ? std::atoi(lv) : 32;  // lanes per relaxation item
+    const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
     for (;; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
