@@ -297,7 +297,7 @@ struct BcCtaArgs {
 // atomics), so a source's levels are spread over CS * 1024 threads.
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(BcCtaArgs a) {
-    __shared__ int s_next_local[2];
+    __shared__ int s_next_local[3];
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = int(cluster.block_rank());
     int* s_next = cluster.map_shared_rank(s_next_local, 0);
@@ -318,7 +318,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             lev[src] = 0;
             log[0] = src;
             loff[0] = 0;
-            s_next[0] = s_next[1] = 0;
+            s_next[0] = s_next[1] = s_next[2] = 0;
         }
         cluster.sync();
         // ---- forward: iterateInBFS ----
@@ -351,7 +351,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             acc = xf_add(acc, sg[k]);
                             ++dag;
                         }
-                        if (got[k]) log[end + atomicAdd(&s_next[L & 1], 1)] = w[k];
+                        if (got[k]) log[end + atomicAdd(&s_next[L % 3], 1)] = w[k];
                     }
                 }
                 if (!a.undirected && L > 0) {
@@ -378,13 +378,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 sig[v] = acc;
             }
+            // one barrier per level: level L pushes to tail L % 3; the tail of
+            // level L+2 (last read right after the previous barrier) is reset now
             cluster.sync();
-            const int next = s_next[L & 1];
+            const int next = s_next[L % 3];
             if (tid == 0) {
-                s_next[(L + 1) & 1] = 0;
+                s_next[(L + 2) % 3] = 0;
                 loff[L + 1] = end;
             }
-            cluster.sync();
             if (next == 0) break;
             beg = end;
             end += next;

@@ -623,7 +623,7 @@ extern "C" int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist) {
         auto& w = *g->sssp;
         cudaStream_t s = g->stream;
         timed_launch(g, "sssp_shard_relax", [&] {
-            k_sssp_scan_relax<unsigned long long, 32><<<g->num_sms * 16, 256, 0, s>>>(
+            k_sssp_scan_relax<unsigned long long, 16><<<g->num_sms * 16, 256, 0, s>>>(
                 w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
                 g->weighted ? g->weights.get() : nullptr,
                 reinterpret_cast<unsigned long long*>(dist), w.shard_ctr.get() + 2);
