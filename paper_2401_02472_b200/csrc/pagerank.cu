@@ -329,7 +329,14 @@ template <bool R>
 __global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
     if (round_skipped(a, round)) return;
     const double* __restrict__ contrib = (round & 1) ? a.contrib1 : a.contrib0;
-    pr_edge_group<R>(a, contrib, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    // grid-stride over 256-group block chunks; the grid is capped at 64
+    // blocks per SM (measured on B200: 1.05 ms vs 1.13 ms for one chunk per
+    // block at RMAT-24); chunks stay warp aligned
+    const int64_t ngroups = R ? (a.e_end - a.e_base + kEdgeGroup - 1) / kEdgeGroup
+                              : (int64_t(a.m) + kEdgeGroup - 1) / kEdgeGroup;
+    for (int64_t g0 = int64_t(blockIdx.x) * blockDim.x; g0 < ngroups;
+         g0 += int64_t(gridDim.x) * blockDim.x)
+        pr_edge_group<R>(a, contrib, g0 + threadIdx.x);
 }
 
 // Pass B: two vertices per thread (16 B vector loads/stores), two pairs in
@@ -579,7 +586,9 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     }
     P.dangling.alloc(3);
     P.block = 256;
-    P.grid = blocks_for(std::max<int64_t>(P.ngroups, 1), 256, INT32_MAX);
+    const char* cap = std::getenv("GDX_PR_GRID_CAP");  // blocks per SM of pass A (A/B)
+    P.grid = blocks_for(std::max<int64_t>(P.ngroups, 1), 256,
+                        (cap ? std::max(1, std::atoi(cap)) : 64) * g->num_sms);
     GDX_CUDA(cudaStreamSynchronize(s));
 }
 
