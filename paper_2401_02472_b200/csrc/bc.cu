@@ -390,6 +390,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             beg = end;
             end += next;
         }
+        cluster.sync();  // loff[levels] (written by thread 0 above) before the backward pass
         const int levels = L + 1;  // loff[0..levels] bound the levels in log
         if (tid == 0) {
             reached += end;
