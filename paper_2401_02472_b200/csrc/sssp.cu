@@ -510,6 +510,8 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const int fgrid = blocks_for(n, 256 * 8, g->num_sms * 8);
     const char* lv = std::getenv("GDX_SSSP_LPI");
     const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
+    const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
+    const int relax_grid = (rc ? std::max(1, std::atoi(rc)) : 64) * g->num_sms;
     for (;; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
@@ -525,7 +527,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         timed_launch(g, "sssp_relax", [&] {
             auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
                     : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
-            fn<<<g->num_sms * 16, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
+            fn<<<relax_grid, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
                                                g->dests.get(),
                                                g->weighted ? g->weights.get() : nullptr, dist,
                                                ovf.get());

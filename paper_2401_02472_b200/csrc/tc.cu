@@ -362,7 +362,9 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
     });
     if (v_end > v_begin) {
         const int64_t groups = (int64_t(v_end) - v_begin + 31) / 32;
-        const int grid = blocks_for(groups * 32, kTcBlock, g->num_sms * 16);
+        const char* cap = std::getenv("GDX_TC_GRID_CAP");  // blocks per SM (A/B)
+        const int grid = blocks_for(groups * 32, kTcBlock,
+                                    (cap ? std::max(1, std::atoi(cap)) : 64) * g->num_sms);
         timed_launch(g, "tc", [&] {
             k_tc_oriented<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, P.off_plus.get(),
                                                     P.adj_plus.get(), P.acc.get());
