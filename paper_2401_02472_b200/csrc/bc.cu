@@ -286,7 +286,7 @@ struct BcCtaArgs {
     int32_t* level;    // [grid][n], -1 = undiscovered (restored after each source)
     double2* sig;      // [grid][n]
     double* delta;     // [grid][n]
-    int32_t* log;      // [grid][n]   discovery order, levels contiguous
+    int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
     double* bc;
     unsigned long long* ctr;
@@ -309,14 +309,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     int32_t* lev = a.level + slot * a.n;
     double2* sig = a.sig + slot * a.n;
     double* delta = a.delta + slot * a.n;
-    int32_t* log = a.log + slot * a.n;
+    int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
     unsigned long long reached = 0, fscan = 0, bscan = 0, dag = 0, levels_max = 0;
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
         if (tid == 0) {
             lev[src] = 0;
-            log[0] = src;
+            log[0] = make_int4(src, a.offsets[src], a.offsets[src + 1], 0);
             loff[0] = 0;
             s_next[0] = s_next[1] = s_next[2] = 0;
         }
@@ -325,9 +325,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         int beg = 0, end = 1, L = 0;
         for (;; ++L) {
             for (int i = beg + tid; i < end; i += kStride) {
-                const int32_t v = log[i];
+                // the log entry carries v's out-edge range (one dependent load fewer)
+                const int4 it = log[i];
+                const int32_t v = it.x, ob = it.y, oe = it.z;
                 double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
-                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
                 fscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
@@ -342,16 +343,22 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         par[k] = a.undirected && L > 0 && lw[k] == L - 1;
                         sg[k] = par[k] ? sig[w[k]] : make_double2(0.0, 0.0);
                     }
+                    int32_t w0[kNb], w1[kNb];
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k)
-                        got[k] = lw[k] == -1 && atomicCAS(&lev[w[k]], -1, L + 1) == -1;
+                    for (int k = 0; k < kNb; ++k) {
+                        const bool cand = lw[k] == -1;
+                        w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
+                        w1[k] = cand ? a.offsets[w[k] + 1] : 0;
+                        got[k] = cand && atomicCAS(&lev[w[k]], -1, L + 1) == -1;
+                    }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
                         if (par[k]) {  // ascending parent order
                             acc = xf_add(acc, sg[k]);
                             ++dag;
                         }
-                        if (got[k]) log[end + atomicAdd(&s_next[L % 3], 1)] = w[k];
+                        if (got[k])
+                            log[end + atomicAdd(&s_next[L % 3], 1)] = make_int4(w[k], w0[k], w1[k], 0);
                     }
                 }
                 if (!a.undirected && L > 0) {
@@ -400,8 +407,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         for (int Lb = levels - 1; Lb >= 0; --Lb) {
             const int b0 = loff[Lb], b1 = loff[Lb + 1];
             for (int i = b0 + tid; i < b1; i += kStride) {
-                const int32_t v = log[i];
-                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+                const int4 it = log[i];
+                const int32_t v = it.x, ob = it.y, oe = it.z;
                 const double2 sv = sig[v];
                 double d = 0.0;
                 bscan += oe - ob;
@@ -432,7 +439,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             cluster.sync();
         }
         // restore `level` for the slot's next source
-        for (int i = tid; i < end; i += kStride) lev[log[i]] = -1;
+        for (int i = tid; i < end; i += kStride) lev[log[i].x] = -1;
         cluster.sync();
     }
     for (int o = 16; o; o >>= 1) {
@@ -478,7 +485,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.level.alloc(size_t(slots) * n);
         W.sig.alloc(size_t(slots) * n * 2);
         W.delta.alloc(size_t(slots) * n);
-        W.cta_log.alloc(size_t(slots) * n);
+        W.cta_log.alloc(size_t(slots) * n * 4);  // int4 entries
         W.cta_loff.alloc(size_t(slots) * (n + 2));
         W.cta_grid = slots;
         GDX_CUDA(cudaMemsetAsync(W.level.get(), 0xff, W.level.bytes(), s));
