@@ -274,6 +274,17 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kBcCta = 1024;
 
+// Per-(slot, vertex) state of the CTA kernel, packed so one 16 B load returns
+// a neighbour's level and sigma together and one 32 B load adds its delta:
+// {level, sigma exponent, sigma mantissa, delta}.
+struct __align__(32) BcRec {
+    int32_t level;  // -1 = undiscovered (restored after each source)
+    int32_t sexp;
+    double smant;
+    double delta;
+    double pad;
+};
+
 struct BcCtaArgs {
     int32_t n;
     int32_t nsrc;
@@ -283,14 +294,33 @@ struct BcCtaArgs {
     const int32_t* __restrict__ in_offsets;
     const int32_t* __restrict__ in_srcs;
     const int32_t* __restrict__ sources;
-    int32_t* level;    // [grid][n], -1 = undiscovered (restored after each source)
-    double2* sig;      // [grid][n]
-    double* delta;     // [grid][n]
+    BcRec* rec;        // [grid][n]
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
     double* bc;
     unsigned long long* ctr;
 };
+
+__device__ inline void rec_level_sigma(const BcRec* r, int32_t& level, double2& sig) {
+    const int4 q = *reinterpret_cast<const int4*>(r);
+    level = q.x;
+    sig = make_double2(__hiloint2double(q.w, q.z), double(q.y));
+}
+__device__ inline void rec_all(const BcRec* r, int32_t& level, double2& sig, double& delta) {
+    int32_t x[8];
+    asm("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
+          "=r"(x[7])
+        : "l"(r));
+    level = x[0];
+    sig = make_double2(__hiloint2double(x[3], x[2]), double(x[1]));
+    delta = __hiloint2double(x[5], x[4]);
+}
+__device__ inline void rec_store_sigma(BcRec* r, int32_t level, double2 sig) {
+    const double m = sig.x;
+    *reinterpret_cast<int4*>(r) =
+        make_int4(level, int32_t(sig.y), __double2loint(m), __double2hiint(m));
+}
 
 // CS CTAs (a thread-block cluster) share one source: the level barrier is a
 // cluster barrier and the queue tail lives in CTA 0's shared memory (DSMEM
@@ -306,16 +336,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     constexpr int kStride = CS * kBcCta;
     const int64_t slot = blockIdx.x / CS;
     const int32_t nslots = gridDim.x / CS;
-    int32_t* lev = a.level + slot * a.n;
-    double2* sig = a.sig + slot * a.n;
-    double* delta = a.delta + slot * a.n;
+    BcRec* rec = a.rec + slot * a.n;
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
     unsigned long long reached = 0, fscan = 0, bscan = 0, dag = 0, levels_max = 0;
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
         if (tid == 0) {
-            lev[src] = 0;
+            rec[src].level = 0;
             log[0] = make_int4(src, a.offsets[src], a.offsets[src + 1], 0);
             loff[0] = 0;
             s_next[0] = s_next[1] = s_next[2] = 0;
@@ -332,24 +360,24 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 fscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
+                    double2 sg[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) lw[k] = w[k] >= 0 ? lev[w[k]] : -2;
-                    double2 sg[kNb];
-                    bool par[kNb], got[kNb];
-#pragma unroll
-                    for (int k = 0; k < kNb; ++k) {
-                        par[k] = a.undirected && L > 0 && lw[k] == L - 1;
-                        sg[k] = par[k] ? sig[w[k]] : make_double2(0.0, 0.0);
+                    for (int k = 0; k < kNb; ++k) {  // level and sigma in one 16 B load
+                        lw[k] = -2;
+                        sg[k] = make_double2(0.0, 0.0);
+                        if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
+                    bool par[kNb], got[kNb];
                     int32_t w0[kNb], w1[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
+                        par[k] = a.undirected && L > 0 && lw[k] == L - 1;
                         const bool cand = lw[k] == -1;
                         w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
                         w1[k] = cand ? a.offsets[w[k] + 1] : 0;
-                        got[k] = cand && atomicCAS(&lev[w[k]], -1, L + 1) == -1;
+                        got[k] = cand && atomicCAS(&rec[w[k]].level, -1, L + 1) == -1;
                     }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
@@ -365,25 +393,25 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
                     fscan += ie - ib;
                     for (int32_t e = ib; e < ie; e += kNb) {
-                        int32_t p[kNb];
-                        bool par[kNb];
+                        int32_t p[kNb], lp[kNb];
                         double2 sg[kNb];
 #pragma unroll
                         for (int k = 0; k < kNb; ++k) p[k] = e + k < ie ? a.in_srcs[e + k] : -1;
 #pragma unroll
-                        for (int k = 0; k < kNb; ++k) par[k] = p[k] >= 0 && lev[p[k]] == L - 1;
+                        for (int k = 0; k < kNb; ++k) {
+                            lp[k] = -2;
+                            sg[k] = make_double2(0.0, 0.0);
+                            if (p[k] >= 0) rec_level_sigma(rec + p[k], lp[k], sg[k]);
+                        }
 #pragma unroll
                         for (int k = 0; k < kNb; ++k)
-                            sg[k] = par[k] ? sig[p[k]] : make_double2(0.0, 0.0);
-#pragma unroll
-                        for (int k = 0; k < kNb; ++k)
-                            if (par[k]) {
+                            if (lp[k] == L - 1) {
                                 acc = xf_add(acc, sg[k]);
                                 ++dag;
                             }
                     }
                 }
-                sig[v] = acc;
+                rec_store_sigma(rec + v, L, acc);
             }
             // one barrier per level: level L pushes to tail L % 3; the tail of
             // level L+2 (last read right after the previous barrier) is reset now
@@ -409,37 +437,38 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             for (int i = b0 + tid; i < b1; i += kStride) {
                 const int4 it = log[i];
                 const int32_t v = it.x, ob = it.y, oe = it.z;
-                const double2 sv = sig[v];
+                int32_t lv;
+                double2 sv;
+                rec_level_sigma(rec + v, lv, sv);
                 double d = 0.0;
                 bscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
-                    int32_t w[kNb];
-                    bool ch[kNb];
+                    int32_t w[kNb], lw[kNb];
                     double2 sw[kNb];
                     double dw[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) ch[k] = w[k] >= 0 && lev[w[k]] == Lb + 1;
-#pragma unroll
-                    for (int k = 0; k < kNb; ++k) {
-                        sw[k] = ch[k] ? sig[w[k]] : make_double2(1.0, 0.0);
-                        dw[k] = ch[k] ? delta[w[k]] : 0.0;
+                    for (int k = 0; k < kNb; ++k) {  // level, sigma and delta in one 32 B load
+                        lw[k] = -2;
+                        sw[k] = make_double2(1.0, 0.0);
+                        dw[k] = 0.0;
+                        if (w[k] >= 0) rec_all(rec + w[k], lw[k], sw[k], dw[k]);
                     }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k)
-                        if (ch[k] && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
+                        if (lw[k] == Lb + 1 && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
                             d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
                             ++dag;
                         }
                 }
-                delta[v] = d;
+                rec[v].delta = d;
                 if (v != src) atomicAdd(&a.bc[v], d);
             }
             cluster.sync();
         }
         // restore `level` for the slot's next source
-        for (int i = tid; i < end; i += kStride) lev[log[i].x] = -1;
+        for (int i = tid; i < end; i += kStride) rec[log[i].x].level = -1;
         cluster.sync();
     }
     for (int o = 16; o; o >>= 1) {
@@ -482,13 +511,11 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.cta_log.release();
         W.cta_loff.release();
         W.batch = 0;
-        W.level.alloc(size_t(slots) * n);
-        W.sig.alloc(size_t(slots) * n * 2);
-        W.delta.alloc(size_t(slots) * n);
+        W.cta_rec.alloc(size_t(slots) * n * 4);  // 32 B BcRec per (slot, vertex)
         W.cta_log.alloc(size_t(slots) * n * 4);  // int4 entries
         W.cta_loff.alloc(size_t(slots) * (n + 2));
         W.cta_grid = slots;
-        GDX_CUDA(cudaMemsetAsync(W.level.get(), 0xff, W.level.bytes(), s));
+        GDX_CUDA(cudaMemsetAsync(W.cta_rec.get(), 0xff, W.cta_rec.bytes(), s));  // level = -1
     }
     W.sources.ensure(size_t(nsrc));
     GDX_CUDA(cudaMemcpyAsync(W.sources.get(), hsrc.data(), size_t(nsrc) * 4,
@@ -503,9 +530,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.in_offsets = g->rev_offsets.get();
     a.in_srcs = g->rev_srcs.get();
     a.sources = W.sources.get();
-    a.level = W.level.get();
-    a.sig = reinterpret_cast<double2*>(W.sig.get());
-    a.delta = W.delta.get();
+    a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
@@ -567,10 +592,8 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         if (nsrc > 0 && cta_mode) {
             run_bc_cta(g, hsrc, totals, launches, max_levels);
         } else if (nsrc > 0) {
-            if (W.cta_grid > 0) {  // switch back from CTA mode: its buffers are sized differently
-                W.level.release();
-                W.sig.release();
-                W.delta.release();
+            if (W.cta_grid > 0) {  // switch back from CTA mode: release its buffers
+                W.cta_rec.release();
                 W.cta_log.release();
                 W.cta_loff.release();
                 W.cta_grid = 0;
