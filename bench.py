@@ -429,10 +429,11 @@ def _shard_roofline(prof, kernels, algo_bytes, pk, launches):
 
 
 def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
-    """C2 PageRank partitioned over the ranks by destination-vertex ranges
-    (distributed.sharded_pr): per round one NCCL all-gather of the contrib
-    slices and one all-reduce of (dangling, unsettled).  Strong scaling: the
-    graph is fixed, every rank computes its rows."""
+    """C2 PageRank partitioned over the ranks by destination-vertex ranges.
+    The exchange is fused into the kernels over peer memory
+    (distributed.sharded_pr_p2p); if that fails, per round one NCCL all-gather
+    of the contrib slices and one all-reduce (distributed.sharded_pr).
+    Strong scaling: the graph is fixed, every rank computes its rows."""
     from paper_2401_02472_b200 import distributed as D
     dg = gdx.DeviceGraph.generate("rmat", 1 << 24, 1 << 28, seed=1, directed=True,
                                   device=dist.local)
@@ -440,10 +441,21 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
     ex = D.DeviceExecutor(dg)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
 
+    # exchange: fused into the kernels over peer memory (NVLink P2P through CUDA
+    # IPC, gdx_pr_p2p_*); NCCL all-gather + all-reduce if peer memory fails
+    exchange = {"kind": "p2p"}
+
     def step():
-        _, rounds = D.sharded_pr(ex, 0.85, 1e-6, 100, to_host=False)
+        if exchange["kind"] == "p2p":
+            _, rounds = D.sharded_pr_p2p(ex, 0.85, 1e-6, 100, to_host=False)
+        else:
+            _, rounds = D.sharded_pr(ex, 0.85, 1e-6, 100, to_host=False)
         return rounds
 
+    try:
+        step()
+    except Exception as e:  # noqa: BLE001 -- recorded in the JSON line
+        exchange.update(kind="nccl", p2p_error=str(e)[:200])
     dg.profile(True)
     for _ in range(args.warmup):
         step()
@@ -467,6 +479,7 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
         "partition": {"ranges": ranges, "rank0_edges": e_r},
+        "exchange": exchange,
     }
     # e2e: every rank uploads the host CSR through the C ABI, runs the sharded
     # fixedPoint and gathers the full rank vector to the host
@@ -527,7 +540,7 @@ def bench_sharded_other(torch, gdx, dist, args, pk, algo: str) -> dict:
                                     replace=False).tolist())
 
         def step():
-            return D.sharded_bc(ex, sources)
+            return D.sharded_bc(ex, sources, to_host=False)
         units, name, kern = float(dg.m) * len(sources), \
             f"C4 BC {len(sources)} sources, {side}^2 grid keep 0.55 undirected", "bc_forward"
     else:  # sssp26
@@ -602,8 +615,9 @@ def run_ours(args) -> None:
         "data": "synthetic: counter-based RMAT generator (a,b,c,d=.57,.19,.19,.05), seed 1, built on GPU",
         "config": {"workload": head["workload"], "graph": "rmat-24", "n": head["n"], "m": head["m"],
                    "pr_rounds": head["rounds"], "damping": 0.85, "threshold": 1e-6, "max_iter": 100,
-                   "parallelism": (f"vertex-range shards x{dist.world} (NCCL all-gather of contrib "
-                                   "slices + all-reduce per round)") if sharded else "single",
+                   "parallelism": (f"vertex-range shards x{dist.world} (exchange: "
+                                   f"{head.get('exchange', {}).get('kind', 'nccl')})")
+                   if sharded else "single",
                    "l2": "flushed (512 MB write) before every timed step"},
         "roofline": head["roofline"], "e2e": head["e2e"], "clocks": head["clocks"],
         "gpu_launches": head["gpu_launches"], "kernels": head["kernels"],

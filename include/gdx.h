@@ -185,6 +185,23 @@ int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, double thres
                        double* contrib_slice /* device */, double* partials /* device [2] */);
 int gdx_pr_shard_rank(gdx_graph* g, int32_t rounds, double* rank_slice);
 
+/* PageRank with the exchange fused into the kernels over peer memory (NVLink
+ * P2P through CUDA IPC; one process per GPU).  After gdx_pr_shard_setup:
+ * gdx_pr_p2p_setup exports this rank's exchange block (handle_out: 64 bytes,
+ * a cudaIpcMemHandle_t); the caller all-gathers the handles (rank order) and
+ * passes them to gdx_pr_p2p_open.  gdx_pr_p2p_init / _round then write every
+ * new contrib value of the rank's rows straight into every rank's block from
+ * the vertex kernel, publish (dangling mass, unsettled vote) with system-scope
+ * atomics, and return the partials summed over all ranks in rank order
+ * (partials_out: host [2]) -- no separate all-gather or all-reduce.  The final
+ * ranks come from gdx_pr_shard_rank.  Same arithmetic as gdx_pagerank. */
+int gdx_pr_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, void* handle_out);
+int gdx_pr_p2p_open(gdx_graph* g, const void* handles /* world * 64 bytes */);
+int gdx_pr_p2p_init(gdx_graph* g, double* partials_out);
+int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, double threshold,
+                     int32_t max_iter, double dangling_in, double* partials_out);
+int gdx_pr_p2p_close(gdx_graph* g);
+
 /* SSSP, vertex ranges: every rank keeps a full int64 replica of dist (device
  * [n], INF = INT64_MAX/2) and prev (device [n], the value each own vertex had
  * when last expanded).  frontier: queue the rank's vertices with dist < prev

@@ -145,6 +145,7 @@ struct Profiler {
 };
 
 struct PrPlan;
+struct PrP2P;
 struct SsspWork;
 struct TcPlan;
 struct BcWork;
@@ -167,6 +168,7 @@ struct gdx_graph {
     gdx::Profiler prof;
     std::unique_ptr<gdx::PrPlan> pr;
     std::unique_ptr<gdx::PrPlan> pr_shard;  // gdx_pr_shard_* (one rank's vertex range)
+    std::unique_ptr<gdx::PrP2P> pr_p2p;     // gdx_pr_p2p_* (peer-memory exchange)
     std::unique_ptr<gdx::SsspWork> sssp;
     std::unique_ptr<gdx::TcPlan> tc;
     std::unique_ptr<gdx::BcWork> bc;

@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "gdx_internal.cuh"
 #include "plans.cuh"
@@ -67,6 +68,10 @@ struct PrArgs {
     int64_t e_begin, e_end, e_base;       // e_base = e_begin rounded down to 8
     int32_t shard;                        // 1: rounds never skip (the host decides)
     double* contrib_slice;                // shard: contrib_out written at [v - v_begin]
+    // peer-memory exchange (gdx_pr_p2p_*): every rank's contrib buffer of the
+    // next publish, written directly over NVLink instead of an all-gather
+    double* const* peers;
+    int32_t npeers;
 };
 
 
@@ -355,7 +360,12 @@ __device__ inline void pr_vertex_one(const PrArgs& a, int round, int64_t v, doub
     if (c >= a.threshold && round < a.max_iter) unsettled = 1;
     rank_out[v] = nr;
     const int32_t d = a.offsets[v + 1] - a.offsets[v];
-    contrib_out[v] = d > 0 ? nr / double(d) : 0.0;
+    const double cv = d > 0 ? nr / double(d) : 0.0;
+    if (a.npeers > 0) {
+        for (int q = 0; q < a.npeers; ++q) a.peers[q][v] = cv;  // P2P stores over NVLink
+    } else {
+        contrib_out[v] = cv;
+    }
     if (d == 0) dang_local += nr;
 }
 
@@ -393,7 +403,7 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
 }
 
 template <bool R>
-__global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
+__device__ __forceinline__ void pr_vertices_body(const PrArgs& a, int round) {
     if (round_skipped(a, round)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.dangling[(round + 2) % 3] = 0.0;
     const double dang_in = *reinterpret_cast<const volatile double*>(&a.dangling[round % 3]);
@@ -416,6 +426,12 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
                               dang_local, unsettled);
     }
     block_flush(a, round, dang_local, unsettled);
+}
+
+template <bool R>
+__global__ void __launch_bounds__(kPrBlock) k_pr_vertices(PrArgs a, int round) {
+    pr_vertices_body<R>(a, round);
+    if (R && a.npeers > 0) __threadfence_system();  // P2P stores performed before the publish
 }
 
 // Non-empty rows of the reverse CSR and the row of every 8-edge group.
@@ -690,6 +706,8 @@ static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshol
     a.e_base = P.e_base;
     a.shard = P.shard ? 1 : 0;
     a.contrib_slice = nullptr;
+    a.peers = nullptr;
+    a.npeers = 0;
     return a;
 }
 
@@ -702,13 +720,18 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_shard_init(PrArgs a, double* pa
          v += (int64_t)gridDim.x * kPrBlock) {
         a.rank0[v] = r0;
         const int32_t od = a.offsets[v + 1] - a.offsets[v];
-        a.contrib_slice[v - a.v_begin] = od > 0 ? r0 / double(od) : 0.0;
+        const double cv = od > 0 ? r0 / double(od) : 0.0;
+        if (a.npeers > 0)
+            for (int q = 0; q < a.npeers; ++q) a.peers[q][v] = cv;
+        else
+            a.contrib_slice[v - a.v_begin] = cv;
         if (od == 0) dang_local += r0;
     }
     typedef cub::BlockReduce<double, kPrBlock> R;
     __shared__ typename R::TempStorage tmp;
     double tot = R(tmp).Sum(dang_local);
     if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&partials[0], tot);
+    if (a.npeers > 0) __threadfence_system();
 }
 
 __global__ void k_pr_shard_partials(const double* dangling, const int32_t* flags, int round,
@@ -900,5 +923,213 @@ extern "C" int gdx_pr_shard_rank(gdx_graph* g, int32_t rounds, double* rank_slic
         copy_out(g, rank_slice, P.rank[rounds & 1].get() + P.v_begin,
                  size_t(P.v_end - P.v_begin) * sizeof(double));
         GDX_CUDA(cudaStreamSynchronize(g->stream));
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Sharded PageRank with the exchange fused into the kernels over peer memory
+// (one process per GPU, NVLink P2P through CUDA IPC).  Every rank exports one
+// device block {contrib[2][n] | partials[2][world][2] | counter}; pass B stores
+// each new contrib value straight into every rank's block (no all-gather), a
+// one-thread publish kernel writes the rank's (dangling, unsettled) partials
+// into every rank's slot and bumps every rank's counter with a system-scope
+// atomic, and the next round's first kernel waits on the local counter.
+// Publish j uses contrib/partial parity j & 1: a rank can be at most one
+// publish ahead of any other (each wait needs all ranks' previous publish),
+// so a parity is never rewritten while a slower rank still reads it.
+// ---------------------------------------------------------------------------
+namespace gdx {
+
+// Spins until the local counter reaches `target`; gives up after ~20 s (a
+// rank died or the peer writes never land) and flags *err instead of hanging.
+__global__ void k_p2p_wait(const unsigned long long* ctr, unsigned long long target, int* err) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*reinterpret_cast<const volatile unsigned long long*>(ctr) < target) {
+        __nanosleep(256);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {
+            *err = 1;
+            break;
+        }
+    }
+    __threadfence_system();
+}
+
+__global__ void k_p2p_publish(const double* dang, const int32_t* unsettled, double* const* slots,
+                              unsigned long long* const* ctrs, int world) {
+    const double d = dang ? *dang : 0.0;
+    const double u = unsettled && *unsettled ? 1.0 : 0.0;
+    for (int q = 0; q < world; ++q) {
+        slots[q][0] = d;
+        slots[q][1] = u;
+    }
+    __threadfence_system();
+    for (int q = 0; q < world; ++q) atomicAdd_system(ctrs[q], 1ull);
+}
+
+}  // namespace gdx
+
+using namespace gdx;
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+
+extern "C" int gdx_pr_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, void* handle_out) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard || !handle_out || world < 1 || rank < 0 || rank >= world)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad p2p setup (call gdx_pr_shard_setup first)");
+        DeviceGuard dg(g->device);
+        auto X = std::make_unique<PrP2P>();
+        X->world = world;
+        X->rank = rank;
+        X->n = g->n;
+        GDX_CUDA(cudaMalloc(&X->block, X->bytes()));  // IPC export needs a plain cudaMalloc block
+        GDX_CUDA(cudaMemset(X->block, 0, X->bytes()));
+        cudaIpcMemHandle_t h;
+        GDX_CUDA(cudaIpcGetMemHandle(&h, X->block));
+        std::memcpy(handle_out, &h, sizeof(h));
+        g->pr_p2p = std::move(X);
+    });
+}
+
+extern "C" int gdx_pr_p2p_open(gdx_graph* g, const void* handles) {
+    return guard_impl([&] {
+        if (!g || !g->pr_p2p || !handles) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p setup");
+        DeviceGuard dg(g->device);
+        auto& X = *g->pr_p2p;
+        X.bases.assign(X.world, nullptr);
+        for (int q = 0; q < X.world; ++q) {
+            if (q == X.rank) {
+                X.bases[q] = X.block;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const char*>(handles) + 64 * q, sizeof(h));
+            void* p = nullptr;
+            GDX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            X.bases[q] = static_cast<double*>(p);
+        }
+        std::vector<double*> pc(2 * X.world), ps(2 * X.world);
+        std::vector<unsigned long long*> pk(X.world);
+        for (int q = 0; q < X.world; ++q) {
+            double* b = X.bases[q];
+            for (int par = 0; par < 2; ++par) {
+                pc[par * X.world + q] = b + par * X.n;
+                ps[par * X.world + q] = b + 2 * X.n + (par * X.world + X.rank) * 2;
+            }
+            pk[q] = reinterpret_cast<unsigned long long*>(b + 2 * X.n + 4 * X.world);
+        }
+        X.peer_contrib.alloc(pc.size());
+        X.peer_slot.alloc(ps.size());
+        X.peer_ctr.alloc(pk.size());
+        GDX_CUDA(cudaMemcpy(X.peer_contrib.get(), pc.data(), pc.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        GDX_CUDA(cudaMemcpy(X.peer_slot.get(), ps.data(), ps.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        GDX_CUDA(cudaMemcpy(X.peer_ctr.get(), pk.data(), pk.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        X.err.alloc(1);
+        GDX_CUDA(cudaMemset(X.err.get(), 0, sizeof(int)));
+    });
+}
+
+// Waits for every rank's publish `j`, then sums the partial slots of parity j & 1.
+static void p2p_gather_partials(gdx_graph* g, PrP2P& X, int64_t j, double* out2) {
+    cudaStream_t s = g->stream;
+    k_p2p_wait<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)(j + 1) * X.world, X.err.get());
+    GDX_LAUNCH_CHECK();
+    std::vector<double> h(2 * X.world);
+    int herr = 0;
+    GDX_CUDA(cudaMemcpyAsync(h.data(), X.own_partials(int(j & 1)), h.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(&herr, X.err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    if (herr)
+        fail(GDX_ERR_CUDA, "CudaError: peer-memory exchange timed out (publish " +
+                               std::to_string(j) + ")");
+    out2[0] = out2[1] = 0.0;
+    for (int q = 0; q < X.world; ++q) {  // rank order: identical sums on every rank
+        out2[0] += h[2 * q];
+        out2[1] += h[2 * q + 1];
+    }
+}
+
+extern "C" int gdx_pr_p2p_init(gdx_graph* g, double* partials_out) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !partials_out)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
+        if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        auto& X = *g->pr_p2p;
+        cudaStream_t s = g->stream;
+        const int64_t j = X.publishes;
+        const int par = int(j & 1);
+        PrArgs a = make_args(g, P, 0.85, 0.0, 0);
+        a.peers = X.peer_contrib.get() + par * X.world;
+        a.npeers = X.world;
+        if (!P.partials.get()) P.partials.alloc(2);
+        GDX_CUDA(cudaMemsetAsync(P.partials.get(), 0, 2 * sizeof(double), s));
+        GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
+        if (j > 0)  // the previous publish must have landed everywhere before parity j&1 is reused
+            k_p2p_wait<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)j * X.world, X.err.get());
+        if (P.v_end > P.v_begin)
+            timed_launch(g, "pr_init", [&] {
+                k_pr_shard_init<<<blocks_for(P.v_end - P.v_begin, kPrBlock, g->num_sms * 8),
+                                  kPrBlock, 0, s>>>(a, P.partials.get());
+            });
+        k_p2p_publish<<<1, 1, 0, s>>>(P.partials.get(), nullptr, X.peer_slot.get() + par * X.world,
+                                      X.peer_ctr.get(), X.world);
+        GDX_LAUNCH_CHECK();
+        X.publishes = j + 1;
+        p2p_gather_partials(g, X, j, partials_out);
+    });
+}
+
+extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, double threshold,
+                                int32_t max_iter, double dangling_in, double* partials_out) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !partials_out)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
+        if (round < 0) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: negative round");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        auto& X = *g->pr_p2p;
+        cudaStream_t s = g->stream;
+        if (P.flags_cap < round + 1) {
+            const int32_t cap = std::max(round + 1, 2 * P.flags_cap);
+            DevBuf<int32_t> nf(cap);
+            P.flags = std::move(nf);
+            P.flags_cap = cap;
+        }
+        const int64_t j = X.publishes;  // this round's publish; it reads publish j-1
+        PrArgs a = make_args(g, P, damping, threshold, max_iter);
+        a.contrib0 = a.contrib1 = X.own_contrib(int((j - 1) & 1));
+        a.peers = X.peer_contrib.get() + (j & 1) * X.world;
+        a.npeers = X.world;
+        GDX_CUDA(cudaMemcpyAsync(P.dangling.get() + round % 3, &dangling_in, sizeof(double),
+                                 cudaMemcpyHostToDevice, s));
+        GDX_CUDA(cudaMemsetAsync(P.flags.get() + round, 0, 4, s));
+        k_p2p_wait<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)j * X.world, X.err.get());
+        GDX_LAUNCH_CHECK();
+        if (P.ngroups > 0)
+            timed_launch(g, "pr_edges", [&] { k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round); });
+        timed_launch(g, "pr_vertices", [&] {
+            k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
+                                             g->num_sms * 8),
+                                  kPrBlock, 0, s>>>(a, round);
+        });
+        k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + round,
+                                      X.peer_slot.get() + (j & 1) * X.world, X.peer_ctr.get(),
+                                      X.world);
+        GDX_LAUNCH_CHECK();
+        X.publishes = j + 1;
+        p2p_gather_partials(g, X, j, partials_out);
+    });
+}
+
+extern "C" int gdx_pr_p2p_close(gdx_graph* g) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        DeviceGuard dg(g->device);
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        g->pr_p2p.reset();
     });
 }

@@ -40,6 +40,30 @@ struct PrPlan {
     size_t smem = 0;
 };
 
+// Peer-memory exchange state of the sharded PageRank (pagerank.cu gdx_pr_p2p_*).
+struct PrP2P {
+    int32_t world = 0, rank = 0;
+    int64_t n = 0;
+    double* block = nullptr;            // own IPC-exported block (cudaMalloc)
+    std::vector<double*> bases;         // every rank's block (own + opened peers)
+    DevBuf<double*> peer_contrib;       // [2][world]: contrib buffer of each parity
+    DevBuf<double*> peer_slot;          // [2][world]: this rank's partial slot in every block
+    DevBuf<unsigned long long*> peer_ctr;  // [world]
+    DevBuf<int> err;                    // set by a timed-out wait
+    int64_t publishes = 0;              // publishes so far (identical on every rank)
+    double* own_contrib(int par) const { return block + par * n; }
+    double* own_partials(int par) const { return block + 2 * n + par * world * 2; }
+    unsigned long long* own_ctr() const {
+        return reinterpret_cast<unsigned long long*>(block + 2 * n + 4 * world);
+    }
+    size_t bytes() const { return (2 * size_t(n) + 4 * size_t(world) + 1) * sizeof(double); }
+    ~PrP2P() {
+        for (int q = 0; q < int(bases.size()); ++q)
+            if (q != rank && bases[q]) cudaIpcCloseMemHandle(bases[q]);
+        if (block) cudaFree(block);
+    }
+};
+
 // SSSP frontier workspace (sssp.cu).
 struct SsspWork {
     DevBuf<uint64_t> dist;   // 32- or 64-bit distances (reinterpreted)

@@ -129,10 +129,19 @@ class DeviceExecutor:
     def bc(self, sources):
         return self.g.bc(sources)
 
+    def bc_into(self, sources, out):
+        """gdx_bc into `out` (a device tensor is written in place)."""
+        self._staged(lambda o: self.g.bc(sources, out=o), out)
+
     def offsets(self):
         if self._off is None:
             self._off = self.g.download().offsets
         return self._off
+
+    def device_offsets(self, name: str):
+        """offsets / rev_offsets as a device tensor (partitioning without a host copy)."""
+        (t,) = self.g.device_arrays([name])
+        return t
 
     def rev_offsets(self):
         if getattr(self, "_roff", None) is None:
@@ -225,17 +234,23 @@ def sharded_tc(ex: Executor, group=None) -> int:
     return int(t.item())
 
 
-def sharded_bc(ex: Executor, sources: Sequence[int], group=None) -> np.ndarray:
-    """ComputeBC across ranks: source blocks + all-reduce of the partial scores."""
+def sharded_bc(ex: Executor, sources: Sequence[int], group=None, to_host: bool = True):
+    """ComputeBC across ranks: source blocks + all-reduce of the partial scores
+    (computed straight into the collective buffer when the executor can)."""
     import torch
     dist = _dist()
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     block = source_blocks(sources, world)[rank]
     n = ex.num_nodes()
-    part = ex.bc(block) if block else np.zeros(n, np.float64)
-    t = torch.from_numpy(np.ascontiguousarray(part, dtype=np.float64)).to(_device_for_collectives())
+    t = torch.zeros(n, dtype=torch.float64, device=_device_for_collectives())
+    if block:
+        into = getattr(ex, "bc_into", None)
+        if into is not None:
+            into(block, t)
+        else:
+            t.copy_(torch.from_numpy(np.ascontiguousarray(ex.bc(block), dtype=np.float64)))
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t.cpu().numpy()
+    return t.cpu().numpy() if to_host else t
 
 
 def _all_gather_slices(slice_buf, ranges, out, group=None):
@@ -250,6 +265,32 @@ def _all_gather_slices(slice_buf, ranges, out, group=None):
     for r, (a, b) in enumerate(ranges):
         if b > a:
             out[a:b].copy_(gathered[r * chunk: r * chunk + (b - a)])
+
+
+def balanced_ranges_device(offsets_t, parts: int) -> list[tuple[int, int]]:
+    """balanced_ranges(diff(offsets) + 1, parts) computed with torch on the
+    offsets' device (no host copy of the CSR)."""
+    import torch
+    n = offsets_t.numel() - 1
+    if n <= 0:
+        return [(0, 0)] * parts
+    w = (offsets_t[1:] - offsets_t[:-1]).to(torch.float64) + 1.0
+    csum = torch.cat([torch.zeros(1, dtype=torch.float64, device=w.device), torch.cumsum(w, 0)])
+    total = csum[-1]
+    t = total * torch.arange(1, parts, dtype=torch.float64, device=w.device) / parts
+    cuts = [0] + torch.searchsorted(csum, t, right=False).tolist() + [n]
+    cuts = np.maximum.accumulate(np.clip(np.asarray(cuts, dtype=np.int64), 0, n))
+    return [(int(cuts[i]), int(cuts[i + 1])) for i in range(parts)]
+
+
+def _partition(ex, kind: str, world: int):
+    """Vertex ranges of `kind` ("pr": by in-edges, "sssp": by out-edges)."""
+    dev = getattr(ex, "device_offsets", None)
+    if dev is not None:
+        return balanced_ranges_device(dev("rev_offsets" if kind == "pr" else "offsets"), world)
+    if kind == "pr":
+        return pr_ranges(ex.rev_offsets(), world)
+    return vertex_ranges(ex.offsets(), world)
 
 
 def pr_ranges(rev_offsets: np.ndarray, parts: int) -> list[tuple[int, int]]:
@@ -272,7 +313,7 @@ def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, gr
     n = ex.num_nodes()
     if n == 0:
         raise GraphdslError("RuntimeError", "RuntimeError: division by zero")
-    ranges = _cached_ranges(ex, "pr", world, lambda: pr_ranges(ex.rev_offsets(), world))
+    ranges = _cached_ranges(ex, "pr", world, lambda: _partition(ex, "pr", world))
     v0, v1 = ranges[rank]
     chunk = max(max(b - a for a, b in ranges), 1)
     f64 = dict(dtype=torch.float64, device=dev)
@@ -307,6 +348,54 @@ def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, gr
     return (out.cpu().numpy() if to_host else out), rounds
 
 
+def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_iter: int,
+                   group=None, to_host: bool = True):
+    """ComputePR across ranks with the exchange fused into the kernels over
+    peer memory (gdx_pr_p2p_*): pass B stores every new contrib value straight
+    into every rank's buffer over NVLink, partials are published with
+    system-scope atomics.  torch.distributed only carries the one-time IPC
+    handle exchange and the final rank gather.  Same result and rounds as
+    sharded_pr / gdx_pagerank."""
+    import torch
+    from ._lib import GraphdslError
+    dist = _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = ex.num_nodes()
+    if n == 0:
+        raise GraphdslError("RuntimeError", "RuntimeError: division by zero")
+    ranges = _cached_ranges(ex, "pr", world, lambda: _partition(ex, "pr", world))
+    v0, v1 = ranges[rank]
+    g = ex.g
+    if getattr(ex, "_p2p", None) != (world, rank, v0, v1):
+        ex.pr_setup(v0, v1)
+        mine = g.pr_p2p_setup(world, rank)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        g.pr_p2p_open(b"".join(allh))
+        ex._p2p = (world, rank, v0, v1)
+    dangling, _ = g.pr_p2p_init()
+    cap = 10 * n + 100
+    want = max_iter + 1 if max_iter >= 0 else 1
+    limit = min(want, cap)
+    rounds = limit
+    for r in range(limit):
+        dangling, unsettled = g.pr_p2p_round(r, damping, threshold, max_iter, dangling)
+        if unsettled == 0.0:
+            rounds = r + 1
+            break
+    else:
+        if limit < want:
+            raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} "
+                                "iterations without converging")
+    dev = _device_for_collectives()
+    chunk = max(max(b - a for a, b in ranges), 1)
+    rank_slice = torch.zeros(chunk, dtype=torch.float64, device=dev)
+    ex.pr_rank(rounds, rank_slice)
+    out = torch.zeros(n, dtype=torch.float64, device=dev)
+    _all_gather_slices(rank_slice, ranges, out, group)
+    return (out.cpu().numpy() if to_host else out), rounds
+
+
 def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats=None):
     """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact;
     numpy, or the collective-device tensor when ``to_host`` is False."""
@@ -318,7 +407,7 @@ def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats
     n = ex.num_nodes()
     if not 0 <= src < n:
         raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
-    v0, v1 = _cached_ranges(ex, "sssp", world, lambda: vertex_ranges(ex.offsets(), world))[rank]
+    v0, v1 = _cached_ranges(ex, "sssp", world, lambda: _partition(ex, "sssp", world))[rank]
     ex.sssp_setup(v0, v1)
     inf = (2**63 - 1) // 2
     d = torch.full((n,), inf, dtype=torch.int64, device=dev)

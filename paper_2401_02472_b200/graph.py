@@ -273,6 +273,30 @@ class DeviceGraph:
     def pr_shard_rank(self, rounds: int, rank_slice) -> None:
         check(_lib.load().gdx_pr_shard_rank(self.handle, int(rounds), _ptr(rank_slice)))
 
+    def pr_p2p_setup(self, world: int, rank: int) -> bytes:
+        h = C.create_string_buffer(64)
+        check(_lib.load().gdx_pr_p2p_setup(self.handle, int(world), int(rank), h))
+        return h.raw
+
+    def pr_p2p_open(self, handles: bytes) -> None:
+        buf = C.create_string_buffer(handles, len(handles))
+        check(_lib.load().gdx_pr_p2p_open(self.handle, buf))
+
+    def pr_p2p_init(self) -> tuple[float, float]:
+        out = (C.c_double * 2)()
+        check(_lib.load().gdx_pr_p2p_init(self.handle, out))
+        return out[0], out[1]
+
+    def pr_p2p_round(self, rnd: int, damping: float, threshold: float, max_iter: int,
+                     dangling_in: float) -> tuple[float, float]:
+        out = (C.c_double * 2)()
+        check(_lib.load().gdx_pr_p2p_round(self.handle, int(rnd), float(damping), float(threshold),
+                                           int(max_iter), float(dangling_in), out))
+        return out[0], out[1]
+
+    def pr_p2p_close(self) -> None:
+        check(_lib.load().gdx_pr_p2p_close(self.handle))
+
     def sssp_shard_setup(self, v_begin: int, v_end: int) -> None:
         check(_lib.load().gdx_sssp_shard_setup(self.handle, int(v_begin), int(v_end)))
 

@@ -207,3 +207,11 @@ def test_pr_ranges_balance_in_edges():
     roff = np.array([0, 50, 50, 51, 52, 100], np.int64)
     r = D.pr_ranges(roff, 2)
     assert r[0][0] == 0 and r[-1][1] == 5 and r[0][1] == r[1][0]
+
+
+def test_balanced_ranges_device_matches_numpy():
+    rng = np.random.default_rng(3)
+    deg = rng.integers(0, 50, size=5000)
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    for parts in (1, 2, 3, 8):
+        assert D.balanced_ranges_device(torch.from_numpy(off), parts) == D.vertex_ranges(off, parts)

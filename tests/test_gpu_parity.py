@@ -367,11 +367,16 @@ def _gpu_shard_worker(rank, world, port, q):
     u, v = p.gen_rmat_edges(n, 16 * n, 21)
     gd = p.build_from_edges(n, u, v, None, True)
     gu = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1, 100, 21)
-    r, rounds = D.sharded_pr(D.DeviceExecutor(G.DeviceGraph.from_csr(gd)), 0.85, 1e-9, 110)
+    exd = D.DeviceExecutor(G.DeviceGraph.from_csr(gd))
+    r, rounds = D.sharded_pr(exd, 0.85, 1e-9, 110)
+    # the peer-memory exchange (CUDA IPC between the ranks' processes), twice:
+    # the second call reuses the exported blocks (publish parity carries over)
+    r2, rounds2 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
+    r3, rounds3 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
     d = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gu)), 7)
     if rank == 0:
         er, erounds = p.pr(gd, 0.85, 1e-9, 110)
-        q.put((r, rounds, er, erounds, d, p.sssp(gu, 7)))
+        q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3))
     tdist.destroy_process_group()
 
 
@@ -389,10 +394,11 @@ def test_sharded_pr_sssp_device(gdx, world):
     procs = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    r, rounds, er, erounds, d, ed = q.get(timeout=500)
+    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3 = q.get(timeout=500)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    assert rounds == erounds
+    assert rounds == erounds == rounds2 == rounds3
     assert rel_err(r, er) < 1e-12
+    assert rel_err(r2, er) < 1e-12 and rel_err(r3, er) < 1e-12
     assert np.array_equal(d, ed)
