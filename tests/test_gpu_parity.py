@@ -373,10 +373,15 @@ def _gpu_shard_worker(rank, world, port, q):
     # the second call reuses the exported blocks (publish parity carries over)
     r2, rounds2 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
     r3, rounds3 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
-    d = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gu)), 7)
+    exu = D.DeviceExecutor(G.DeviceGraph.from_csr(gu))
+    d = D.sharded_sssp(exu, 7)
+    srcs = [0, 5, 5, 99, 4000, 17, 2048]
+    bc = D.sharded_bc(exu, srcs)
+    tc = D.sharded_tc(exu)
     if rank == 0:
         er, erounds = p.pr(gd, 0.85, 1e-9, 110)
-        q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3))
+        q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3,
+               bc, p.bc(gu, srcs), tc, p.tc(gu)))
     tdist.destroy_process_group()
 
 
@@ -394,7 +399,7 @@ def test_sharded_pr_sssp_device(gdx, world):
     procs = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3 = q.get(timeout=500)
+    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3, bc, ebc, tc, etc_ = q.get(timeout=500)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
@@ -402,3 +407,4 @@ def test_sharded_pr_sssp_device(gdx, world):
     assert rel_err(r, er) < 1e-12
     assert rel_err(r2, er) < 1e-12 and rel_err(r3, er) < 1e-12
     assert np.array_equal(d, ed)
+    assert rel_err(bc, ebc) < 1e-9 and tc == etc_
