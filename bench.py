@@ -334,7 +334,8 @@ def bench_sssp(torch, gdx, dist, args, pk, scale: int = 18) -> dict:
            "edges_visited_over_m": sts[-1]["edges_visited"] / dg.m,
            "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / args.steps,
-           "roofline": roofline(prof, "sssp_relax+sssp_frontier" if "sssp_relax" in prof
+           "roofline": roofline(prof, "sssp_graph" if "sssp_graph" in prof
+                                else "sssp_relax+sssp_frontier" if "sssp_relax" in prof
                                 else "sssp_rounds", sum(s["algorithmic_bytes"] for s in sts), pk),
            "gpu_launches": int(sum(v[1] for v in prof.values()))}
     if scale > 18:  # C1 is checked bit-exactly by the tests; larger graphs by certificate

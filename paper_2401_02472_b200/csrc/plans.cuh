@@ -79,6 +79,14 @@ struct SsspWork {
     int32_t shard_v0 = 0, shard_v1 = 0;
     DevBuf<int2> shard_queue;
     DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges]
+    // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    void* gkey[2][4] = {};
+    DevBuf<unsigned long long> graph_acc, graph_ovf;
+    ~SsspWork() {
+        for (auto& e : gexec)
+            if (e) cudaGraphExecDestroy(e);
+    }
 };
 
 // Triangle-counting workspace (tc.cu).

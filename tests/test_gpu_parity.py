@@ -155,7 +155,7 @@ def test_sssp_c1_bit_exact(gdx, port):
             assert st["rounds"] >= 2 and st["edges_visited"] >= g.m * 0.5
 
 
-@pytest.mark.parametrize("mode", ["persistent", "scan"])
+@pytest.mark.parametrize("mode", ["persistent", "scan", "graph"])
 def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
     """Both SSSP executions (persistent cooperative kernel for small graphs,
     frontier-scan rounds for large ones) are bit-exact on config 1."""
@@ -167,7 +167,7 @@ def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
         assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
 
 
-@pytest.mark.parametrize("mode", ["persistent", "scan"])
+@pytest.mark.parametrize("mode", ["persistent", "scan", "graph"])
 def test_sssp_64bit_distances(gdx, port, mode, monkeypatch):
     monkeypatch.setenv("GDX_SSSP_MODE", mode)
     u, v = port.gen_rmat_edges(5000, 40000, 8)

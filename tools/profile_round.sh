@@ -20,6 +20,6 @@ cap() {  # name algo kernel-regex skip
 cap pr_edges pr k_pr_edges 2
 cap pr_vertices pr k_pr_vertices 2
 cap tc tc k_tc_oriented 0
-cap sssp_c1 sssp k_sssp_rounds 1
+cap sssp_c1_relax sssp k_sssp_scan_relax 3
 cap sssp_c5_relax sssp26 k_sssp_scan_relax 3
 cap bc bc k_bc_cta 0
