@@ -58,9 +58,8 @@ struct PrArgs {
     int32_t max_iter;
     // edge-aligned two-pass plan (k_pr_edges + k_pr_vertices)
     int32_t m, nnz;
-    const int32_t* __restrict__ nz_row;   // vertex of the k-th row with in-edges
-    const int32_t* __restrict__ nz_end;   // rev_offsets[nz_row[k] + 1]
-    const int32_t* __restrict__ grp_row;  // nz row holding edge 8g
+    const int2* __restrict__ nz;          // k-th row with in-edges: (vertex, rev_offsets[vertex + 1])
+    const int2* __restrict__ grp;         // per 8-edge group: (nz index of its first row, that row's end)
     double* row_sum;                      // per vertex, zero between rounds
     // row range [v_begin, v_end) and its in-edges [e_begin, e_end) (the whole
     // graph on one GPU; one rank's slice when sharded, gdx_pr_shard_*)
@@ -273,12 +272,14 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
         for (int k = 0; k < kEdgeGroup; ++k)
             v[k] = k >= klo && k < khi ? __ldg(&contrib[s[k]]) : 0.0;
     }
-    int32_t key = any ? a.grp_row[g] : INT32_MAX;
+    // grp[g] = (first non-empty row of the group, that row's end): one load
+    const int2 gk = any ? a.grp[g] : make_int2(INT32_MAX, 0);
+    int32_t key = gk.x;
     const int32_t first = key;
     double run = 0.0, first_val = 0.0;
     bool first_done = false;
     if (any) {
-        int32_t end = a.nz_end[key];
+        int32_t end = gk.y, row = -1;  // row of `key` once loaded from nz (not needed for `first`)
 #pragma unroll
         for (int k = 0; k < kEdgeGroup; ++k) {
             if (k >= klo && k < khi) {
@@ -287,10 +288,12 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
                         first_val = run;
                         first_done = true;
                     } else {
-                        a.row_sum[a.nz_row[key]] = run;
+                        a.row_sum[row] = run;
                     }
                     run = 0.0;
-                    end = a.nz_end[++key];
+                    const int2 nk = a.nz[++key];  // (row, end) of the next non-empty row
+                    row = nk.x;
+                    end = nk.y;
                 }
                 run += v[k];
             }
@@ -300,7 +303,7 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
                 first_val = run;
                 first_done = true;
             } else {
-                a.row_sum[a.nz_row[key]] = run;
+                a.row_sum[row] = run;
             }
             run = 0.0;
             ++key;
@@ -319,15 +322,15 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
     if (first_done) {
         const double tot = first_val + (lane > 0 && pkey == first ? pval : 0.0);
         const int64_t warp_e0 = e_base + (g & ~int64_t(31)) * kEdgeGroup;
-        const int64_t start = first > 0 ? a.nz_end[first - 1] : e_begin;
-        const int32_t row = a.nz_row[first];
+        const int64_t start = first > 0 ? a.nz[first - 1].y : e_begin;
+        const int32_t row = a.nz[first].x;
         if (start < warp_e0)
             atomicAdd(&a.row_sum[row], tot);  // row began in an earlier warp's edges
         else
             a.row_sum[row] = tot;
     }
     // the warp's trailing row continues into the next warp's edges
-    if (lane == 31 && val != 0.0 && key < a.nnz) atomicAdd(&a.row_sum[a.nz_row[key]], val);
+    if (lane == 31 && val != 0.0 && key < a.nnz) atomicAdd(&a.row_sum[a.nz[key].x], val);
 }
 
 template <bool R>
@@ -442,30 +445,29 @@ __global__ void k_pr_nz_flags(int32_t v0, int32_t cnt, const int32_t* __restrict
         flag[i] = rev_offsets[v0 + i + 1] > rev_offsets[v0 + i];
 }
 __global__ void k_pr_nz_fill(int32_t v0, int32_t cnt, const int32_t* __restrict__ rev_offsets,
-                             const int32_t* __restrict__ pos, int32_t* nz_row, int32_t* nz_end) {
+                             const int32_t* __restrict__ pos, int2* nz) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = v0 + i;
         if (rev_offsets[v + 1] > rev_offsets[v]) {
-            nz_row[pos[i]] = int32_t(v);
-            nz_end[pos[i]] = rev_offsets[v + 1];
+            nz[pos[i]] = make_int2(int32_t(v), rev_offsets[v + 1]);
         }
     }
 }
 __global__ void k_pr_grp_rows(int64_t ngroups, int64_t e_base, int64_t e_begin, int32_t nnz,
-                              const int32_t* __restrict__ nz_end, int32_t* grp_row) {
+                              const int2* __restrict__ nz, int2* grp) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = max(e_base + g * kEdgeGroup, e_begin);
-        int32_t lo = 0, hi = nnz;  // first k with nz_end[k] > e
+        int32_t lo = 0, hi = nnz;  // first k whose row ends after edge e
         while (lo < hi) {
             const int32_t mid = (lo + hi) >> 1;
-            if (nz_end[mid] <= e)
+            if (nz[mid].y <= e)
                 lo = mid + 1;
             else
                 hi = mid;
         }
-        grp_row[g] = lo;
+        grp[g] = make_int2(lo, lo < nnz ? nz[lo].y : 0);
     }
 }
 
@@ -580,18 +582,17 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     P.e_end = eb[1];
     P.e_base = P.e_begin & ~int64_t(kEdgeGroup - 1);
     P.nnz = last[0] + last[1];
-    P.nz_row.alloc(size_t(P.nnz) + 1);
-    P.nz_end.alloc(size_t(P.nnz) + 1);
+    P.nz.alloc(size_t(P.nnz) + 1);
     if (cnt > 0) {
         k_pr_nz_fill<<<grid, 256, 0, s>>>(v_begin, cnt, g->rev_offsets.get(), pos.get(),
-                                          P.nz_row.get(), P.nz_end.get());
+                                          P.nz.get());
         GDX_LAUNCH_CHECK();
     }
     P.ngroups = (P.e_end - P.e_base + kEdgeGroup - 1) / kEdgeGroup;
-    P.grp_row.alloc(size_t(P.ngroups) + 1);
+    P.grp.alloc(size_t(P.ngroups) + 1);
     if (P.ngroups > 0) {
         k_pr_grp_rows<<<blocks_for(P.ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
-            P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz_end.get(), P.grp_row.get());
+            P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz.get(), P.grp.get());
         GDX_LAUNCH_CHECK();
     }
     P.row_sum.alloc(n);
@@ -695,9 +696,8 @@ static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshol
     a.max_iter = max_iter;
     a.m = g->m;
     a.nnz = P.nnz;
-    a.nz_row = P.nz_row.get();
-    a.nz_end = P.nz_end.get();
-    a.grp_row = P.grp_row.get();
+    a.nz = P.nz.get();
+    a.grp = P.grp.get();
     a.row_sum = P.row_sum.get();
     a.v_begin = P.shard ? P.v_begin : 0;
     a.v_end = P.shard ? P.v_end : g->n;

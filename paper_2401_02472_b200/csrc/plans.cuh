@@ -25,8 +25,8 @@ struct PrPlan {
     DevBuf<int32_t> flags;                // per-round "unsettled" votes
     // edge-aligned two-pass plan (variant 60)
     int32_t nnz = 0;
-    DevBuf<int32_t> nz_row, nz_end;       // non-empty rows of the reverse CSR and their ends
-    DevBuf<int32_t> grp_row;              // nz row holding edge 8g
+    DevBuf<int2> nz;                      // non-empty rows of the reverse CSR: (vertex, end)
+    DevBuf<int2> grp;                     // per 8-edge group: (nz index of its first row, its end)
     DevBuf<double> row_sum;               // per-vertex gather sums (zero between rounds)
     int32_t v_begin = 0, v_end = 0;       // row range of the plan
     int64_t e_begin = 0, e_end = 0, e_base = 0, ngroups = 0;
