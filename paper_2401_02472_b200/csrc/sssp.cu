@@ -8,9 +8,9 @@
 // Default execution (gdx_sssp): frontier-scan rounds, looped on the device by
 // a CUDA graph with a conditional WHILE node (no host round trip per round):
 //   * k_sssp_scan_frontier: vertices whose distance dropped since they were
-//     last expanded (dist < prev; prev := dist) emit relaxation items of <= 128
+//     last expanded (dist < prev; prev := dist) emit relaxation items of <= 64
 //     out-edges (hubs are split), one global atomic per 2048-vertex chunk;
-//   * k_sssp_scan_relax: 16 lanes per item, each lane's 8 edges loaded
+//   * k_sssp_scan_relax: 16 lanes per item, each lane's 4 edges loaded
 //     together (dests/weights, then the dist[u] gathers, then the atomicMin of
 //     the improving ones);
 //   * k_sssp_graph_finish: counts the round, clears the counters and keeps
@@ -360,7 +360,7 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
 // (dist < prev), into the local replica, and the caller merges the replicas
 // with an element-wise MIN all-reduce (distributed.py sharded_sssp).
 // ---------------------------------------------------------------------------
-constexpr int kShardChunk = 128;  // edges per relaxation item
+constexpr int kShardChunk = 64;  // edges per relaxation item (C5: 23.7 ms vs 26.1 at 128, 25.6 at 32)
 
 // Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
 // distance dropped since they were last expanded (dist < prev; prev := dist).
