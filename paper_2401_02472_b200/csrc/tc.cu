@@ -210,9 +210,9 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
     }
 }
 
-constexpr int kTcStage = 1024;  // ints of staged N+ lists per warp
+constexpr int kTcStage = 512;  // ints of staged N+ lists per warp
 
-__global__ void __launch_bounds__(kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
+__global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, int32_t v_end,
                                                           const int32_t* __restrict__ off_plus,
                                                           const int32_t* __restrict__ adj,
                                                           unsigned long long* acc) {
