@@ -79,6 +79,29 @@ __device__ inline double xf_ratio(double2 a, double2 b) {
 // critical path is a few dependent memory steps instead of one per neighbour.
 constexpr int kNb = 4;
 
+// Items whose adjacency exceeds kHeavy edges are deferred to a warp-cooperative
+// pass at the end of the block's chunk (lanes stride over the edges, partial
+// sums combined with warp shuffles): on skewed graphs a hub's 10^5 neighbours
+// would otherwise serialise one thread for the whole level.
+constexpr int kHeavy = 64;
+
+__device__ inline double2 xf_warp_sum(double2 a) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double2 b;
+        b.x = __shfl_xor_sync(0xffffffffu, a.x, o);
+        b.y = __shfl_xor_sync(0xffffffffu, a.y, o);
+        a = xf_add(a, b);
+    }
+    return a;
+}
+
+__device__ inline double warp_sum(double d) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    return d;
+}
+
 __device__ inline long long ld_volatile_ll(const long long* p) {
     return *reinterpret_cast<const volatile long long*>(p);
 }
@@ -97,17 +120,28 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
     constexpr int kBcQueue = 4 * kBcBlock;
     cg::grid_group grid = cg::this_grid();
     __shared__ uint64_t s_q[kBcQueue];
-    __shared__ int s_qn;
+    __shared__ int s_qn, s_hn;
+    __shared__ long long s_h[kBcBlock];  // deferred heavy items (log indices)
     __shared__ long long s_gpos;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     unsigned long long fscan = 0, dag = 0;
     long long beg = 0, end = a.S;
     int L = 0;
     for (;; ++L) {
         for (long long base = beg + (long long)blockIdx.x * kBcBlock; base < end;
              base += (long long)gridDim.x * kBcBlock) {
-            if (tid == 0) s_qn = 0;
+            if (tid == 0) s_qn = s_hn = 0;
             __syncthreads();
+            auto push = [&](int32_t s, int32_t w) {
+                const uint64_t x = (uint64_t(s) << 32) | uint32_t(w);
+                const int pos = atomicAdd(&s_qn, 1);
+                if (pos < kBcQueue) {
+                    s_q[pos] = x;
+                } else {
+                    const long long p = atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], 1ull);
+                    a.log[end + p] = x;
+                }
+            };
             const long long idx = base + tid;
             if (idx < end) {
                 const uint64_t item = a.log[idx];
@@ -116,18 +150,13 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
                 int32_t* lev = a.level + sb;
                 double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
                 const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
-                fscan += oe - ob;
-                auto push = [&](int32_t w) {
-                    const uint64_t x = (uint64_t(s) << 32) | uint32_t(w);
-                    const int pos = atomicAdd(&s_qn, 1);
-                    if (pos < kBcQueue) {
-                        s_q[pos] = x;
-                    } else {
-                        const long long p = atomicAdd((unsigned long long*)&a.lvl_cnt[L + 1], 1ull);
-                        a.log[end + p] = x;
-                    }
-                };
-                for (int32_t e = ob; e < oe; e += kNb) {
+                const bool heavy = oe - ob > kHeavy ||
+                                   (!a.undirected && L > 0 &&
+                                    a.in_offsets[v + 1] - a.in_offsets[v] > kHeavy);
+                if (heavy) s_h[atomicAdd(&s_hn, 1)] = idx;
+                const int32_t oend = heavy ? ob : oe;  // heavy: no light pass
+                fscan += oend - ob;
+                for (int32_t e = ob; e < oend; e += kNb) {
                     int32_t w[kNb], lw[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
@@ -149,10 +178,10 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
                             acc = xf_add(acc, sg[k]);
                             ++dag;
                         }
-                        if (got[k]) push(w[k]);
+                        if (got[k]) push(s, w[k]);
                     }
                 }
-                if (!a.undirected && L > 0) {
+                if (!heavy && !a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
                     fscan += ie - ib;
                     for (int32_t e = ib; e < ie; e += kNb) {
@@ -174,7 +203,40 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
                             }
                     }
                 }
-                a.sig[sb + v] = acc;
+                if (!heavy) a.sig[sb + v] = acc;
+            }
+            __syncthreads();
+            // heavy items: one warp each, lanes stride over the adjacency
+            for (int h = tid >> 5; h < s_hn; h += kBcBlock / 32) {
+                const uint64_t item = a.log[s_h[h]];
+                const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
+                const int64_t sb = int64_t(s) * a.n;
+                int32_t* lev = a.level + sb;
+                double2 acc = make_double2(L == 0 && lane == 0 ? 1.0 : 0.0, 0.0);
+                const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+                if (lane == 0) fscan += oe - ob;
+                for (int32_t e = ob + lane; e < oe; e += 32) {
+                    const int32_t w = a.dests[e];
+                    const int32_t lw = lev[w];
+                    if (a.undirected && L > 0 && lw == L - 1) {
+                        acc = xf_add(acc, a.sig[sb + w]);
+                        ++dag;
+                    }
+                    if (lw == -1 && atomicCAS(&lev[w], -1, L + 1) == -1) push(s, w);
+                }
+                if (!a.undirected && L > 0) {
+                    const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
+                    if (lane == 0) fscan += ie - ib;
+                    for (int32_t e = ib + lane; e < ie; e += 32) {
+                        const int32_t p = a.in_srcs[e];
+                        if (lev[p] == L - 1) {
+                            acc = xf_add(acc, a.sig[sb + p]);
+                            ++dag;
+                        }
+                    }
+                }
+                acc = xf_warp_sum(acc);
+                if (lane == 0) a.sig[sb + v] = acc;
             }
             __syncthreads();
             const int qn = min(s_qn, kBcQueue);
@@ -207,24 +269,33 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_forward(BcArgs a) {
 template <int kBcBlock>
 __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
     cg::grid_group grid = cg::this_grid();
-    const int tid = threadIdx.x;
+    __shared__ int s_hn;
+    __shared__ long long s_h[kBcBlock];  // deferred heavy items (log indices)
+    const int tid = threadIdx.x, lane = tid & 31;
     const long long total = (long long)a.ctr[kTail];
     const int levels = int(a.ctr[kLevels]);
     unsigned long long bscan = 0, dag = 0;
     long long end = total;
     for (int L = levels - 1; L >= 0; --L) {
         const long long beg = end - a.lvl_cnt[L];
-        for (long long idx = beg + (long long)blockIdx.x * kBcBlock + tid; idx < end;
-             idx += (long long)gridDim.x * kBcBlock) {
+        for (long long base = beg + (long long)blockIdx.x * kBcBlock; base < end;
+             base += (long long)gridDim.x * kBcBlock) {
+          if (tid == 0) s_hn = 0;
+          __syncthreads();
+          const long long idx = base + tid;
+          if (idx < end) {
             const uint64_t item = a.log[idx];
             const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
             const int64_t sb = int64_t(s) * a.n;
             const int32_t* lev = a.level + sb;
             const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+            const bool heavy = oe - ob > kHeavy;
+            if (heavy) s_h[atomicAdd(&s_hn, 1)] = idx;
+            const int32_t oend = heavy ? ob : oe;
             const double2 sv = a.sig[sb + v];
             double d = 0.0;
-            bscan += oe - ob;
-            for (int32_t e = ob; e < oe; e += kNb) {
+            bscan += oend - ob;
+            for (int32_t e = ob; e < oend; e += kNb) {
                 int32_t w[kNb];
                 bool ch[kNb];
                 double2 sw[kNb];
@@ -245,8 +316,38 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
                         ++dag;
                     }
             }
-            a.delta[sb + v] = d;
-            if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
+            if (!heavy) {
+                a.delta[sb + v] = d;
+                if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
+            }
+          }
+          __syncthreads();
+          for (int h = tid >> 5; h < s_hn; h += kBcBlock / 32) {
+            const uint64_t item = a.log[s_h[h]];
+            const int32_t s = int32_t(item >> 32), v = int32_t(item & 0xffffffffu);
+            const int64_t sb = int64_t(s) * a.n;
+            const int32_t* lev = a.level + sb;
+            const int32_t ob = a.offsets[v], oe = a.offsets[v + 1];
+            const double2 sv = a.sig[sb + v];
+            double d = 0.0;
+            if (lane == 0) bscan += oe - ob;
+            for (int32_t e = ob + lane; e < oe; e += 32) {
+                const int32_t w = a.dests[e];
+                if (lev[w] == L + 1) {
+                    const double2 sw = a.sig[sb + w];
+                    if (sw.x > 0.0) {
+                        d += xf_ratio(sv, sw) * (1.0 + a.delta[sb + w]);
+                        ++dag;
+                    }
+                }
+            }
+            d = warp_sum(d);
+            if (lane == 0) {
+                a.delta[sb + v] = d;
+                if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
+            }
+          }
+          __syncthreads();
         }
         end = beg;
         grid.sync();
@@ -295,6 +396,7 @@ struct BcCtaArgs {
     const int32_t* __restrict__ in_srcs;
     const int32_t* __restrict__ sources;
     BcRec* rec;        // [grid][n]
+    bool any_heavy;    // some vertex has more than kHeavy out- (or in-) edges
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
     double* bc;
@@ -325,14 +427,96 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, double2 sig) {
 // CS CTAs (a thread-block cluster) share one source: the level barrier is a
 // cluster barrier and the queue tail lives in CTA 0's shared memory (DSMEM
 // atomics), so a source's levels are spread over CS * 1024 threads.
-template <int CS>
+// Heavy items of the CTA kernel (one warp each, lanes stride over the
+// adjacency).  Out of line so their registers do not weigh on the light path.
+__device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* rec, int4* log,
+                                                  const int* s_h, int hn, int L, int end,
+                                                  int* s_next, unsigned long long& fscan,
+                                                  unsigned long long& dag) {
+    const int ltid = threadIdx.x, lane = ltid & 31;
+    for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
+        const int4 it = log[s_h[h]];
+        const int32_t v = it.x, ob = it.y, oe = it.z;
+        double2 acc = make_double2(L == 0 && lane == 0 ? 1.0 : 0.0, 0.0);
+        if (lane == 0) fscan += oe - ob;
+        for (int32_t e = ob + lane; e < oe; e += 32) {
+            const int32_t w = a.dests[e];
+            int32_t lw;
+            double2 sg;
+            rec_level_sigma(rec + w, lw, sg);
+            if (a.undirected && L > 0 && lw == L - 1) {
+                acc = xf_add(acc, sg);
+                ++dag;
+            }
+            if (lw == -1) {
+                const int32_t w0 = a.offsets[w], w1 = a.offsets[w + 1];
+                if (atomicCAS(&rec[w].level, -1, L + 1) == -1)
+                    log[end + atomicAdd(&s_next[L % 3], 1)] = make_int4(w, w0, w1, 0);
+            }
+        }
+        if (!a.undirected && L > 0) {
+            const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
+            if (lane == 0) fscan += ie - ib;
+            for (int32_t e = ib + lane; e < ie; e += 32) {
+                int32_t lp;
+                double2 sg;
+                rec_level_sigma(rec + a.in_srcs[e], lp, sg);
+                if (lp == L - 1) {
+                    acc = xf_add(acc, sg);
+                    ++dag;
+                }
+            }
+        }
+        acc = xf_warp_sum(acc);
+        if (lane == 0) rec_store_sigma(rec + v, L, acc);
+    }
+}
+
+__device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec* rec, const int4* log,
+                                                   const int* s_h, int hn, int Lb, int32_t src,
+                                                   unsigned long long& bscan,
+                                                   unsigned long long& dag) {
+    const int ltid = threadIdx.x, lane = ltid & 31;
+    for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
+        const int4 it = log[s_h[h]];
+        const int32_t v = it.x, ob = it.y, oe = it.z;
+        int32_t lv;
+        double2 sv;
+        rec_level_sigma(rec + v, lv, sv);
+        double d = 0.0;
+        if (lane == 0) bscan += oe - ob;
+        for (int32_t e = ob + lane; e < oe; e += 32) {
+            int32_t lw;
+            double2 sw;
+            double dw;
+            rec_all(rec + a.dests[e], lw, sw, dw);
+            if (lw == Lb + 1 && sw.x > 0.0) {
+                d += xf_ratio(sv, sw) * (1.0 + dw);
+                ++dag;
+            }
+        }
+        d = warp_sum(d);
+        if (lane == 0) {
+            rec[v].delta = d;
+            if (v != src) atomicAdd(&a.bc[v], d);
+        }
+    }
+}
+
+// HEAVY = false compiles the kernel without the heavy-item paths (graphs whose
+// maximum degree is at most kHeavy, e.g. road-like grids): no extra barrier and
+// no register pressure from code that never runs.
+template <int CS, bool HEAVY>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(BcCtaArgs a) {
     __shared__ int s_next_local[3];
+    __shared__ int s_hn;
+    __shared__ int s_h[kBcCta];  // this CTA's deferred heavy items (log indices) of a level
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = int(cluster.block_rank());
     int* s_next = cluster.map_shared_rank(s_next_local, 0);
     const int tid = crank * kBcCta + int(threadIdx.x);
     const int ltid = threadIdx.x;
+    if (ltid == 0) s_hn = 0;
     constexpr int kStride = CS * kBcCta;
     const int64_t slot = blockIdx.x / CS;
     const int32_t nslots = gridDim.x / CS;
@@ -352,10 +536,23 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // ---- forward: iterateInBFS ----
         int beg = 0, end = 1, L = 0;
         for (;; ++L) {
+            int deferred = 0;
             for (int i = beg + tid; i < end; i += kStride) {
                 // the log entry carries v's out-edge range (one dependent load fewer)
                 const int4 it = log[i];
                 const int32_t v = it.x, ob = it.y, oe = it.z;
+                bool heavy = HEAVY && (oe - ob > kHeavy ||
+                                       (!a.undirected && L > 0 &&
+                                        a.in_offsets[v + 1] - a.in_offsets[v] > kHeavy));
+                if (heavy) {
+                    const int hp = atomicAdd(&s_hn, 1);
+                    if (hp < kBcCta) {
+                        s_h[hp] = i;
+                        deferred = 1;
+                        continue;
+                    }
+                    heavy = false;  // list full: this item runs on its own thread
+                }
                 double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
                 fscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
@@ -413,6 +610,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 rec_store_sigma(rec + v, L, acc);
             }
+            // heavy items of this CTA: one warp each, lanes stride over the adjacency
+            // (graphs without a vertex above kHeavy skip the extra barrier)
+            if (HEAVY && __syncthreads_count(deferred) > 0) {
+                bc_cta_heavy_forward(a, rec, log, s_h, min(s_hn, kBcCta), L, end, s_next, fscan, dag);
+                __syncthreads();
+                if (ltid == 0) s_hn = 0;
+            }
             // one barrier per level: level L pushes to tail L % 3; the tail of
             // level L+2 (last read right after the previous barrier) is reset now
             cluster.sync();
@@ -434,9 +638,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // ---- backward: iterateInReverse ----
         for (int Lb = levels - 1; Lb >= 0; --Lb) {
             const int b0 = loff[Lb], b1 = loff[Lb + 1];
+            int deferred = 0;
             for (int i = b0 + tid; i < b1; i += kStride) {
                 const int4 it = log[i];
                 const int32_t v = it.x, ob = it.y, oe = it.z;
+                if (HEAVY && oe - ob > kHeavy) {
+                    const int hp = atomicAdd(&s_hn, 1);
+                    if (hp < kBcCta) {
+                        s_h[hp] = i;
+                        deferred = 1;
+                        continue;
+                    }
+                }
                 int32_t lv;
                 double2 sv;
                 rec_level_sigma(rec + v, lv, sv);
@@ -465,6 +678,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 rec[v].delta = d;
                 if (v != src) atomicAdd(&a.bc[v], d);
             }
+            if (HEAVY && __syncthreads_count(deferred) > 0) {
+                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, bscan, dag);
+                __syncthreads();
+                if (ltid == 0) s_hn = 0;
+            }
             cluster.sync();
         }
         // restore `level` for the slot's next source
@@ -485,6 +703,27 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         atomicAdd(&a.ctr[kReached], reached);
         atomicMax(&a.ctr[kLevels], levels_max);
     }
+}
+
+__global__ void k_max_degree(int32_t n, const int32_t* __restrict__ off, int32_t* out) {
+    int32_t m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, off[v + 1] - off[v]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+static int32_t max_degree(gdx_graph* g, const int32_t* off) {
+    if (!off || g->n == 0) return 0;
+    DevBuf<int32_t> d(1);
+    GDX_CUDA(cudaMemsetAsync(d.get(), 0, 4, g->stream));
+    k_max_degree<<<blocks_for(g->n, 256, g->num_sms * 4), 256, 0, g->stream>>>(g->n, off, d.get());
+    GDX_LAUNCH_CHECK();
+    int32_t h = 0;
+    GDX_CUDA(cudaMemcpyAsync(&h, d.get(), 4, cudaMemcpyDeviceToHost, g->stream));
+    GDX_CUDA(cudaStreamSynchronize(g->stream));
+    return h;
 }
 
 static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
@@ -531,6 +770,10 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.in_srcs = g->rev_srcs.get();
     a.sources = W.sources.get();
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
+    if (W.max_deg < 0)
+        W.max_deg = std::max(max_degree(g, g->offsets.get()),
+                             g->directed ? max_degree(g, g->rev_offsets.get()) : 0);
+    a.any_heavy = W.max_deg > kHeavy;
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
@@ -538,12 +781,21 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     if (g->directed && (!a.in_offsets || !a.in_srcs))
         fail(GDX_ERR_UNSUPPORTED, "Unsupported: directed BC needs the reverse CSR");
     timed_launch(g, "bc_cta", [&] {
-        if (CS == 4)
-            k_bc_cta<4><<<grid, kBcCta, 0, s>>>(a);
-        else if (CS == 2)
-            k_bc_cta<2><<<grid, kBcCta, 0, s>>>(a);
-        else
-            k_bc_cta<1><<<grid, kBcCta, 0, s>>>(a);
+        if (a.any_heavy) {
+            if (CS == 4)
+                k_bc_cta<4, true><<<grid, kBcCta, 0, s>>>(a);
+            else if (CS == 2)
+                k_bc_cta<2, true><<<grid, kBcCta, 0, s>>>(a);
+            else
+                k_bc_cta<1, true><<<grid, kBcCta, 0, s>>>(a);
+        } else {
+            if (CS == 4)
+                k_bc_cta<4, false><<<grid, kBcCta, 0, s>>>(a);
+            else if (CS == 2)
+                k_bc_cta<2, false><<<grid, kBcCta, 0, s>>>(a);
+            else
+                k_bc_cta<1, false><<<grid, kBcCta, 0, s>>>(a);
+        }
     });
     ++launches;
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
@@ -584,11 +836,18 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         GDX_CUDA(cudaMemsetAsync(W.bc.get(), 0, n * sizeof(double), s));
         unsigned long long totals[kBcCtrs] = {};
         int launches = 0, max_levels = 0;
-        // CTA-per-source mode when there are enough sources to fill the GPU
-        // with independent BFS trees (GDX_BC_MODE=grid|cta overrides).
+        // CTA-cluster-per-source mode when there are enough sources to fill
+        // the GPU with independent BFS trees, or when no vertex has more than
+        // kHeavy edges (low-degree, typically high-diameter graphs: barrier
+        // latency dominates, measured 2x faster even for one source); the
+        // grid-wide kernels otherwise (few sources on skewed graphs, whose
+        // wide levels want every SM).  GDX_BC_MODE=grid|cta overrides.
         const char* mode = std::getenv("GDX_BC_MODE");
+        if (W.max_deg < 0 && nsrc > 0)
+            W.max_deg = std::max(max_degree(g, g->offsets.get()),
+                                 g->directed ? max_degree(g, g->rev_offsets.get()) : 0);
         const bool cta_mode = mode ? std::string(mode) == "cta"
-                                   : nsrc >= std::max(16, g->num_sms / 4);
+                                   : nsrc >= std::max(16, g->num_sms / 4) || W.max_deg <= kHeavy;
         if (nsrc > 0 && cta_mode) {
             run_bc_cta(g, hsrc, totals, launches, max_levels);
         } else if (nsrc > 0) {
