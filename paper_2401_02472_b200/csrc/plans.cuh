@@ -93,6 +93,8 @@ struct SsspWork {
 struct TcPlan {
     DevBuf<unsigned long long> acc;
     DevBuf<int32_t> hi_start;  // first index of N(v) with dest > v
+    DevBuf<int32_t> heavy, heavy_cnt;  // degree binning: vertices with |N+(v)| > kTcHeavy
+    DevBuf<long long> heavy_pre;       // their pair prefix
     DevBuf<int32_t> off_plus;  // oriented CSR (undirected graphs): N+(v) = N(v) ∩ (v, inf)
     DevBuf<int32_t> adj_plus;
     DevBuf<uint8_t> scan_tmp;

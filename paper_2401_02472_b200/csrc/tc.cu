@@ -210,6 +210,7 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
     }
 }
 
+constexpr int kTcHeavy = 256;  // |N+(v)| above which a vertex's pairs are binned to k_tc_heavy
 constexpr int kTcStage = 512;  // ints of staged N+ lists per warp
 
 __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, int32_t v_end,
@@ -241,7 +242,9 @@ __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, in
         __syncwarp();
         const int32_t* A = staged ? sA - r0 : adj;  // A[x] for x in [r0, last_end)
         // pairs (v, i): u = N+(v)[i] for i < len-1 (the last u has no tail)
-        const int32_t np = max(oe - ob - 1, 0);
+        // heavy vertices (|N+(v)| > kTcHeavy) are left to k_tc_heavy, which
+        // spreads their pairs over the whole grid instead of one warp
+        const int32_t np = oe - ob > kTcHeavy ? 0 : max(oe - ob - 1, 0);
         int incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -289,9 +292,40 @@ __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, in
                 w[t] = q0 + 4 * t < cbe ? adj4[(q0 >> 2) + t]
                                         : make_int4(INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX);
             int32_t p = cpu + 1;  // tail of N+(v) after u: A[p .. ckoe)
+            scanned += (ckoe - p) + (cbe - cbb) + 2;
+            const int32_t la = ckoe - p, lb = cbe - cbb;
+            if (la > 16 * lb + 16 || lb > 16 * la + 16) {
+                // very unequal lists (hubs of skewed graphs): walk the short one,
+                // binary-search the long one (O(short * log long), not O(long))
+                unsigned long long c = 0;
+                if (la <= lb) {
+                    int32_t lo = cbb;
+                    for (int32_t i = p; i < ckoe && lo < cbe; ++i) {
+                        const int32_t x = A[i];
+                        int32_t hi = cbe;
+                        while (lo < hi) {
+                            const int32_t mid = (lo + hi) >> 1;
+                            if (adj[mid] < x) lo = mid + 1; else hi = mid;
+                        }
+                        if (lo < cbe && adj[lo] == x) ++c;
+                    }
+                } else {
+                    int32_t lo = p;
+                    for (int32_t i = cbb; i < cbe && lo < ckoe; ++i) {
+                        const int32_t x = adj[i];
+                        int32_t hi = ckoe;
+                        while (lo < hi) {
+                            const int32_t mid = (lo + hi) >> 1;
+                            if (A[mid] < x) lo = mid + 1; else hi = mid;
+                        }
+                        if (lo < ckoe && A[lo] == x) ++c;
+                    }
+                }
+                count += c;
+                continue;
+            }
             int32_t ap = A[p];
             const int32_t a_last = A[ckoe - 1];
-            scanned += (ckoe - p) + (cbe - cbb) + 2;
             unsigned long long c = 0;
             bool done = false;
 #pragma unroll
@@ -336,6 +370,96 @@ __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, in
     }
 }
 
+// |N+(a) tail ∩ N+(u)| for one pair: merge, or walk the shorter list and
+// binary-search the longer one when their lengths differ by > 16x.
+__device__ inline unsigned long long tc_intersect(const int32_t* __restrict__ adj, int32_t p,
+                                                  int32_t ae, int32_t bb, int32_t be) {
+    const int32_t la = ae - p, lb = be - bb;
+    if (la <= 0 || lb <= 0) return 0;
+    unsigned long long c = 0;
+    if (la > 16 * lb || lb > 16 * la) {
+        const int32_t s0 = la <= lb ? p : bb, s1 = la <= lb ? ae : be;
+        int32_t lo = la <= lb ? bb : p;
+        const int32_t hi0 = la <= lb ? be : ae;
+        for (int32_t i = s0; i < s1 && lo < hi0; ++i) {
+            const int32_t x = adj[i];
+            int32_t hi = hi0;
+            while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (adj[mid] < x) lo = mid + 1; else hi = mid;
+            }
+            if (lo < hi0 && adj[lo] == x) ++c;
+        }
+        return c;
+    }
+    int32_t x = adj[p], y = adj[bb];
+    while (true) {
+        if (x < y) {
+            if (++p >= ae) break;
+            x = adj[p];
+        } else if (y < x) {
+            if (++bb >= be) break;
+            y = adj[bb];
+        } else {
+            ++c;
+            if (++p >= ae || ++bb >= be) break;
+            x = adj[p];
+            y = adj[bb];
+        }
+    }
+    return c;
+}
+
+// Degree binning: vertices with more than kTcHeavy oriented neighbours.
+__global__ void k_tc_heavy_list(int32_t v_begin, int32_t v_end, const int32_t* __restrict__ off_plus,
+                                int32_t* heavy, int32_t* cnt) {
+    for (int64_t v = v_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < v_end;
+         v += (int64_t)gridDim.x * blockDim.x)
+        if (off_plus[v + 1] - off_plus[v] > kTcHeavy) heavy[atomicAdd(cnt, 1)] = int32_t(v);
+}
+
+__global__ void k_tc_heavy_sizes(int32_t nh, const int32_t* __restrict__ heavy,
+                                 const int32_t* __restrict__ off_plus, long long* sizes) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += gridDim.x * blockDim.x) {
+        const int32_t v = heavy[h];
+        sizes[h] = max(off_plus[v + 1] - off_plus[v] - 1, 0);
+    }
+}
+
+// The heavy vertices' pairs (v, i), i < |N+(v)| - 1, one per thread over the
+// whole grid (pre[h] = first pair of heavy vertex h).
+__global__ void __launch_bounds__(256) k_tc_heavy(int32_t nh, const int32_t* __restrict__ heavy,
+                                                  const long long* __restrict__ pre,
+                                                  const int32_t* __restrict__ off_plus,
+                                                  const int32_t* __restrict__ adj,
+                                                  unsigned long long* acc) {
+    unsigned long long count = 0, scanned = 0;
+    const long long total = pre[nh];
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total;
+         j += (long long)gridDim.x * blockDim.x) {
+        int32_t lo = 0, hi = nh;  // last h with pre[h] <= j
+        while (hi - lo > 1) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= j) lo = mid; else hi = mid;
+        }
+        const int32_t v = heavy[lo];
+        const int32_t ob = off_plus[v], oe = off_plus[v + 1];
+        const int32_t pu = ob + int32_t(j - pre[lo]);
+        const int32_t u = adj[pu];
+        const int32_t bb = off_plus[u], be = off_plus[u + 1];
+        scanned += (oe - pu - 1) + (be - bb) + 2;
+        count += tc_intersect(adj, pu + 1, oe, bb, be);
+    }
+    for (int o = 16; o; o >>= 1) {
+        count += __shfl_xor_sync(0xffffffffu, count, o);
+        scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (count) atomicAdd(&acc[0], count);
+        if (scanned) atomicAdd(&acc[1], scanned);
+    }
+}
+
 static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_stats* stats) {
     cudaStream_t s = g->stream;
     auto& P = *g->tc;
@@ -370,7 +494,42 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
                                                     P.adj_plus.get(), P.acc.get());
         });
     }
-    if (stats) stats->launches = 2 + (v_end > v_begin);
+    // degree binning: the heavy vertices' pairs over the whole grid
+    int heavy_launches = 0;
+    if (v_end > v_begin) {
+        P.heavy.ensure(size_t(v_end - v_begin) + 1);
+        P.heavy_cnt.ensure(1);
+        GDX_CUDA(cudaMemsetAsync(P.heavy_cnt.get(), 0, 4, s));
+        k_tc_heavy_list<<<blocks_for(v_end - v_begin, 256, g->num_sms * 8), 256, 0, s>>>(
+            v_begin, v_end, P.off_plus.get(), P.heavy.get(), P.heavy_cnt.get());
+        GDX_LAUNCH_CHECK();
+        int32_t nh = 0;
+        GDX_CUDA(cudaMemcpyAsync(&nh, P.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        if (nh > 0) {
+            P.heavy_pre.ensure(size_t(nh) + 1);
+            k_tc_heavy_sizes<<<blocks_for(nh, 256, 1024), 256, 0, s>>>(
+                nh, P.heavy.get(), P.off_plus.get(), P.heavy_pre.get() + 1);
+            GDX_LAUNCH_CHECK();
+            GDX_CUDA(cudaMemsetAsync(P.heavy_pre.get(), 0, 8, s));
+            size_t tb = 0;
+            GDX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, P.heavy_pre.get() + 1,
+                                                   P.heavy_pre.get() + 1, nh, s));
+            P.scan_tmp.ensure(tb);
+            GDX_CUDA(cub::DeviceScan::InclusiveSum(P.scan_tmp.get(), tb, P.heavy_pre.get() + 1,
+                                                   P.heavy_pre.get() + 1, nh, s));
+            std::vector<long long> pre(size_t(nh) + 1, 0);
+            GDX_CUDA(cudaMemcpyAsync(&pre[nh], P.heavy_pre.get() + nh, 8, cudaMemcpyDeviceToHost, s));
+            GDX_CUDA(cudaStreamSynchronize(s));
+            const int grid = blocks_for(pre[nh], 256, g->num_sms * 16);
+            timed_launch(g, "tc_heavy", [&] {
+                k_tc_heavy<<<grid, 256, 0, s>>>(nh, P.heavy.get(), P.heavy_pre.get(),
+                                                P.off_plus.get(), P.adj_plus.get(), P.acc.get());
+            });
+            heavy_launches = 1;
+        }
+    }
+    if (stats) stats->launches = 2 + (v_end > v_begin) + heavy_launches;
 }
 
 static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_out,

@@ -408,3 +408,22 @@ def test_sharded_pr_sssp_device(gdx, world):
     assert rel_err(r2, er) < 1e-12 and rel_err(r3, er) < 1e-12
     assert np.array_equal(d, ed)
     assert rel_err(bc, ebc) < 1e-9 and tc == etc_
+
+
+def test_tc_hub_degree_binning(gdx, port):
+    """A hub whose oriented list exceeds the light-path bound (|N+| > 256) goes
+    through the degree-binned k_tc_heavy; lists of very unequal length take
+    the galloping intersection."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    u = np.concatenate([np.zeros(n - 1, np.int32), rng.integers(1, n, 20000).astype(np.int32)])
+    v = np.concatenate([np.arange(1, n, dtype=np.int32), rng.integers(1, n, 20000).astype(np.int32)])
+    for directed in (False, True):
+        g = port.build_from_edges(n, u, v, None, directed)
+        dg = gdx.DeviceGraph.from_csr(g)
+        st = {}
+        assert dg.tc(stats=st) == port.tc(g), directed
+        if not directed:
+            assert st["launches"] == 4  # orientation x2, light pairs, heavy pairs
+            assert dg.tc_range(0, 1) + dg.tc_range(1, n) == port.tc(g)
+            assert dg.tc_range(0, 1) == port.tc_range(g, 0, 1)
