@@ -24,6 +24,9 @@
 namespace gdx {
 
 constexpr int kTcBlock = 256;
+// degree binning: a vertex with more (oriented) neighbours than this has its
+// pairs spread over the whole grid (k_tc_heavy / k_tc_heavy_mid)
+constexpr int kTcHeavy = 256;
 
 // first index in [lo, hi) with a[i] > x
 __device__ inline int32_t upper_bound_dev(const int32_t* __restrict__ a, int32_t lo, int32_t hi,
@@ -105,8 +108,8 @@ __global__ void __launch_bounds__(kTcBlock) k_tc(int32_t v_begin, int32_t v_end,
         const bool valid = v < v_end;
         const int32_t vb = valid ? offsets[v] : 0;
         const int32_t ve = valid ? offsets[v + 1] : 0;
-        const int32_t len = ve - vb;
-        const int32_t hs = valid ? upper_bound_dev(dests, vb, ve, v) : 0;  // first w > v
+        const int32_t len = ve - vb > kTcHeavy ? 0 : ve - vb;  // heavy: k_tc_heavy_mid
+        const int32_t hs = valid && len ? upper_bound_dev(dests, vb, ve, v) : 0;  // first w > v
         int incl = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -210,7 +213,6 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
     }
 }
 
-constexpr int kTcHeavy = 256;  // |N+(v)| above which a vertex's pairs are binned to k_tc_heavy
 constexpr int kTcStage = 512;  // ints of staged N+ lists per warp
 
 __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, int32_t v_end,
@@ -419,11 +421,80 @@ __global__ void k_tc_heavy_list(int32_t v_begin, int32_t v_end, const int32_t* _
 }
 
 __global__ void k_tc_heavy_sizes(int32_t nh, const int32_t* __restrict__ heavy,
-                                 const int32_t* __restrict__ off_plus, long long* sizes) {
+                                 const int32_t* __restrict__ off, int32_t drop, long long* sizes) {
     for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += gridDim.x * blockDim.x) {
         const int32_t v = heavy[h];
-        sizes[h] = max(off_plus[v + 1] - off_plus[v] - 1, 0);
+        sizes[h] = max(off[v + 1] - off[v] - drop, 0);
     }
+}
+
+// Directed graphs (tc.sp's middle vertex): the edges (v, u), u < v, of the
+// heavy middle vertices, one per thread over the whole grid.
+__global__ void __launch_bounds__(256) k_tc_heavy_mid(int32_t nh, const int32_t* __restrict__ heavy,
+                                                      const long long* __restrict__ pre,
+                                                      const int32_t* __restrict__ offsets,
+                                                      const int32_t* __restrict__ dests,
+                                                      unsigned long long* acc) {
+    unsigned long long count = 0, scanned = 0;
+    const long long total = pre[nh];
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total;
+         j += (long long)gridDim.x * blockDim.x) {
+        int32_t lo = 0, hi = nh;  // last h with pre[h] <= j
+        while (hi - lo > 1) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= j) lo = mid; else hi = mid;
+        }
+        const int32_t v = heavy[lo];
+        const int32_t vb = offsets[v], ve = offsets[v + 1];
+        const int32_t u = dests[vb + int32_t(j - pre[lo])];
+        if (u >= v) continue;
+        const int32_t hs = upper_bound_dev(dests, vb, ve, v);  // N(v) ∩ (v, inf)
+        const int32_t ub = offsets[u], ue = offsets[u + 1];
+        const int32_t bs = upper_bound_dev(dests, ub, ue, v);  // N(u) ∩ (v, inf)
+        scanned += (ve - hs) + (ue - bs);
+        count += tc_intersect(dests, hs, ve, bs, ue);
+    }
+    for (int o = 16; o; o >>= 1) {
+        count += __shfl_xor_sync(0xffffffffu, count, o);
+        scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (count) atomicAdd(&acc[0], count);
+        if (scanned) atomicAdd(&acc[1], scanned);
+    }
+}
+
+// Lists the vertices of [v_begin, v_end) with more than kTcHeavy entries in
+// `off` and the prefix of their pair counts (deg - drop); returns their count.
+static int32_t tc_heavy_plan(gdx_graph* g, TcPlan& P, int32_t v_begin, int32_t v_end,
+                             const int32_t* off, int32_t drop, long long* total_pairs) {
+    cudaStream_t s = g->stream;
+    *total_pairs = 0;
+    if (v_end <= v_begin) return 0;
+    P.heavy.ensure(size_t(v_end - v_begin) + 1);
+    P.heavy_cnt.ensure(1);
+    GDX_CUDA(cudaMemsetAsync(P.heavy_cnt.get(), 0, 4, s));
+    k_tc_heavy_list<<<blocks_for(v_end - v_begin, 256, g->num_sms * 8), 256, 0, s>>>(
+        v_begin, v_end, off, P.heavy.get(), P.heavy_cnt.get());
+    GDX_LAUNCH_CHECK();
+    int32_t nh = 0;
+    GDX_CUDA(cudaMemcpyAsync(&nh, P.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    if (nh == 0) return 0;
+    P.heavy_pre.ensure(size_t(nh) + 1);
+    k_tc_heavy_sizes<<<blocks_for(nh, 256, 1024), 256, 0, s>>>(nh, P.heavy.get(), off, drop,
+                                                              P.heavy_pre.get() + 1);
+    GDX_LAUNCH_CHECK();
+    GDX_CUDA(cudaMemsetAsync(P.heavy_pre.get(), 0, 8, s));
+    size_t tb = 0;
+    GDX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, P.heavy_pre.get() + 1,
+                                           P.heavy_pre.get() + 1, nh, s));
+    P.scan_tmp.ensure(tb);
+    GDX_CUDA(cub::DeviceScan::InclusiveSum(P.scan_tmp.get(), tb, P.heavy_pre.get() + 1,
+                                           P.heavy_pre.get() + 1, nh, s));
+    GDX_CUDA(cudaMemcpyAsync(total_pairs, P.heavy_pre.get() + nh, 8, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    return nh;
 }
 
 // The heavy vertices' pairs (v, i), i < |N+(v)| - 1, one per thread over the
@@ -496,38 +567,15 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
     }
     // degree binning: the heavy vertices' pairs over the whole grid
     int heavy_launches = 0;
-    if (v_end > v_begin) {
-        P.heavy.ensure(size_t(v_end - v_begin) + 1);
-        P.heavy_cnt.ensure(1);
-        GDX_CUDA(cudaMemsetAsync(P.heavy_cnt.get(), 0, 4, s));
-        k_tc_heavy_list<<<blocks_for(v_end - v_begin, 256, g->num_sms * 8), 256, 0, s>>>(
-            v_begin, v_end, P.off_plus.get(), P.heavy.get(), P.heavy_cnt.get());
-        GDX_LAUNCH_CHECK();
-        int32_t nh = 0;
-        GDX_CUDA(cudaMemcpyAsync(&nh, P.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, s));
-        GDX_CUDA(cudaStreamSynchronize(s));
-        if (nh > 0) {
-            P.heavy_pre.ensure(size_t(nh) + 1);
-            k_tc_heavy_sizes<<<blocks_for(nh, 256, 1024), 256, 0, s>>>(
-                nh, P.heavy.get(), P.off_plus.get(), P.heavy_pre.get() + 1);
-            GDX_LAUNCH_CHECK();
-            GDX_CUDA(cudaMemsetAsync(P.heavy_pre.get(), 0, 8, s));
-            size_t tb = 0;
-            GDX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, P.heavy_pre.get() + 1,
-                                                   P.heavy_pre.get() + 1, nh, s));
-            P.scan_tmp.ensure(tb);
-            GDX_CUDA(cub::DeviceScan::InclusiveSum(P.scan_tmp.get(), tb, P.heavy_pre.get() + 1,
-                                                   P.heavy_pre.get() + 1, nh, s));
-            std::vector<long long> pre(size_t(nh) + 1, 0);
-            GDX_CUDA(cudaMemcpyAsync(&pre[nh], P.heavy_pre.get() + nh, 8, cudaMemcpyDeviceToHost, s));
-            GDX_CUDA(cudaStreamSynchronize(s));
-            const int grid = blocks_for(pre[nh], 256, g->num_sms * 16);
-            timed_launch(g, "tc_heavy", [&] {
-                k_tc_heavy<<<grid, 256, 0, s>>>(nh, P.heavy.get(), P.heavy_pre.get(),
-                                                P.off_plus.get(), P.adj_plus.get(), P.acc.get());
-            });
-            heavy_launches = 1;
-        }
+    long long pairs = 0;
+    const int32_t nh = tc_heavy_plan(g, P, v_begin, v_end, P.off_plus.get(), 1, &pairs);
+    if (nh > 0 && pairs > 0) {
+        const int grid = blocks_for(pairs, 256, g->num_sms * 16);
+        timed_launch(g, "tc_heavy", [&] {
+            k_tc_heavy<<<grid, 256, 0, s>>>(nh, P.heavy.get(), P.heavy_pre.get(), P.off_plus.get(),
+                                            P.adj_plus.get(), P.acc.get());
+        });
+        heavy_launches = 1;
     }
     if (stats) stats->launches = 2 + (v_end > v_begin) + heavy_launches;
 }
@@ -554,6 +602,14 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
             k_tc<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, g->offsets.get(), g->dests.get(),
                                            P.acc.get());
         });
+        long long pairs = 0;
+        const int32_t nh = tc_heavy_plan(g, P, v_begin, v_end, g->offsets.get(), 0, &pairs);
+        if (nh > 0 && pairs > 0)
+            timed_launch(g, "tc_heavy", [&] {
+                k_tc_heavy_mid<<<blocks_for(pairs, 256, g->num_sms * 16), 256, 0, s>>>(
+                    nh, P.heavy.get(), P.heavy_pre.get(), g->offsets.get(), g->dests.get(),
+                    P.acc.get());
+            });
     }
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     GDX_CUDA(cudaMemcpyAsync(h, P.acc.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
