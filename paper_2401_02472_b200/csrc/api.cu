@@ -130,6 +130,34 @@ size_t pool_trim() {
     return n;
 }
 
+__global__ void k_max_degree(int32_t n, const int32_t* __restrict__ off, int32_t* out) {
+    int32_t m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, off[v + 1] - off[v]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+int32_t graph_max_degree(gdx_graph* g) {
+    if (g->max_degree >= 0) return g->max_degree;
+    int32_t best = 0;
+    for (const int32_t* off : {g->offsets.get(), g->directed ? g->rev_offsets.get() : nullptr}) {
+        if (!off || g->n == 0) continue;
+        DevBuf<int32_t> d(1);
+        GDX_CUDA(cudaMemsetAsync(d.get(), 0, 4, g->stream));
+        k_max_degree<<<blocks_for(g->n, 256, g->num_sms * 4), 256, 0, g->stream>>>(g->n, off,
+                                                                                  d.get());
+        GDX_LAUNCH_CHECK();
+        int32_t h = 0;
+        GDX_CUDA(cudaMemcpyAsync(&h, d.get(), 4, cudaMemcpyDeviceToHost, g->stream));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        best = std::max(best, h);
+    }
+    g->max_degree = best;
+    return best;
+}
+
 int guard_impl(const std::function<void()>& f) {
     try {
         f();

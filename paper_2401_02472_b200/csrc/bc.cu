@@ -705,27 +705,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     }
 }
 
-__global__ void k_max_degree(int32_t n, const int32_t* __restrict__ off, int32_t* out) {
-    int32_t m = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
-        m = max(m, off[v + 1] - off[v]);
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
-}
-
-static int32_t max_degree(gdx_graph* g, const int32_t* off) {
-    if (!off || g->n == 0) return 0;
-    DevBuf<int32_t> d(1);
-    GDX_CUDA(cudaMemsetAsync(d.get(), 0, 4, g->stream));
-    k_max_degree<<<blocks_for(g->n, 256, g->num_sms * 4), 256, 0, g->stream>>>(g->n, off, d.get());
-    GDX_LAUNCH_CHECK();
-    int32_t h = 0;
-    GDX_CUDA(cudaMemcpyAsync(&h, d.get(), 4, cudaMemcpyDeviceToHost, g->stream));
-    GDX_CUDA(cudaStreamSynchronize(g->stream));
-    return h;
-}
-
 static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
                        unsigned long long* totals, int& launches, int& max_levels) {
     auto& W = *g->bc;
@@ -770,10 +749,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.in_srcs = g->rev_srcs.get();
     a.sources = W.sources.get();
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
-    if (W.max_deg < 0)
-        W.max_deg = std::max(max_degree(g, g->offsets.get()),
-                             g->directed ? max_degree(g, g->rev_offsets.get()) : 0);
-    a.any_heavy = W.max_deg > kHeavy;
+    a.any_heavy = graph_max_degree(g) > kHeavy;
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
@@ -843,11 +819,9 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         // grid-wide kernels otherwise (few sources on skewed graphs, whose
         // wide levels want every SM).  GDX_BC_MODE=grid|cta overrides.
         const char* mode = std::getenv("GDX_BC_MODE");
-        if (W.max_deg < 0 && nsrc > 0)
-            W.max_deg = std::max(max_degree(g, g->offsets.get()),
-                                 g->directed ? max_degree(g, g->rev_offsets.get()) : 0);
         const bool cta_mode = mode ? std::string(mode) == "cta"
-                                   : nsrc >= std::max(16, g->num_sms / 4) || W.max_deg <= kHeavy;
+                                   : nsrc >= std::max(16, g->num_sms / 4) ||
+                                         (nsrc > 0 && graph_max_degree(g) <= kHeavy);
         if (nsrc > 0 && cta_mode) {
             run_bc_cta(g, hsrc, totals, launches, max_levels);
         } else if (nsrc > 0) {

@@ -159,6 +159,7 @@ struct gdx_graph {
     bool directed = true;
     bool weighted = false;     // false => every weight is 1
     int32_t max_weight = 1;
+    int32_t max_degree = -1;   // max out- (and, directed, in-) degree; lazily computed
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -208,6 +209,10 @@ inline int blocks_for(int64_t items, int threads, int cap) {
     if (b < 1) b = 1;
     return static_cast<int>(b < cap ? b : cap);
 }
+
+// Max out-degree (and in-degree for directed graphs), computed once per handle
+// (api.cu); the kernels pick hub-aware or latency-oriented variants from it.
+int32_t graph_max_degree(gdx_graph* g);
 
 // Builds the reverse CSR (csr.cpp:77-94 semantics) on the device.
 void build_reverse_device(gdx_graph* g);

@@ -116,7 +116,6 @@ struct BcWork {
     int block = 0;
     // CTA-per-source mode (k_bc_cta): one state slot per CTA
     int32_t cta_grid = 0;
-    int32_t max_deg = -1;       // max out- (and in-) degree, computed once per handle
     DevBuf<double> cta_rec;     // [cta_grid][n] x 32 B (level, sigma exp, mantissa, delta)
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]

@@ -745,11 +745,15 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         // rounds (bandwidth-bound), small ones the persistent kernel
         // (latency-bound); GDX_SSSP_MODE=scan|persistent overrides.
         // Default: frontier-scan rounds driven on the device by a CUDA graph
-        // with a conditional WHILE node (C1: 0.37 ms vs 0.44 ms for the
+        // with a conditional WHILE node (C1: 0.36 ms vs 0.44 ms for the
         // persistent kernel and 0.56 ms with a host round trip per round).
         // GDX_SSSP_MODE=persistent|scan|graph selects one for A/B runs.
+        // Low-degree graphs (max degree <= 64: road-like, high diameter, thousands
+        // of small rounds) take the persistent kernel instead: its queue touches
+        // only the frontier while a scan reads all n per round (2000^2 grid:
+        // 27 ms vs 76 ms).
         const char* mode = std::getenv("GDX_SSSP_MODE");
-        const std::string md = mode ? mode : "graph";
+        const std::string md = mode ? mode : graph_max_degree(g) <= 64 ? "persistent" : "graph";
         const bool graph = md == "graph";
         const bool scan = md == "scan" || graph;
         if (scan) {
