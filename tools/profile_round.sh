@@ -12,8 +12,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     --log-file $O/launches_pr.csv python bench.py --algos "" --steps 2 --warmup 3 \
     --no-cpu-baseline > $O/launches_bench.log 2>&1
 echo "launch list rc=$?"
-cap() {  # name algo kernel-regex skip
-    timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$3" -s "$4" -c 1 \
+cap() {  # name algo kernel-regex skip   (kernels inside a CUDA graph with conditional
+         # nodes cannot be profiled one by one: SSSP captures use the host-driven loop,
+         # GDX_SSSP_MODE=scan, which runs the same kernels)
+    GDX_SSSP_MODE=scan timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$3" -s "$4" -c 1 \
         -o $O/ncu_$1 -f python tools/kernel_driver.py --algo "$2" --reps 2 > $O/ncu_$1.log 2>&1
     echo "ncu $1 rc=$?"
 }
