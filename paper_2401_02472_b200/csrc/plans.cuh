@@ -14,16 +14,10 @@ gdx_graph* make_graph(int device);
 
 // PageRank merge-path plan (pagerank.cu).
 struct PrPlan {
-    int32_t ntiles = 0;
-    int32_t nslots = 0;
-    DevBuf<int2> tile_coord;              // ntiles+1 merge-path (row, edge) coordinates
-    DevBuf<int2> tile_slots;              // per tile: (first-row slot, carry slot), -1 = none
-    DevBuf<int32_t> slot_row;             // row of each spanning slot
-    DevBuf<double> slot_acc;              // partial sums per slot (zeroed after use)
     DevBuf<double> rank[2], contrib[2];
     DevBuf<double> dangling;              // 3 rotating accumulators
     DevBuf<int32_t> flags;                // per-round "unsettled" votes
-    // edge-aligned two-pass plan (variant 60)
+    // edge-aligned two-pass plan
     int32_t nnz = 0;
     DevBuf<int2> nz;                      // non-empty rows of the reverse CSR: (vertex, end)
     DevBuf<int2> grp;                     // per 8-edge group: (nz index of its first row, its end)
@@ -34,10 +28,7 @@ struct PrPlan {
     DevBuf<double> partials;              // shard: [dangling partial, unsettled]
     int32_t flags_cap = 0;
     int grid = 0;
-    int variant = 7;
-    int tile = 0;
     int block = 256;
-    size_t smem = 0;
 };
 
 // Peer-memory exchange state of the sharded PageRank (pagerank.cu gdx_pr_p2p_*).
