@@ -427,3 +427,27 @@ def test_tc_hub_degree_binning(gdx, port):
             assert st["launches"] == 4  # orientation x2, light pairs, heavy pairs
             assert dg.tc_range(0, 1) + dg.tc_range(1, n) == port.tc(g)
             assert dg.tc_range(0, 1) == port.tc_range(g, 0, 1)
+
+
+def test_memory_pool_reuse_and_trim(gdx, port):
+    """Destroyed graphs' device buffers are reused by the next graph of the same
+    shape (no new cudaMalloc: free memory stays flat) and gdx_pool_trim hands
+    them back to the driver."""
+    import ctypes as C
+    torch = pytest.importorskip("torch")
+    from paper_2401_02472_b200 import _lib
+    u, v = port.gen_rmat_edges(1 << 14, 1 << 17, 3)
+    g = port.build_from_edges(1 << 14, u, v, None, True)
+    exp, it = port.pr(g, 0.85, 1e-9, 110)
+    free = []
+    for _ in range(4):
+        dg = gdx.DeviceGraph.from_csr(g)
+        got, rounds = dg.pagerank(0.85, 1e-9, 110)
+        assert rounds == it and rel_err(got, exp) < 1e-12
+        dg.close()
+        free.append(torch.cuda.mem_get_info()[0])
+    assert max(free[1:]) - min(free[1:]) < (4 << 20)  # steady state: blocks reused
+    released = C.c_int64(0)
+    _lib.check(_lib.load().gdx_pool_trim(C.byref(released)))
+    assert released.value > 0
+    assert torch.cuda.mem_get_info()[0] >= free[-1]
