@@ -156,7 +156,31 @@ static void radix_sort_keys(cudaStream_t s, CubTemp& tmp, K* kin, K* kout, int64
 
 static int grid_for(gdx_graph* g, int64_t items) { return blocks_for(items, 256, g->num_sms * 16); }
 
-// Reverse CSR: sort (dest << b | src) with the forward edge id as payload.
+// Undirected graphs are stored symmetrically with sorted rows, so the reverse
+// CSR equals the forward one; rev_eid[e] (row v, entry u) is the forward id of
+// (u, v): offsets[u] + position of v in N(u).  One warp per row.
+__global__ void k_rev_eid_symmetric(int32_t n, const int32_t* __restrict__ offsets,
+                                    const int32_t* __restrict__ dests, int32_t* rev_eid) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        for (int32_t e = offsets[v] + lane; e < offsets[v + 1]; e += 32) {
+            const int32_t u = dests[e];
+            int32_t lo = offsets[u], hi = offsets[u + 1];
+            while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (dests[mid] < int32_t(v))
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            rev_eid[e] = lo;
+        }
+    }
+}
+
+// Reverse CSR: sort (dest << b | src) with the forward edge id as payload
+// (directed graphs); undirected graphs copy the forward arrays.
 void build_reverse_device(gdx_graph* g) {
     const int32_t n = g->n;
     const int64_t m = g->m;
@@ -169,6 +193,16 @@ void build_reverse_device(gdx_graph* g) {
         return;
     }
     if (!g->dests.get()) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no forward adjacency");
+    if (!g->directed) {
+        GDX_CUDA(cudaMemcpyAsync(g->rev_offsets.get(), g->offsets.get(), (size_t(n) + 1) * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+        GDX_CUDA(cudaMemcpyAsync(g->rev_srcs.get(), g->dests.get(), size_t(m) * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+        k_rev_eid_symmetric<<<grid_for(g, int64_t(n) * 32), 256, 0, s>>>(
+            n, g->offsets.get(), g->dests.get(), g->rev_eid.get());
+        GDX_LAUNCH_CHECK();
+        return;
+    }
     const int b = key_bits(n);
     DevBuf<uint64_t> k0(m), k1(m);
     DevBuf<int32_t> e0(m);
