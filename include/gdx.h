@@ -215,6 +215,13 @@ int gdx_pr_p2p_close(gdx_graph* g);
 int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end);
 int gdx_sssp_shard_frontier(gdx_graph* g, int64_t* dist, int64_t* prev, int64_t* count_out);
 int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist);
+/* The same rounds over int32 replicas (INF = INT32_MAX): half the gather and
+ * collective bytes.  out2 = {improved count, overflow}: overflow is 1 when a
+ * relaxation since the previous frontier call would have reached INT32_MAX;
+ * the caller then reruns with the int64 entry points (distributed.py
+ * sharded_sssp), so the result is exact either way. */
+int gdx_sssp_shard_frontier32(gdx_graph* g, int32_t* dist, int32_t* prev, int64_t* out2);
+int gdx_sssp_shard_relax32(gdx_graph* g, int32_t* dist);
 
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with

@@ -96,6 +96,8 @@ SIGNATURES = {
     "gdx_sssp_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32], C.c_int),
     "gdx_sssp_shard_frontier": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "gdx_sssp_shard_relax": ([C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_shard_frontier32": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_shard_relax32": ([C.c_void_p, C.c_void_p], C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),

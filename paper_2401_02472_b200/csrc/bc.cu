@@ -24,6 +24,7 @@
 //     Where the reference's sigma is finite the quotients are identical.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "gdx_internal.cuh"
@@ -401,7 +402,19 @@ struct BcCtaArgs {
     int32_t* loff;     // [grid][n+2] level boundaries in log
     double* bc;
     unsigned long long* ctr;
+    unsigned long long* trace;  // optional: slot 0's (globaltimer ns, items) per level step
+    int32_t trace_cap;
 };
+
+__device__ inline void bc_trace(const BcCtaArgs& a, int64_t slot, int tid, int& k, int items) {
+    if (a.trace && slot == 0 && tid == 0 && k < a.trace_cap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[2 * k] = t;
+        a.trace[2 * k + 1] = (unsigned long long)(unsigned)items;
+    }
+    ++k;
+}
 
 __device__ inline void rec_level_sigma(const BcRec* r, int32_t& level, double2& sig) {
     const int4 q = *reinterpret_cast<const int4*>(r);
@@ -524,6 +537,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
     unsigned long long reached = 0, fscan = 0, bscan = 0, dag = 0, levels_max = 0;
+    int tk = 0;
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
         if (tid == 0) {
@@ -621,6 +635,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             // level L+2 (last read right after the previous barrier) is reset now
             cluster.sync();
             const int next = s_next[L % 3];
+            bc_trace(a, slot, tid, tk, end - beg);
             if (tid == 0) {
                 s_next[(L + 2) % 3] = 0;
                 loff[L + 1] = end;
@@ -684,6 +699,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 if (ltid == 0) s_hn = 0;
             }
             cluster.sync();
+            bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
         }
         // restore `level` for the slot's next source
         for (int i = tid; i < end; i += kStride) rec[log[i].x].level = -1;
@@ -754,6 +770,16 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
     a.ctr = W.ctrs.get();
+    // GDX_BC_TRACE=<file>: slot 0's per-level-step (ns since the previous step, items)
+    const char* trace = std::getenv("GDX_BC_TRACE");
+    a.trace = nullptr;
+    a.trace_cap = 1 << 16;
+    DevBuf<unsigned long long> tbuf;
+    if (trace) {
+        tbuf.alloc(size_t(2) * a.trace_cap);
+        GDX_CUDA(cudaMemsetAsync(tbuf.get(), 0, tbuf.bytes(), s));
+        a.trace = tbuf.get();
+    }
     if (g->directed && (!a.in_offsets || !a.in_srcs))
         fail(GDX_ERR_UNSUPPORTED, "Unsupported: directed BC needs the reverse CSR");
     timed_launch(g, "bc_cta", [&] {
@@ -782,6 +808,15 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     totals[kBwdScan] += h[kBwdScan];
     totals[kDag] += h[kDag];
     max_levels = std::max<int>(max_levels, int(h[kLevels]));
+    if (trace) {
+        std::vector<unsigned long long> t(size_t(2) * a.trace_cap);
+        GDX_CUDA(cudaMemcpy(t.data(), a.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(trace, "w")) {
+            for (int k = 1; k < a.trace_cap && t[2 * k]; ++k)
+                std::fprintf(f, "%llu %lld\n", t[2 * k] - t[2 * k - 2], (long long)int(t[2 * k + 1]));
+            std::fclose(f);
+        }
+    }
 }
 
 }  // namespace gdx

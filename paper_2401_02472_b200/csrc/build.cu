@@ -93,7 +93,7 @@ __global__ void k_low_bits(int64_t m, int b, const uint64_t* __restrict__ keys,
 __device__ inline int32_t edge_source(const int32_t* __restrict__ offsets, int32_t n, int64_t e) {
     int32_t lo = 0, hi = n - 1;
     while (lo < hi) {
-        int32_t mid = (lo + hi + 1) >> 1;
+        int32_t mid = lo + ((hi - lo + 1) >> 1);
         if (offsets[mid] <= e)
             lo = mid;
         else
@@ -168,7 +168,7 @@ __global__ void k_rev_eid_symmetric(int32_t n, const int32_t* __restrict__ offse
             const int32_t u = dests[e];
             int32_t lo = offsets[u], hi = offsets[u + 1];
             while (lo < hi) {
-                const int32_t mid = (lo + hi) >> 1;
+                const int32_t mid = lo + ((hi - lo) >> 1);
                 if (dests[mid] < int32_t(v))
                     lo = mid + 1;
                 else

@@ -314,7 +314,7 @@ __global__ void k_pr_grp_rows(int64_t ngroups, int64_t e_base, int64_t e_begin, 
         const int64_t e = max(e_base + g * kEdgeGroup, e_begin);
         int32_t lo = 0, hi = nnz;  // first k whose row ends after edge e
         while (lo < hi) {
-            const int32_t mid = (lo + hi) >> 1;
+            const int32_t mid = lo + ((hi - lo) >> 1);
             if (nz[mid].y <= e)
                 lo = mid + 1;
             else

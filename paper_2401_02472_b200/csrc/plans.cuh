@@ -68,6 +68,7 @@ struct SsspWork {
     // gdx_sssp_shard_*: this rank's vertex range and relaxation items
     bool shard_ready = false;
     int32_t shard_v0 = 0, shard_v1 = 0;
+    int64_t shard_edges = 0;
     DevBuf<int2> shard_queue;
     DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges]
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width

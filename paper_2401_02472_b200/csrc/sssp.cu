@@ -28,6 +28,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <limits>
 
 #include "gdx_internal.cuh"
 #include "plans.cuh"
@@ -360,6 +361,7 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
 // (dist < prev), into the local replica, and the caller merges the replicas
 // with an element-wise MIN all-reduce (distributed.py sharded_sssp).
 // ---------------------------------------------------------------------------
+constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-cooperatively
 constexpr int kShardChunk = 64;  // edges per relaxation item (C5: 23.7 ms vs 26.1 at 128, 25.6 at 32)
 
 // Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
@@ -378,25 +380,37 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
     __shared__ unsigned long long s_base;
     for (int64_t c0 = v0 + int64_t(blockIdx.x) * 256 * kPer; c0 < v1;
          c0 += int64_t(gridDim.x) * 256 * kPer) {
-        int items[kPer], first[kPer];
+        // all loads of the chunk are issued before any is consumed: the prev
+        // stores would otherwise order each vertex's loads after the previous
+        // vertex's (possible aliasing), one DRAM round trip per vertex
+        D dk[kPer], pk[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            dk[k] = v < v1 ? dist[v] : D(0);
+            pk[k] = v < v1 ? prev[v] : D(0);
+        }
+        int items[kPer], first[kPer], last[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            const bool f = dk[k] < pk[k];  // false past v1 (both 0)
+            first[k] = f ? offsets[v] : 0;
+            last[k] = f ? offsets[v + 1] : -1;
+        }
         int mine = 0, sinks = 0;
         unsigned long long vis = 0, edg = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
             items[k] = 0;
-            first[k] = 0;
-            if (v < v1) {
-                const D d = dist[v];
-                if (d < prev[v]) {
-                    prev[v] = d;
-                    const int32_t b = offsets[v], deg = offsets[v + 1] - b;
-                    first[k] = b;
-                    items[k] = (deg + kShardChunk - 1) / kShardChunk;
-                    sinks += deg == 0;
-                    ++vis;
-                    edg += deg;
-                }
+            if (last[k] >= 0) {
+                prev[v] = dk[k];
+                const int32_t deg = last[k] - first[k];
+                items[k] = (deg + kShardChunk - 1) / kShardChunk;
+                sinks += deg == 0;
+                ++vis;
+                edg += deg;
             }
             mine += items[k];
         }
@@ -432,10 +446,38 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int32_t v = int32_t(c0 + int64_t(k) * 256 + threadIdx.x);
-            for (int t = 0; t < items[k]; ++t) queue[pos++] = make_int2(v, first[k] + t * kShardChunk);
+            // a hub's items (a degree-10^6 vertex has ~10^4) are written by the
+            // whole warp, not serially by its own lane
+            const bool big = items[k] > kSplitItems;
+            if (!big)
+                for (int t = 0; t < items[k]; ++t) queue[pos + t] = make_int2(v, first[k] + t * kShardChunk);
+            unsigned hubs = __ballot_sync(full, big);
+            while (hubs) {
+                const int l = __ffs(hubs) - 1;
+                hubs &= hubs - 1;
+                const unsigned long long hb = __shfl_sync(full, pos, l);
+                const int hc = __shfl_sync(full, items[k], l);
+                const int32_t hv = __shfl_sync(full, v, l), hf = __shfl_sync(full, first[k], l);
+                for (int t = lane; t < hc; t += 32) queue[hb + t] = make_int2(hv, hf + t * kShardChunk);
+            }
+            pos += items[k];
         }
         __syncthreads();
     }
+}
+
+// Frontier-scan grid: one wave of resident blocks (a second partial wave
+// would double the chunk loop of the blocks in it); GDX_SSSP_FGRID = blocks
+// per SM overrides.
+template <class D>
+static int frontier_grid(const gdx_graph* g, int64_t cnt) {
+    static const int per_sm = [] {
+        if (const char* e = std::getenv("GDX_SSSP_FGRID")) return std::max(1, std::atoi(e));
+        int b = 0;
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sssp_scan_frontier<D>, 256, 0));
+        return std::max(1, b);
+    }();
+    return blocks_for(cnt, 256 * 8, g->num_sms * per_sm);
 }
 
 // Relaxation: one warp per item (<= kShardChunk out-edges of one vertex), lanes
@@ -465,7 +507,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
             u[k] = e < e1 ? dests[e] : -1;
             const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
             c[k] = dv + w;
-            if (sizeof(D) == 4 && u[k] >= 0 && dv > D(0xFFFFFFFEu) - w) {
+            if (sizeof(D) == 4 && u[k] >= 0 && dv > std::numeric_limits<D>::max() - D(1) - w) {
                 *ovf = 1;
                 u[k] = -1;
             }
@@ -522,7 +564,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
     GDX_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
     const int32_t n = g->n;
-    const int fgrid = blocks_for(n, 256 * 8, g->num_sms * 8);
+    const int fgrid = frontier_grid<D>(g, n);
     unsigned long long* ctr = w.shard_ctr.get();
     k_sssp_scan_frontier<D><<<fgrid, 256, 0, cs>>>(0, n, g->offsets.get(), dist, prev,
                                                    w.shard_queue.get(), ctr);
@@ -566,7 +608,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     unsigned long long vvis = 0, evis = 0;
     int rounds = 0, launches = 1;
-    const int fgrid = blocks_for(n, 256 * 8, g->num_sms * 8);
+    const int fgrid = frontier_grid<D>(g, n);
     const char* lv = std::getenv("GDX_SSSP_LPI");
     const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
     const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
@@ -669,55 +711,82 @@ extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end
         GDX_CUDA(cudaMemcpy(&eb[1], g->offsets.get() + v_end, 4, cudaMemcpyDeviceToHost));
         w.shard_v0 = v_begin;
         w.shard_v1 = v_end;
+        w.shard_edges = int64_t(eb[1]) - eb[0];
         w.shard_queue.ensure(size_t(v_end - v_begin) + size_t(eb[1] - eb[0]) / kShardChunk + 1);
         w.shard_ctr.ensure(5);
         w.shard_ready = true;
     });
 }
 
+// D = unsigned long long (int64 replicas, INF = INT64_MAX/2) or int (int32
+// replicas, INF = INT32_MAX; a relaxation that would reach INF raises the
+// overflow flag reported by the next frontier call).
+template <class D>
+static void shard_frontier(gdx_graph* g, D* dist, D* prev, int64_t* out, int nout) {
+    if (!g || !g->sssp || !g->sssp->shard_ready)
+        fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+    auto& w = *g->sssp;
+    const int32_t cnt = w.shard_v1 - w.shard_v0;
+    if (!out || (g->n > 0 && (!dist || !prev)))
+        fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+    DeviceGuard dg(g->device);
+    cudaStream_t s = g->stream;
+    // counters 0,1 (items, improved sinks) and 3,4 (stats) restart every round;
+    // 2 (overflow) accumulates over the relaxations since the previous call
+    GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get(), 0, 2 * sizeof(unsigned long long), s));
+    GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get() + 3, 0, 2 * sizeof(unsigned long long), s));
+    if (cnt > 0)
+        timed_launch(g, "sssp_shard_frontier", [&] {
+            k_sssp_scan_frontier<D><<<frontier_grid<D>(g, cnt), 256, 0, s>>>(
+                w.shard_v0, w.shard_v1, g->offsets.get(), dist, prev, w.shard_queue.get(),
+                w.shard_ctr.get());
+        });
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h, w.shard_ctr.get(), 3 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get() + 2, 0, sizeof(unsigned long long), s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    // out (device or host): queued items + improved sinks of this rank [, overflow]
+    const int64_t c[2] = {int64_t(h[0] + h[1]), int64_t(h[2] != 0)};
+    GDX_CUDA(cudaMemcpy(out, c, size_t(nout) * sizeof(int64_t), cudaMemcpyDefault));
+}
+
+template <class D>
+static void shard_relax(gdx_graph* g, D* dist) {
+    if (!g || !g->sssp || !g->sssp->shard_ready)
+        fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+    if (g->n > 0 && !dist) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+    DeviceGuard dg(g->device);
+    auto& w = *g->sssp;
+    cudaStream_t s = g->stream;
+    // the single-GPU rule (gdx_sssp): deeper grids for large relaxation sets
+    const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 64) * g->num_sms;
+    timed_launch(g, "sssp_shard_relax", [&] {
+        k_sssp_scan_relax<D, 16><<<blocks, 256, 0, s>>>(
+            w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
+            g->weighted ? g->weights.get() : nullptr, dist, w.shard_ctr.get() + 2);
+    });
+}
+
 extern "C" int gdx_sssp_shard_frontier(gdx_graph* g, int64_t* dist, int64_t* prev,
                                        int64_t* count_out) {
     return guard_impl([&] {
-        if (!g || !g->sssp || !g->sssp->shard_ready)
-            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
-        DeviceGuard dg(g->device);
-        auto& w = *g->sssp;
-        cudaStream_t s = g->stream;
-        GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get(), 0, 5 * sizeof(unsigned long long), s));
-        const int32_t cnt = w.shard_v1 - w.shard_v0;
-        if (cnt > 0)
-            timed_launch(g, "sssp_shard_frontier", [&] {
-                k_sssp_scan_frontier<unsigned long long>
-                    <<<blocks_for(cnt, 256 * 8, g->num_sms * 8), 256, 0, s>>>(
-                        w.shard_v0, w.shard_v1, g->offsets.get(),
-                        reinterpret_cast<const unsigned long long*>(dist),
-                        reinterpret_cast<unsigned long long*>(prev), w.shard_queue.get(),
-                        w.shard_ctr.get());
-            });
-        // count_out (device or host): queued items + improved sinks of this rank
-        unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
-        GDX_CUDA(cudaMemcpyAsync(h, w.shard_ctr.get(), 2 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-        GDX_CUDA(cudaStreamSynchronize(s));
-        const int64_t c = int64_t(h[0] + h[1]);
-        GDX_CUDA(cudaMemcpy(count_out, &c, sizeof(c), cudaMemcpyDefault));
+        shard_frontier(g, reinterpret_cast<unsigned long long*>(dist),
+                       reinterpret_cast<unsigned long long*>(prev), count_out, 1);
     });
 }
 
 extern "C" int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist) {
-    return guard_impl([&] {
-        if (!g || !g->sssp || !g->sssp->shard_ready)
-            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
-        DeviceGuard dg(g->device);
-        auto& w = *g->sssp;
-        cudaStream_t s = g->stream;
-        timed_launch(g, "sssp_shard_relax", [&] {
-            k_sssp_scan_relax<unsigned long long, 16><<<g->num_sms * 16, 256, 0, s>>>(
-                w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
-                g->weighted ? g->weights.get() : nullptr,
-                reinterpret_cast<unsigned long long*>(dist), w.shard_ctr.get() + 2);
-        });
-    });
+    return guard_impl([&] { shard_relax(g, reinterpret_cast<unsigned long long*>(dist)); });
+}
+
+extern "C" int gdx_sssp_shard_frontier32(gdx_graph* g, int32_t* dist, int32_t* prev,
+                                         int64_t* out2) {
+    return guard_impl([&] { shard_frontier(g, dist, prev, out2, 2); });
+}
+
+extern "C" int gdx_sssp_shard_relax32(gdx_graph* g, int32_t* dist) {
+    return guard_impl([&] { shard_relax(g, dist); });
 }
 
 extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {

@@ -32,7 +32,7 @@ constexpr int kTcHeavy = 256;
 __device__ inline int32_t upper_bound_dev(const int32_t* __restrict__ a, int32_t lo, int32_t hi,
                                           int32_t x) {
     while (lo < hi) {
-        int32_t mid = (lo + hi) >> 1;
+        int32_t mid = lo + ((hi - lo) >> 1);
         if (a[mid] <= x)
             lo = mid + 1;
         else
@@ -45,7 +45,7 @@ __device__ inline int32_t upper_bound_dev(const int32_t* __restrict__ a, int32_t
 __device__ inline int32_t lower_bound_dev(const int32_t* __restrict__ a, int32_t lo, int32_t hi,
                                           int32_t x) {
     while (lo < hi) {
-        int32_t mid = (lo + hi) >> 1;
+        int32_t mid = lo + ((hi - lo) >> 1);
         if (a[mid] < x)
             lo = mid + 1;
         else
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, in
                         const int32_t x = A[i];
                         int32_t hi = cbe;
                         while (lo < hi) {
-                            const int32_t mid = (lo + hi) >> 1;
+                            const int32_t mid = lo + ((hi - lo) >> 1);
                             if (adj[mid] < x) lo = mid + 1; else hi = mid;
                         }
                         if (lo < cbe && adj[lo] == x) ++c;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, in
                         const int32_t x = adj[i];
                         int32_t hi = ckoe;
                         while (lo < hi) {
-                            const int32_t mid = (lo + hi) >> 1;
+                            const int32_t mid = lo + ((hi - lo) >> 1);
                             if (A[mid] < x) lo = mid + 1; else hi = mid;
                         }
                         if (lo < ckoe && A[lo] == x) ++c;
@@ -387,7 +387,7 @@ __device__ inline unsigned long long tc_intersect(const int32_t* __restrict__ ad
             const int32_t x = adj[i];
             int32_t hi = hi0;
             while (lo < hi) {
-                const int32_t mid = (lo + hi) >> 1;
+                const int32_t mid = lo + ((hi - lo) >> 1);
                 if (adj[mid] < x) lo = mid + 1; else hi = mid;
             }
             if (lo < hi0 && adj[lo] == x) ++c;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) k_tc_heavy_mid(int32_t nh, const int32_t*
          j += (long long)gridDim.x * blockDim.x) {
         int32_t lo = 0, hi = nh;  // last h with pre[h] <= j
         while (hi - lo > 1) {
-            const int32_t mid = (lo + hi) >> 1;
+            const int32_t mid = lo + ((hi - lo) >> 1);
             if (pre[mid] <= j) lo = mid; else hi = mid;
         }
         const int32_t v = heavy[lo];
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(256) k_tc_heavy(int32_t nh, const int32_t* __r
          j += (long long)gridDim.x * blockDim.x) {
         int32_t lo = 0, hi = nh;  // last h with pre[h] <= j
         while (hi - lo > 1) {
-            const int32_t mid = (lo + hi) >> 1;
+            const int32_t mid = lo + ((hi - lo) >> 1);
             if (pre[mid] <= j) lo = mid; else hi = mid;
         }
         const int32_t v = heavy[lo];

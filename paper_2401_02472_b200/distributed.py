@@ -111,6 +111,10 @@ class Executor(Protocol):
 
     def sssp_relax(self, dist) -> None: ...
 
+    # optional int32 replicas (gdx_sssp_shard_*32): (count, overflow) per round
+    # def sssp_frontier32(self, dist, prev) -> tuple[int, int]: ...
+    # def sssp_relax32(self, dist) -> None: ...
+
 
 class DeviceExecutor:
     """Per-rank compute on this rank's GPU (libgdx.so)."""
@@ -190,6 +194,12 @@ class DeviceExecutor:
 
     def sssp_relax(self, dist):
         self._staged(self.g.sssp_shard_relax, dist)
+
+    def sssp_frontier32(self, dist, prev):
+        return self._staged(self.g.sssp_shard_frontier32, dist, prev)
+
+    def sssp_relax32(self, dist):
+        self._staged(self.g.sssp_shard_relax32, dist)
 
 
 # ---------------------------------------------------------------------------- sharded entry points
@@ -396,9 +406,18 @@ def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_i
     return (out.cpu().numpy() if to_host else out), rounds
 
 
-def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats=None):
+INF64 = (2**63 - 1) // 2
+INF32 = 2**31 - 1
+
+
+def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats=None,
+                 width: Optional[int] = None):
     """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact;
-    numpy, or the collective-device tensor when ``to_host`` is False."""
+    numpy, or the collective-device tensor when ``to_host`` is False.
+
+    Rounds run over int32 replicas when the executor has them (half the
+    gather and all-reduce bytes); if any rank's relaxation would reach
+    INT32_MAX the call reruns over int64 replicas (``width`` forces one)."""
     import torch
     from ._lib import GraphdslError
     dist = _dist()
@@ -409,20 +428,49 @@ def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats
         raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
     v0, v1 = _cached_ranges(ex, "sssp", world, lambda: _partition(ex, "sssp", world))[rank]
     ex.sssp_setup(v0, v1)
-    inf = (2**63 - 1) // 2
-    d = torch.full((n,), inf, dtype=torch.int64, device=dev)
-    prev = torch.full((n,), inf, dtype=torch.int64, device=dev)
+    d = None
+    if width != 64 and hasattr(ex, "sssp_frontier32"):
+        d32 = _sssp_rounds(ex, src, n, dev, torch.int32, group, stats)
+        if d32 is not None:
+            d = d32.to(torch.int64)
+            d[d32 == INF32] = INF64
+    elif width == 32:
+        raise GraphdslError("Unsupported", "Unsupported: executor has no int32 SSSP shard")
+    if d is None:
+        d = _sssp_rounds(ex, src, n, dev, torch.int64, group, stats)
+    return d.cpu().numpy() if to_host else d
+
+
+def _sssp_rounds(ex, src, n, dev, dtype, group, stats):
+    """fixedPoint rounds of sharded_sssp over `dtype` replicas; None when an
+    int32 relaxation overflowed on any rank."""
+    import torch
+    from ._lib import GraphdslError
+    dist = _dist()
+    wide = dtype == torch.int64
+    d = torch.full((n,), INF64 if wide else INF32, dtype=dtype, device=dev)
+    prev = d.clone()
     d[src] = 0
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     cap = 10 * n + 100
-    for _ in range(cap + 1):
-        cnt.fill_(ex.sssp_frontier(d, prev))
+    for r in range(cap + 1):
+        if wide:
+            cnt[0], cnt[1] = ex.sssp_frontier(d, prev), 0
+        else:
+            cnt[0], cnt[1] = ex.sssp_frontier32(d, prev)
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
-        if int(cnt.item()) == 0:
+        c, ovf = (int(x) for x in cnt.tolist())
+        if ovf:
+            return None
+        if c == 0:
             if stats is not None:
-                stats["rounds"] = _ + 1
-            return d.cpu().numpy() if to_host else d
-        ex.sssp_relax(d)
+                stats["rounds"] = r + 1
+                stats["width"] = 64 if wide else 32
+            return d
+        if wide:
+            ex.sssp_relax(d)
+        else:
+            ex.sssp_relax32(d)
         dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
     raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} iterations")
 

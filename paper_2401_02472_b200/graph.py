@@ -308,6 +308,15 @@ class DeviceGraph:
     def sssp_shard_relax(self, dist) -> None:
         check(_lib.load().gdx_sssp_shard_relax(self.handle, _ptr(dist)))
 
+    def sssp_shard_frontier32(self, dist, prev):
+        """int32 replicas (INF = INT32_MAX) -> (improved count, overflow flag)."""
+        c = np.zeros(2, np.int64)
+        check(_lib.load().gdx_sssp_shard_frontier32(self.handle, _ptr(dist), _ptr(prev), _ptr(c)))
+        return int(c[0]), int(c[1])
+
+    def sssp_shard_relax32(self, dist) -> None:
+        check(_lib.load().gdx_sssp_shard_relax32(self.handle, _ptr(dist)))
+
     # ---- measurement -----------------------------------------------------------
     def profile(self, enable: bool = True) -> None:
         check(_lib.load().gdx_profile_enable(self.handle, int(enable)))

@@ -105,6 +105,7 @@ class OracleExecutor:
     # --- SSSP shard: numpy restatement of gdx_sssp_shard_* ---
     def sssp_setup(self, v0, v1):
         self.s0, self.s1 = v0, v1
+        self.ovf = 0
 
     def sssp_frontier(self, dist, prev):
         d, p = dist.numpy(), prev.numpy()
@@ -120,6 +121,24 @@ class OracleExecutor:
         for v in self.front:
             e = slice(off[v], off[v + 1])
             np.minimum.at(d, dst[e], d[v] + w[e].astype(np.int64))
+
+    # int32 replicas (gdx_sssp_shard_*32): INF = INT32_MAX, a relaxation that
+    # would reach it raises the overflow flag reported by the next frontier call
+    def sssp_frontier32(self, dist, prev):
+        c = self.sssp_frontier(dist, prev)
+        o, self.ovf = self.ovf, 0
+        return c, o
+
+    def sssp_relax32(self, dist):
+        d = dist.numpy()
+        off, dst = self.g.offsets, self.g.dests
+        w = self.g.weights if self.g.weights is not None else np.ones(self.g.m, np.int32)
+        for v in self.front:
+            e = slice(off[v], off[v + 1])
+            c = int(d[v]) + w[e].astype(np.int64)
+            ok = c < D.INF32
+            self.ovf |= int(not ok.all())
+            np.minimum.at(d, dst[e][ok], c[ok].astype(np.int32))
 
 
 def _worker(rank, world, port, q):
@@ -174,11 +193,22 @@ def _worker_pr_sssp(rank, world, port, q):
     gd = p.build_from_edges(n, u, v, None, True)
     rank_v, rounds = D.sharded_pr(OracleExecutor(gd), 0.85, 1e-9, 110)
     gu = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1, 100, 9)
-    d0 = D.sharded_sssp(OracleExecutor(gu), 0)
-    d5 = D.sharded_sssp(OracleExecutor(gu), 5)
+    st0, st5, st64, stbig = {}, {}, {}, {}
+    d0 = D.sharded_sssp(OracleExecutor(gu), 0, stats=st0)
+    d5 = D.sharded_sssp(OracleExecutor(gu), 5, stats=st5)
+    d0w = D.sharded_sssp(OracleExecutor(gu), 0, width=64, stats=st64)
+    # weights near 2^30: int32 replicas overflow, the call reruns over int64
+    gb = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1 << 29, 1 << 30, 4)
+    db = D.sharded_sssp(OracleExecutor(gb), 0, stats=stbig)
     if rank == 0:
         exp_r, exp_rounds = p.pr(gd, 0.85, 1e-9, 110)
-        q.put((rank_v, rounds, exp_r, exp_rounds, d0, p.sssp(gu, 0), d5, p.sssp(gu, 5)))
+        e0 = p.sssp(gu, 0)
+        assert np.array_equal(d0w, e0) and st64["width"] == 64
+        assert st0["width"] == 32 and st5["width"] == 32
+        eb = p.sssp(gb, 0)
+        assert np.array_equal(db, eb) and stbig["width"] == 64
+        assert eb[eb < D.INF64].max() >= D.INF32  # the case really overflows int32
+        q.put((rank_v, rounds, exp_r, exp_rounds, d0, e0, d5, p.sssp(gu, 5)))
     dist.destroy_process_group()
 
 

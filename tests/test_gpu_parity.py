@@ -374,14 +374,20 @@ def _gpu_shard_worker(rank, world, port, q):
     r2, rounds2 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
     r3, rounds3 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
     exu = D.DeviceExecutor(G.DeviceGraph.from_csr(gu))
-    d = D.sharded_sssp(exu, 7)
+    st32, st64, stb = {}, {}, {}
+    d = D.sharded_sssp(exu, 7, stats=st32)  # int32 replicas
+    d64 = D.sharded_sssp(exu, 7, width=64, stats=st64)
+    # weights near 2^30: the int32 rounds overflow and the call reruns over int64
+    gb = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1 << 29, 1 << 30, 4)
+    db = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gb)), 0, stats=stb)
     srcs = [0, 5, 5, 99, 4000, 17, 2048]
     bc = D.sharded_bc(exu, srcs)
     tc = D.sharded_tc(exu)
     if rank == 0:
         er, erounds = p.pr(gd, 0.85, 1e-9, 110)
         q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3,
-               bc, p.bc(gu, srcs), tc, p.tc(gu)))
+               bc, p.bc(gu, srcs), tc, p.tc(gu),
+               (d64, st32["width"], st64["width"], db, p.sssp(gb, 0), stb["width"])))
     tdist.destroy_process_group()
 
 
@@ -399,7 +405,8 @@ def test_sharded_pr_sssp_device(gdx, world):
     procs = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3, bc, ebc, tc, etc_ = q.get(timeout=500)
+    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3, bc, ebc, tc, etc_, wide = \
+        q.get(timeout=500)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
@@ -407,6 +414,9 @@ def test_sharded_pr_sssp_device(gdx, world):
     assert rel_err(r, er) < 1e-12
     assert rel_err(r2, er) < 1e-12 and rel_err(r3, er) < 1e-12
     assert np.array_equal(d, ed)
+    d64, w32, w64, db, edb, wb = wide
+    assert np.array_equal(d64, ed) and (w32, w64) == (32, 64)
+    assert np.array_equal(db, edb) and wb == 64 and edb[edb < (2**63 - 1) // 2].max() >= 2**31 - 1
     assert rel_err(bc, ebc) < 1e-9 and tc == etc_
 
 
@@ -451,3 +461,26 @@ def test_memory_pool_reuse_and_trim(gdx, port):
     _lib.check(_lib.load().gdx_pool_trim(C.byref(released)))
     assert released.value > 0
     assert torch.cuda.mem_get_info()[0] >= free[-1]
+
+
+@pytest.mark.timeout(300)
+def test_reverse_ids_past_2e9_edges(gdx):
+    """RMAT-26 undirected (2.1e9 stored edges, offsets near INT32_MAX): the
+    mirror ids of the undirected reverse CSR, checked on 2^24 sampled edges
+    weighted towards the top of the edge range, where a midpoint (lo + hi) / 2
+    would overflow int32."""
+    import torch
+    dg = gdx.DeviceGraph.generate("rmat", 1 << 26, 1 << 30, seed=1, directed=False)
+    assert dg.m > (1 << 30) + (1 << 29)
+    off, dst, rsrc, reid = dg.device_arrays(["offsets", "dests", "rev_srcs", "rev_eid"])
+    dg.close()
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    k = 1 << 24
+    e = torch.cat([torch.randint(0, dg.m, (k // 2,), device="cuda", generator=gen),
+                   torch.randint(dg.m - (1 << 28), dg.m, (k // 2,), device="cuda", generator=gen)])
+    row = torch.searchsorted(off.long(), e, right=True) - 1
+    u = dst[e].long()
+    r = reid[e].long()
+    assert bool(torch.all(rsrc[e] == dst[e]))
+    assert bool(torch.all((off.long()[u] <= r) & (r < off.long()[u + 1])))
+    assert bool(torch.all(dst[r].long() == row))
