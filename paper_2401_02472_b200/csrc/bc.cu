@@ -704,6 +704,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // restore `level` for the slot's next source
         for (int i = tid; i < end; i += kStride) rec[log[i].x].level = -1;
         cluster.sync();
+        bc_trace(a, slot, tid, tk, 1 << 30);  // restore step
     }
     for (int o = 16; o; o >>= 1) {
         fscan += __shfl_xor_sync(0xffffffffu, fscan, o);

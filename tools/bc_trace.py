@@ -19,9 +19,11 @@ import paper_2401_02472_b200 as gdx  # noqa: E402
 
 def summarise(path):
     t = np.loadtxt(path, dtype=np.float64, ndmin=2)
+    rest = t[t[:, 1] == 1 << 30]
+    t = t[t[:, 1] != 1 << 30]
     fwd, bwd = t[t[:, 1] >= 0], t[t[:, 1] < 0] * [1, -1]
-    out = {}
-    for name, x in (("fwd", fwd), ("bwd", bwd)):
+    out = {"restore_us": (rest[:, 0] / 1e3).round(1).tolist()}
+    for name, x in (("fwd", fwd), ("bwd", bwd)):  # noqa: B007
         if len(x) == 0:
             continue
         ns, items = x[:, 0], x[:, 1]
