@@ -114,6 +114,12 @@ void pinned_free(void* p) {
     pinned_free_list().push_back(p);
 }
 
+size_t pool_cached() {
+    auto& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    return P.cached;
+}
+
 size_t pool_trim() {
     auto& P = pool();
     std::lock_guard<std::mutex> lk(P.mu);

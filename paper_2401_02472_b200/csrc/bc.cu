@@ -736,7 +736,21 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     else
         while (CS < 4 && int64_t(2 * CS) * std::min<int32_t>(nsrc, g->num_sms) <= g->num_sms) CS *= 2;
     if (CS != 1 && CS != 2 && CS != 4) CS = 1;
-    const int slots = std::max(1, std::min<int32_t>(nsrc, g->num_sms / CS));
+    int slots = std::max(1, std::min<int32_t>(nsrc, g->num_sms / CS));
+    // a slot holds 52 B per vertex (record, log entry, level bound): fewer
+    // slots (each then runs several sources) when they would not fit
+    {
+        size_t free_b = 0, tot_b = 0;
+        GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+        const size_t per_slot = size_t(n) * 52 + 8;
+        const size_t held =
+            W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() + pool_cached();
+        const int64_t fit = int64_t(double(free_b + held) * 0.85 / double(per_slot));
+        if (fit < 1)
+            fail(GDX_ERR_OUT_OF_MEMORY, "OutOfMemory: BC needs " + std::to_string(per_slot) +
+                                            " bytes of device memory per source slot");
+        slots = int(std::min<int64_t>(slots, fit));
+    }
     const int grid = slots * CS;
     if (W.cta_grid < slots) {
         W.level.release();

@@ -56,6 +56,7 @@ struct DeviceGuard {
 void* pool_alloc(size_t bytes, size_t* got);
 void pool_free(void* p, size_t bytes);
 size_t pool_trim();
+size_t pool_cached();  // bytes held free by the pool (all devices)
 void* pinned_alloc();
 void pinned_free(void* p);
 
