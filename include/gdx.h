@@ -222,6 +222,16 @@ int gdx_sssp_shard_relax(gdx_graph* g, int64_t* dist);
  * sharded_sssp), so the result is exact either way. */
 int gdx_sssp_shard_frontier32(gdx_graph* g, int32_t* dist, int32_t* prev, int64_t* out2);
 int gdx_sssp_shard_relax32(gdx_graph* g, int32_t* dist);
+/* Delta exchange: the int32 relaxation that also lists, once,
+ * every vertex whose replica distance it lowered -- changed_ids / changed_dist
+ * (device, capacity n) receive the ids and their values after the round,
+ * *count_out (host or device) their number.  The caller all-gathers the lists
+ * and applies every rank's pairs with gdx_sssp_shard_apply32 (element-wise MIN;
+ * ids < 0 are padding) instead of MIN-all-reducing the whole replica. */
+int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t* changed_ids,
+                                 int32_t* changed_dist, int64_t* count_out);
+int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t* ids, const int32_t* vals,
+                           int64_t count);
 
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with

@@ -98,6 +98,8 @@ SIGNATURES = {
     "gdx_sssp_shard_relax": ([C.c_void_p, C.c_void_p], C.c_int),
     "gdx_sssp_shard_frontier32": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "gdx_sssp_shard_relax32": ([C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_shard_relax32_delta": ([C.c_void_p] + [C.c_void_p] * 4, C.c_int),
+    "gdx_sssp_shard_apply32": ([C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64], C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),

@@ -70,7 +70,9 @@ struct SsspWork {
     int32_t shard_v0 = 0, shard_v1 = 0;
     int64_t shard_edges = 0;
     DevBuf<int2> shard_queue;
-    DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges]
+    DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges, changed]
+    DevBuf<int32_t> shard_mark;  // delta mode: round in which a vertex was last listed as changed
+    int32_t shard_round = 0;
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     void* gkey[2][4] = {};

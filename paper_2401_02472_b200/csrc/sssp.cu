@@ -483,13 +483,23 @@ static int frontier_grid(const gdx_graph* g, int64_t cnt) {
 // Relaxation: one warp per item (<= kShardChunk out-edges of one vertex), lanes
 // over the edges; 32-bit distances flag an overflow (ctr[2]) instead of
 // wrapping -- the caller then reruns with 64-bit distances.
-template <class D, int LPI>
+// Delta mode (sharded SSSP, gdx_sssp_shard_relax32_delta): every vertex whose
+// distance this relaxation lowered is listed once per round (mark = round).
+struct SsspDelta {
+    int32_t* mark;
+    int32_t* changed;
+    unsigned long long* count;
+    int32_t round;
+};
+
+template <class D, int LPI, bool DELTA = false>
 __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict__ queue,
                                                         const unsigned long long* __restrict__ ctr,
                                                         const int32_t* __restrict__ offsets,
                                                         const int32_t* __restrict__ dests,
                                                         const int32_t* __restrict__ weights,
-                                                        D* dist, unsigned long long* ovf) {
+                                                        D* dist, unsigned long long* ovf,
+                                                        SsspDelta dl = {}) {
     // LPI lanes per item: lane groups of LPI take one item each
     const int sub = threadIdx.x & (LPI - 1);
     constexpr int kU = kShardChunk / LPI;  // edges per lane per item, all loads issued together
@@ -516,7 +526,37 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
         for (int k = 0; k < kU; ++k) du[k] = u[k] >= 0 ? dist[u[k]] : D(0);
 #pragma unroll
         for (int k = 0; k < kU; ++k)
-            if (u[k] >= 0 && c[k] < du[k]) atomicMin(&dist[u[k]], c[k]);
+            if (u[k] >= 0 && c[k] < du[k]) {
+                if (DELTA) {
+                    if (c[k] < atomicMin(&dist[u[k]], c[k]) &&
+                        atomicMax(&dl.mark[u[k]], dl.round) < dl.round)
+                        dl.changed[atomicAdd(dl.count, 1ull)] = u[k];
+                } else {
+                    atomicMin(&dist[u[k]], c[k]);
+                }
+            }
+    }
+}
+
+// (id, value) pairs of the vertices listed by a delta relaxation.
+template <class D>
+__global__ void k_sssp_delta_values(const int32_t* __restrict__ changed,
+                                    const unsigned long long* __restrict__ count,
+                                    const D* __restrict__ dist, D* vals) {
+    const unsigned long long c = *count;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < c;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        vals[i] = dist[changed[i]];
+}
+
+// Element-wise MIN of received (id, value) pairs into the replica (id < 0: padding).
+template <class D>
+__global__ void k_sssp_delta_apply(const int32_t* __restrict__ ids, const D* __restrict__ vals,
+                                   int64_t count, D* dist) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ids[i];
+        if (v >= 0 && vals[i] < dist[v]) atomicMin(&dist[v], vals[i]);
     }
 }
 
@@ -571,7 +611,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
     auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
             : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
     fn<<<relax_grid, 256, 0, cs>>>(w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
-                                   g->weighted ? g->weights.get() : nullptr, dist, ovf);
+                                   g->weighted ? g->weights.get() : nullptr, dist, ovf, SsspDelta{});
     k_sssp_graph_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), h);
     cudaGraph_t captured;
     GDX_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -659,7 +699,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
             fn<<<relax_grid, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
                                                g->dests.get(),
                                                g->weighted ? g->weights.get() : nullptr, dist,
-                                               ovf.get());
+                                               ovf.get(), SsspDelta{});
         });
         ++launches;
     }
@@ -713,7 +753,7 @@ extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end
         w.shard_v1 = v_end;
         w.shard_edges = int64_t(eb[1]) - eb[0];
         w.shard_queue.ensure(size_t(v_end - v_begin) + size_t(eb[1] - eb[0]) / kShardChunk + 1);
-        w.shard_ctr.ensure(5);
+        w.shard_ctr.ensure(6);
         w.shard_ready = true;
     });
 }
@@ -787,6 +827,59 @@ extern "C" int gdx_sssp_shard_frontier32(gdx_graph* g, int32_t* dist, int32_t* p
 
 extern "C" int gdx_sssp_shard_relax32(gdx_graph* g, int32_t* dist) {
     return guard_impl([&] { shard_relax(g, dist); });
+}
+
+extern "C" int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t* changed_ids,
+                                            int32_t* changed_dist, int64_t* count_out) {
+    return guard_impl([&] {
+        if (!g || !g->sssp || !g->sssp->shard_ready)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+        if (!count_out || (g->n > 0 && (!dist || !changed_ids || !changed_dist)))
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        DeviceGuard dg(g->device);
+        auto& w = *g->sssp;
+        cudaStream_t s = g->stream;
+        if (!w.shard_mark.get() || w.shard_mark.bytes() < size_t(g->n) * 4 ||
+            w.shard_round == INT32_MAX) {
+            w.shard_mark.ensure(size_t(g->n));
+            GDX_CUDA(cudaMemsetAsync(w.shard_mark.get(), 0xff, size_t(g->n) * 4, s));  // -1
+            w.shard_round = 0;
+        }
+        SsspDelta dl{w.shard_mark.get(), changed_ids, w.shard_ctr.get() + 5, ++w.shard_round};
+        GDX_CUDA(cudaMemsetAsync(dl.count, 0, sizeof(unsigned long long), s));
+        const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 64) * g->num_sms;
+        timed_launch(g, "sssp_shard_relax", [&] {
+            k_sssp_scan_relax<int, 16, true><<<blocks, 256, 0, s>>>(
+                w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
+                g->weighted ? g->weights.get() : nullptr, dist,
+                w.shard_ctr.get() + 2, dl);
+        });
+        timed_launch(g, "sssp_shard_delta", [&] {
+            k_sssp_delta_values<int><<<g->num_sms * 4, 256, 0, s>>>(changed_ids, dl.count, dist,
+                                                                   changed_dist);
+        });
+        unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+        GDX_CUDA(cudaMemcpyAsync(h, dl.count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        const int64_t c = int64_t(h[0]);
+        GDX_CUDA(cudaMemcpy(count_out, &c, sizeof(c), cudaMemcpyDefault));
+    });
+}
+
+extern "C" int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t* ids,
+                                      const int32_t* vals, int64_t count) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        if (count < 0 || (count > 0 && (!dist || !ids || !vals)))
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        if (count == 0) return;
+        DeviceGuard dg(g->device);
+        cudaStream_t s = g->stream;
+        timed_launch(g, "sssp_shard_apply", [&] {
+            k_sssp_delta_apply<int><<<blocks_for(count, 256, g->num_sms * 8), 256, 0, s>>>(
+                ids, vals, count, dist);
+        });
+    });
 }
 
 extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {

@@ -114,6 +114,9 @@ class Executor(Protocol):
     # optional int32 replicas (gdx_sssp_shard_*32): (count, overflow) per round
     # def sssp_frontier32(self, dist, prev) -> tuple[int, int]: ...
     # def sssp_relax32(self, dist) -> None: ...
+    # and the delta exchange: the relaxation lists the vertices it lowered
+    # def sssp_relax32_delta(self, dist, ids, vals) -> int: ...
+    # def sssp_apply32(self, dist, ids, vals, count) -> None: ...
 
 
 class DeviceExecutor:
@@ -200,6 +203,12 @@ class DeviceExecutor:
 
     def sssp_relax32(self, dist):
         self._staged(self.g.sssp_shard_relax32, dist)
+
+    def sssp_relax32_delta(self, dist, ids, vals):
+        return self._staged(self.g.sssp_shard_relax32_delta, dist, ids, vals)
+
+    def sssp_apply32(self, dist, ids, vals, count):
+        self._staged(lambda d, i, v: self.g.sssp_shard_apply32(d, i, v, count), dist, ids, vals)
 
 
 # ---------------------------------------------------------------------------- sharded entry points
@@ -411,13 +420,18 @@ INF32 = 2**31 - 1
 
 
 def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats=None,
-                 width: Optional[int] = None):
+                 width: Optional[int] = None, exchange: Optional[str] = None):
     """ComputeSSSP across ranks -> int64[n] (INF = INT64_MAX/2), bit-exact;
     numpy, or the collective-device tensor when ``to_host`` is False.
 
     Rounds run over int32 replicas when the executor has them (half the
     gather and all-reduce bytes); if any rank's relaxation would reach
-    INT32_MAX the call reruns over int64 replicas (``width`` forces one)."""
+    INT32_MAX the call reruns over int64 replicas (``width`` forces one).
+    ``exchange``: "delta" (default with int32 replicas and more than one rank)
+    all-gathers only the vertices each rank lowered in the round and applies
+    them with an element-wise MIN, falling back to the dense MIN all-reduce of
+    the replica in rounds where the lists are not smaller; "dense" always
+    all-reduces the replica."""
     import torch
     from ._lib import GraphdslError
     dist = _dist()
@@ -426,32 +440,40 @@ def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats
     n = ex.num_nodes()
     if not 0 <= src < n:
         raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
+    if exchange not in (None, "delta", "dense"):
+        raise GraphdslError("InvalidArgument", f"InvalidArgument: exchange {exchange!r}")
     v0, v1 = _cached_ranges(ex, "sssp", world, lambda: _partition(ex, "sssp", world))[rank]
     ex.sssp_setup(v0, v1)
     d = None
     if width != 64 and hasattr(ex, "sssp_frontier32"):
-        d32 = _sssp_rounds(ex, src, n, dev, torch.int32, group, stats)
+        delta = exchange != "dense" and world > 1 and hasattr(ex, "sssp_relax32_delta")
+        d32 = _sssp_rounds(ex, src, n, dev, torch.int32, group, stats, delta)
         if d32 is not None:
             d = d32.to(torch.int64)
             d[d32 == INF32] = INF64
     elif width == 32:
         raise GraphdslError("Unsupported", "Unsupported: executor has no int32 SSSP shard")
     if d is None:
-        d = _sssp_rounds(ex, src, n, dev, torch.int64, group, stats)
+        d = _sssp_rounds(ex, src, n, dev, torch.int64, group, stats, False)
     return d.cpu().numpy() if to_host else d
 
 
-def _sssp_rounds(ex, src, n, dev, dtype, group, stats):
+def _sssp_rounds(ex, src, n, dev, dtype, group, stats, delta):
     """fixedPoint rounds of sharded_sssp over `dtype` replicas; None when an
     int32 relaxation overflowed on any rank."""
     import torch
     from ._lib import GraphdslError
     dist = _dist()
+    world = dist.get_world_size(group)
     wide = dtype == torch.int64
     d = torch.full((n,), INF64 if wide else INF32, dtype=dtype, device=dev)
     prev = d.clone()
     d[src] = 0
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    if delta:
+        ids = torch.empty(n, dtype=torch.int32, device=dev)
+        vals = torch.empty(n, dtype=torch.int32, device=dev)
+    sparse_rounds = dense_rounds = 0
     cap = 10 * n + 100
     for r in range(cap + 1):
         if wide:
@@ -464,14 +486,33 @@ def _sssp_rounds(ex, src, n, dev, dtype, group, stats):
             return None
         if c == 0:
             if stats is not None:
-                stats["rounds"] = r + 1
-                stats["width"] = 64 if wide else 32
+                stats.update(rounds=r + 1, width=64 if wide else 32,
+                             exchange={"sparse_rounds": sparse_rounds, "dense_rounds": dense_rounds})
             return d
-        if wide:
-            ex.sssp_relax(d)
-        else:
-            ex.sssp_relax32(d)
-        dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
+        if not delta:
+            if wide:
+                ex.sssp_relax(d)
+            else:
+                ex.sssp_relax32(d)
+            if world > 1:
+                dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
+                dense_rounds += 1
+            continue
+        k = ex.sssp_relax32_delta(d, ids, vals)
+        ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(ks, torch.tensor([k], dtype=torch.int64, device=dev), group=group)
+        kmax = max(int(x) for x in torch.cat(ks).tolist())
+        if 2 * world * kmax > n:  # the lists are not smaller than the replica
+            dist.all_reduce(d, op=dist.ReduceOp.MIN, group=group)
+            dense_rounds += 1
+        elif kmax > 0:
+            ids[k:kmax] = -1  # padding to the common length
+            gi = [torch.empty(kmax, dtype=torch.int32, device=dev) for _ in range(world)]
+            gv = [torch.empty(kmax, dtype=torch.int32, device=dev) for _ in range(world)]
+            dist.all_gather(gi, ids[:kmax], group=group)
+            dist.all_gather(gv, vals[:kmax], group=group)
+            ex.sssp_apply32(d, torch.cat(gi), torch.cat(gv), world * kmax)
+            sparse_rounds += 1
     raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} iterations")
 
 

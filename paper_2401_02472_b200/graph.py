@@ -317,6 +317,18 @@ class DeviceGraph:
     def sssp_shard_relax32(self, dist) -> None:
         check(_lib.load().gdx_sssp_shard_relax32(self.handle, _ptr(dist)))
 
+    def sssp_shard_relax32_delta(self, dist, ids, vals) -> int:
+        """int32 relaxation listing the vertices it lowered (ids, their values)
+        -> how many."""
+        c = np.zeros(1, np.int64)
+        check(_lib.load().gdx_sssp_shard_relax32_delta(self.handle, _ptr(dist), _ptr(ids),
+                                                       _ptr(vals), _ptr(c)))
+        return int(c[0])
+
+    def sssp_shard_apply32(self, dist, ids, vals, count: int) -> None:
+        check(_lib.load().gdx_sssp_shard_apply32(self.handle, _ptr(dist), _ptr(ids), _ptr(vals),
+                                                 int(count)))
+
     # ---- measurement -----------------------------------------------------------
     def profile(self, enable: bool = True) -> None:
         check(_lib.load().gdx_profile_enable(self.handle, int(enable)))

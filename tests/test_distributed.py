@@ -129,6 +129,21 @@ class OracleExecutor:
         o, self.ovf = self.ovf, 0
         return c, o
 
+    def sssp_relax32_delta(self, dist, ids, vals):
+        """gdx_sssp_shard_relax32_delta: the relaxation plus the list of the
+        vertices whose replica distance it lowered (once each) and their values."""
+        before = dist.numpy().copy()
+        self.sssp_relax32(dist)
+        d = dist.numpy()
+        ch = np.flatnonzero(d < before).astype(np.int32)
+        ids[:len(ch)] = torch.from_numpy(ch)
+        vals[:len(ch)] = torch.from_numpy(d[ch])
+        return len(ch)
+
+    def sssp_apply32(self, dist, ids, vals, count):
+        d, i, v = dist.numpy(), ids.numpy()[:count], vals.numpy()[:count]
+        np.minimum.at(d, i[i >= 0], v[i >= 0])
+
     def sssp_relax32(self, dist):
         d = dist.numpy()
         off, dst = self.g.offsets, self.g.dests
@@ -197,6 +212,8 @@ def _worker_pr_sssp(rank, world, port, q):
     d0 = D.sharded_sssp(OracleExecutor(gu), 0, stats=st0)
     d5 = D.sharded_sssp(OracleExecutor(gu), 5, stats=st5)
     d0w = D.sharded_sssp(OracleExecutor(gu), 0, width=64, stats=st64)
+    std = {}
+    d0d = D.sharded_sssp(OracleExecutor(gu), 0, exchange="dense", stats=std)
     # weights near 2^30: int32 replicas overflow, the call reruns over int64
     gb = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1 << 29, 1 << 30, 4)
     db = D.sharded_sssp(OracleExecutor(gb), 0, stats=stbig)
@@ -204,6 +221,8 @@ def _worker_pr_sssp(rank, world, port, q):
         exp_r, exp_rounds = p.pr(gd, 0.85, 1e-9, 110)
         e0 = p.sssp(gu, 0)
         assert np.array_equal(d0w, e0) and st64["width"] == 64
+        assert np.array_equal(d0d, e0) and std["exchange"]["sparse_rounds"] == 0
+        assert st0["exchange"]["sparse_rounds"] > 0  # the delta exchange ran
         assert st0["width"] == 32 and st5["width"] == 32
         eb = p.sssp(gb, 0)
         assert np.array_equal(db, eb) and stbig["width"] == 64

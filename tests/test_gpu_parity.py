@@ -377,6 +377,7 @@ def _gpu_shard_worker(rank, world, port, q):
     st32, st64, stb = {}, {}, {}
     d = D.sharded_sssp(exu, 7, stats=st32)  # int32 replicas
     d64 = D.sharded_sssp(exu, 7, width=64, stats=st64)
+    dd = D.sharded_sssp(exu, 7, exchange="dense")
     # weights near 2^30: the int32 rounds overflow and the call reruns over int64
     gb = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1 << 29, 1 << 30, 4)
     db = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gb)), 0, stats=stb)
@@ -387,7 +388,8 @@ def _gpu_shard_worker(rank, world, port, q):
         er, erounds = p.pr(gd, 0.85, 1e-9, 110)
         q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3,
                bc, p.bc(gu, srcs), tc, p.tc(gu),
-               (d64, st32["width"], st64["width"], db, p.sssp(gb, 0), stb["width"])))
+               (d64, st32["width"], st64["width"], db, p.sssp(gb, 0), stb["width"], dd,
+                st32["exchange"])))
     tdist.destroy_process_group()
 
 
@@ -414,8 +416,9 @@ def test_sharded_pr_sssp_device(gdx, world):
     assert rel_err(r, er) < 1e-12
     assert rel_err(r2, er) < 1e-12 and rel_err(r3, er) < 1e-12
     assert np.array_equal(d, ed)
-    d64, w32, w64, db, edb, wb = wide
-    assert np.array_equal(d64, ed) and (w32, w64) == (32, 64)
+    d64, w32, w64, db, edb, wb, dd, exch = wide
+    assert np.array_equal(d64, ed) and (w32, w64) == (32, 64) and np.array_equal(dd, ed)
+    assert world == 1 or exch["sparse_rounds"] > 0  # delta exchange (lists < replica)
     assert np.array_equal(db, edb) and wb == 64 and edb[edb < (2**63 - 1) // 2].max() >= 2**31 - 1
     assert rel_err(bc, ebc) < 1e-9 and tc == etc_
 
