@@ -121,6 +121,13 @@ class Dist:
         torch.cuda.set_device(self.local)
         if self.world > 1 or force:
             import torch.distributed as dist
+            if "RANK" not in os.environ:  # --sharded without torchrun: a 1-rank group
+                import socket
+                sk = socket.socket()
+                sk.bind(("127.0.0.1", 0))
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                                  RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+                sk.close()
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
 
@@ -143,7 +150,7 @@ class Dist:
 
 # ------------------------------------------------------------------------ our arm
 
-def timed_steps(torch, dist, step, steps: int, warmup: int, flush):
+def timed_steps(torch, dist, step, steps: int, warmup: int, flush, keep_all: bool = True):
     """W warm-up steps, then K steps each preceded by an L2 flush; returns
     (per-step ms list, bracketed total ms).  Device time via CUDA events on the
     current stream (the library runs on it, see gdx_graph_set_stream)."""
@@ -152,13 +159,18 @@ def timed_steps(torch, dist, step, steps: int, warmup: int, flush):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
+    # keep_all=False keeps only the last step's result: holding every step's
+    # device output (C5's 537 MB distance vector) would make the later steps
+    # allocate under memory pressure inside the timed region
     results = []
     dist.barrier(torch)
     t0 = time.perf_counter()
     for a, b in evs:
         flush.zero_()
         a.record()
-        results.append(step())
+        r = step()
+        results = results + [r] if keep_all else [r]
+        del r
         b.record()
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
@@ -241,7 +253,8 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
         return r
 
     dg.close()
-    e2e_step()
+    for _ in range(args.warmup):
+        e2e_step()
     dist.barrier(torch)
     t0 = time.perf_counter()
     rr = []
@@ -401,7 +414,7 @@ def bench_bc(torch, gdx, dist, args, pk) -> dict:
         return st
 
     dg.profile(True)
-    for _ in range(max(1, args.warmup // 3)):
+    for _ in range(args.warmup):
         step()
     dg.profile_reset()
     sts.clear()
@@ -502,7 +515,8 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
         return r
 
     dg.close()
-    e2e_step()
+    for _ in range(args.warmup):
+        e2e_step()
     dist.barrier(torch)
     t0 = time.perf_counter()
     rr = [e2e_step() for _ in range(args.steps)]
@@ -556,11 +570,13 @@ def bench_sharded_other(torch, gdx, dist, args, pk, algo: str) -> dict:
         units, name, kern = float(dg.m), \
             "C5 SSSP RMAT-26 ef16 undirected, weights U[1,100], src 0", "sssp_shard_relax"
     dg.profile(True)
-    for _ in range(1 if algo != "tc" else args.warmup):
+    for _ in range(args.warmup):  # W >= 3 (the second C5 call still pays ~60 ms of first-use cost)
         step()
     dg.profile_reset()
     steps = max(1, args.steps // 2) if algo == "bc" else args.steps
-    ms, wall, outs = timed_steps(torch, dist, step, steps, 0, flush)
+    ms, wall, outs = timed_steps(torch, dist, step, steps, 0, flush, keep_all=False)
+    if dist.rank == 0:
+        print(f"{algo} sharded steps (ms): " + " ".join(f"{x:.1f}" for x in ms), file=sys.stderr)
     prof = dg.profile_read()
     total = dist.max(torch, sum(ms))
     res = {"workload": name, "n": dg.n, "m": dg.m, "steps": steps,

@@ -203,6 +203,15 @@ int gdx_pr_p2p_open(gdx_graph* g, const void* handles /* world * 64 bytes */);
 int gdx_pr_p2p_init(gdx_graph* g, double* partials_out);
 int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, double threshold,
                      int32_t max_iter, double dangling_in, double* partials_out);
+/* Rounds [first, first + count) enqueued without host round trips: each ends
+ * with a device-side wait for every rank's publish and the rank-ordered sum of
+ * the published partials (next round's dangling mass, global vote); a round
+ * after a settled one exits on the device.  dangling_in is used for round 0
+ * only (from gdx_pr_p2p_init).  *settled_out = the first round in the range
+ * whose global vote is "settled", or -1.  Every rank must issue the same ranges. */
+int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, double damping,
+                      double threshold, int32_t max_iter, double dangling_in,
+                      int32_t* settled_out);
 int gdx_pr_p2p_close(gdx_graph* g);
 
 /* SSSP, vertex ranges: every rank keeps a full int64 replica of dist (device

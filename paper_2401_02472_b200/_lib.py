@@ -92,6 +92,8 @@ SIGNATURES = {
     "gdx_pr_p2p_init": ([C.c_void_p, f64p], C.c_int),
     "gdx_pr_p2p_round": ([C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_double,
                           f64p], C.c_int),
+    "gdx_pr_p2p_rounds": ([C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                           C.c_double, C.c_void_p], C.c_int),
     "gdx_pr_p2p_close": ([C.c_void_p], C.c_int),
     "gdx_sssp_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32], C.c_int),
     "gdx_sssp_shard_frontier": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

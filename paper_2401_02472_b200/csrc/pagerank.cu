@@ -679,6 +679,35 @@ __global__ void k_p2p_publish(const double* dang, const int32_t* unsettled, doub
     for (int q = 0; q < world; ++q) atomicAdd_system(ctrs[q], 1ull);
 }
 
+// Device-side end of a peer-memory round (gdx_pr_p2p_rounds): wait until
+// every rank's publish `target / world - 1` has landed, then sum the published
+// (dangling, unsettled) slots in rank order -- identical on every rank -- into
+// the next round's dangling mass and this round's global vote, which the next
+// round's kernels read to exit early once the ranks have settled.
+__global__ void k_p2p_combine(const unsigned long long* ctr, unsigned long long target, int* err,
+                              const double* slots, int world, double* dangling_next,
+                              int32_t* vote) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*reinterpret_cast<const volatile unsigned long long*>(ctr) < target) {
+        __nanosleep(256);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {
+            *err = 1;
+            break;
+        }
+    }
+    __threadfence_system();
+    const volatile double* vs = slots;
+    double d = 0.0, u = 0.0;
+    for (int q = 0; q < world; ++q) {
+        d += vs[2 * q];
+        u += vs[2 * q + 1];
+    }
+    *dangling_next = d;
+    *vote = u != 0.0 ? 1 : 0;
+}
+
 }  // namespace gdx
 
 using namespace gdx;
@@ -833,6 +862,74 @@ extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, dou
         GDX_LAUNCH_CHECK();
         X.publishes = j + 1;
         p2p_gather_partials(g, X, j, partials_out);
+    });
+}
+
+extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, double damping,
+                                 double threshold, int32_t max_iter, double dangling_in,
+                                 int32_t* settled_out) {
+    return guard_impl([&] {
+        if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !settled_out)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
+        if (first < 0 || count < 1) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad round range");
+        DeviceGuard dg(g->device);
+        auto& P = *g->pr_shard;
+        auto& X = *g->pr_p2p;
+        cudaStream_t s = g->stream;
+        const int32_t last = first + count;
+        if (P.flags_cap < last) {
+            const int32_t cap = std::max(last, 2 * P.flags_cap);
+            DevBuf<int32_t> nf(cap);
+            if (first > 0 && P.flags.get()) {  // earlier rounds' votes decide skipping
+                GDX_CUDA(cudaMemcpyAsync(nf.get(), P.flags.get(), size_t(first) * 4,
+                                         cudaMemcpyDeviceToDevice, s));
+                GDX_CUDA(cudaStreamSynchronize(s));  // before the old block returns to the pool
+            }
+            P.flags = std::move(nf);
+            P.flags_cap = cap;
+        }
+        if (first == 0) {  // round 0's dangling mass comes from gdx_pr_p2p_init
+            GDX_CUDA(cudaMemcpyAsync(P.dangling.get(), &dangling_in, sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+        }
+        GDX_CUDA(cudaMemsetAsync(P.flags.get() + first, 0, size_t(count) * 4, s));
+        for (int32_t round = first; round < last; ++round) {
+            const int64_t j = X.publishes;
+            PrArgs a = make_args(g, P, damping, threshold, max_iter);
+            a.shard = 0;  // a round after a settled one exits on the device
+            a.contrib0 = a.contrib1 = X.own_contrib(int((j - 1) & 1));
+            a.peers = X.peer_contrib.get() + (j & 1) * X.world;
+            a.npeers = X.world;
+            if (P.ngroups > 0)
+                timed_launch(g, "pr_edges", [&] { k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round); });
+            timed_launch(g, "pr_vertices", [&] {
+                k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
+                                                 g->num_sms * 8),
+                                      kPrBlock, 0, s>>>(a, round);
+            });
+            k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + round,
+                                          X.peer_slot.get() + (j & 1) * X.world, X.peer_ctr.get(),
+                                          X.world);
+            GDX_LAUNCH_CHECK();
+            k_p2p_combine<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)(j + 1) * X.world,
+                                          X.err.get(), X.own_partials(int(j & 1)), X.world,
+                                          P.dangling.get() + (round + 1) % 3, P.flags.get() + round);
+            GDX_LAUNCH_CHECK();
+            X.publishes = j + 1;
+        }
+        std::vector<int32_t> votes(static_cast<size_t>(count));
+        int herr = 0;
+        GDX_CUDA(cudaMemcpyAsync(votes.data(), P.flags.get() + first, size_t(count) * 4,
+                                 cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaMemcpyAsync(&herr, X.err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        if (herr) fail(GDX_ERR_CUDA, "CudaError: peer-memory exchange timed out");
+        *settled_out = -1;
+        for (int32_t i = 0; i < count; ++i)
+            if (votes[size_t(i)] == 0) {
+                *settled_out = first + i;
+                break;
+            }
     });
 }
 

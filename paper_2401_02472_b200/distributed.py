@@ -397,11 +397,17 @@ def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_i
     want = max_iter + 1 if max_iter >= 0 else 1
     limit = min(want, cap)
     rounds = limit
-    for r in range(limit):
-        dangling, unsettled = g.pr_p2p_round(r, damping, threshold, max_iter, dangling)
-        if unsettled == 0.0:
-            rounds = r + 1
+    # rounds in growing batches without host round trips (the same schedule
+    # on every rank); rounds past the settled one exit on the device
+    r, batch = 0, 4
+    while r < limit:
+        cnt = min(batch, limit - r)
+        settled = g.pr_p2p_rounds(r, cnt, damping, threshold, max_iter, dangling)
+        if settled >= 0:
+            rounds = settled + 1
             break
+        r += cnt
+        batch = min(2 * batch, 64)
     else:
         if limit < want:
             raise GraphdslError("NonTermination", f"NonTermination: fixedPoint exceeded {cap} "

@@ -294,6 +294,16 @@ class DeviceGraph:
                                            int(max_iter), float(dangling_in), out))
         return out[0], out[1]
 
+    def pr_p2p_rounds(self, first: int, count: int, damping: float, threshold: float,
+                      max_iter: int, dangling_in: float) -> int:
+        """Rounds [first, first+count) without host round trips -> the first
+        settled round in the range, or -1."""
+        st = C.c_int32(-1)
+        check(_lib.load().gdx_pr_p2p_rounds(self.handle, int(first), int(count), float(damping),
+                                            float(threshold), int(max_iter), float(dangling_in),
+                                            C.byref(st)))
+        return st.value
+
     def pr_p2p_close(self) -> None:
         check(_lib.load().gdx_pr_p2p_close(self.handle))
 
