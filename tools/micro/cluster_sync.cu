@@ -12,15 +12,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) k(int iters, i
     int* mine = buf + (blockIdx.x / 2) * (1 << 20);
     int x = tid;
     for (int it = 0; it < iters; ++it) {
-        if (MODE == 1) mine[(tid * 97 + it * 131) & ((1 << 20) - 1)] = it;          // store
-        if (MODE == 2) atomicAdd(&acc[(tid * 7919 + it * 104729) % n], 1.0);        // red
+        if (MODE == 1 || MODE == 5) mine[(tid * 97 + it * 131) & ((1 << 20) - 1)] = it;          // store
+        if (MODE == 2 || MODE == 6) atomicAdd(&acc[(tid * 7919 + it * 104729) % n], 1.0);        // red
         if (MODE == 3) x = mine[(x * 97 + it) & ((1 << 20) - 1)] & 1023;             // 1 L2 load
         if (MODE == 4) {                                                             // 3 dep loads
             x = mine[(x * 97 + it) & ((1 << 20) - 1)] & 1023;
             x = mine[(x * 31 + it + 7) & ((1 << 20) - 1)] & 1023;
             x = mine[(x * 13 + it + 5) & ((1 << 20) - 1)] & 1023;
         }
-        cl.sync();
+        if (MODE >= 5) {  // relaxed arrive (no release of the prior stores) + wait
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+        } else {
+            cl.sync();
+        }
     }
     if (x == -5) buf[0] = x;
 }
@@ -54,5 +58,7 @@ int main() {
     printf("global red.f64 + sync    : %.2f us\n", run<2>(it, buf, acc, n));
     printf("1 dependent load + sync  : %.2f us\n", run<3>(it, buf, acc, n));
     printf("3 dependent loads + sync : %.2f us\n", run<4>(it, buf, acc, n));
+    printf("store + relaxed arrive    : %.2f us\n", run<5>(it, buf, acc, n));
+    printf("red + relaxed arrive      : %.2f us\n", run<6>(it, buf, acc, n));
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
