@@ -92,6 +92,23 @@ def test_errors_match_reference(gdx, known):
     assert it == 51
 
 
+def test_shard_entry_points_validate(gdx, known):
+    """The multi-GPU entry points fail loudly on misuse instead of launching."""
+    import torch
+    g = known_graph(known["weighted_triangle"])
+    dg = gdx.DeviceGraph.from_csr(g)
+    d = torch.zeros(dg.n, dtype=torch.int32, device="cuda")
+    with pytest.raises(gdx.GraphdslError, match="no shard plan"):
+        dg.sssp_shard_relax32_delta(d, d.clone(), d.clone())
+    with pytest.raises(gdx.GraphdslError, match="no shard plan"):
+        dg.sssp_shard_frontier32(d, d.clone())
+    with pytest.raises(gdx.GraphdslError, match="out of bounds"):
+        dg.sssp_shard_setup(0, dg.n + 1)
+    with pytest.raises(gdx.GraphdslError, match="no p2p plan"):
+        dg.pr_p2p_rounds(0, 4, 0.85, 1e-6, 100, 0.0)
+    dg.sssp_shard_apply32(d, d, d, 0)  # nothing to apply: a no-op
+
+
 # ---- acceptance criterion 2 sweep: 200 reference graphs ------------------------------
 
 def test_sweep_vs_reference(gdx, sweep):
