@@ -75,8 +75,8 @@ struct SsspWork {
     int32_t shard_round = 0;
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    void* gkey[2][4] = {};
-    DevBuf<unsigned long long> graph_acc, graph_ovf;
+    void* gkey[2][5] = {};
+    DevBuf<unsigned long long> graph_acc;  // [rounds, vertices, edges, overflow]
     ~SsspWork() {
         for (auto& e : gexec)
             if (e) cudaGraphExecDestroy(e);

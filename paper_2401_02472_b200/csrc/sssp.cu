@@ -561,7 +561,11 @@ __global__ void k_sssp_delta_apply(const int32_t* __restrict__ ids, const D* __r
 }
 
 template <class D>
-__global__ void k_sssp_scan_init(int32_t n, int32_t src, D inf, D* dist, D* prev) {
+__global__ void k_sssp_scan_init(int32_t n, int32_t src, D inf, D* dist, D* prev,
+                                 unsigned long long* z0, int nz0, unsigned long long* z1, int nz1) {
+    // also zeroes the call's counters (z0[0, nz0), z1[0, nz1)): no memsets
+    if (blockIdx.x == 0 && threadIdx.x < nz0) z0[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < nz1) z1[threadIdx.x] = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         dist[i] = i == src ? D(0) : inf;
@@ -639,11 +643,15 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     w.shard_queue.ensure(items_cap);
     w.shard_ctr.ensure(5);
     unsigned long long* ctr = w.shard_ctr.get();
+    // graph path: round counters, [rounds, vertices, edges, overflow] in
+    // graph_acc; host loop: its own overflow flag
+    w.graph_acc.ensure(4);
     DevBuf<unsigned long long> ovf(1);
-    GDX_CUDA(cudaMemsetAsync(ovf.get(), 0, 8, s));
+    unsigned long long* ovf_flag = use_graph ? w.graph_acc.get() + 3 : ovf.get();
     timed_launch(g, "sssp_init", [&] {
-        k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, src, inf, dist,
-                                                                              prev);
+        k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
+            n, src, inf, dist, prev, ctr, 5, use_graph ? w.graph_acc.get() : ovf.get(),
+            use_graph ? 4 : 1);
     });
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     unsigned long long vvis = 0, evis = 0;
@@ -657,29 +665,17 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const int relax_grid =
         (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 64)) * g->num_sms;
     if (use_graph) {
-        w.graph_acc.ensure(4);
-        w.graph_ovf.ensure(1);
         const int di = sizeof(D) == 4 ? 0 : 1;
-        void* key[4] = {dist, prev, w.shard_queue.get(), ctr};
+        // the instantiated graph bakes in these buffers
+        void* key[5] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get()};
         bool same = w.gexec[di] != nullptr;
-        for (int i = 0; i < 4; ++i) same = same && w.gkey[di][i] == key[i];
+        for (int i = 0; i < 5; ++i) same = same && w.gkey[di][i] == key[i];
         if (!same) {
             if (w.gexec[di]) cudaGraphExecDestroy(w.gexec[di]);
-            w.gexec[di] = build_sssp_graph<D>(g, dist, prev, w.graph_ovf.get(), lpi, relax_grid);
-            for (int i = 0; i < 4; ++i) w.gkey[di][i] = key[i];
+            w.gexec[di] = build_sssp_graph<D>(g, dist, prev, ovf_flag, lpi, relax_grid);
+            for (int i = 0; i < 5; ++i) w.gkey[di][i] = key[i];
         }
-        GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
-        GDX_CUDA(cudaMemsetAsync(w.graph_acc.get(), 0, 4 * sizeof(unsigned long long), s));
-        GDX_CUDA(cudaMemsetAsync(w.graph_ovf.get(), 0, 8, s));
         timed_launch(g, "sssp_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.gexec[di], s)); });
-        GDX_CUDA(cudaMemcpyAsync(h, w.graph_acc.get(), 3 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-        GDX_CUDA(cudaStreamSynchronize(s));
-        rounds = int(h[0]);
-        vvis = h[1];
-        evis = h[2];
-        launches += 3 * (rounds + 1);
-        GDX_CUDA(cudaMemcpyAsync(ovf.get(), w.graph_ovf.get(), 8, cudaMemcpyDeviceToDevice, s));
     }
     for (; !use_graph; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
@@ -713,9 +709,18 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         k_sssp_widen<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, dist, inf, target);
     });
     if (!dev_out) copy_out(g, dist_out, target, size_t(n) * sizeof(int64_t));
-    GDX_CUDA(cudaMemcpyAsync(h, ovf.get(), 8, cudaMemcpyDeviceToHost, s));
+    // one host read per call: the graph path's counters and the overflow flag
+    GDX_CUDA(cudaMemcpyAsync(h, use_graph ? w.graph_acc.get() : ovf.get(),
+                             (use_graph ? 4 : 1) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
-    const bool overflow = h[0] != 0;
+    const bool overflow = (use_graph ? h[3] : h[0]) != 0;
+    if (use_graph) {
+        rounds = int(h[0]);
+        vvis = h[1];
+        evis = h[2];
+        launches += 3 * (rounds + 1);
+    }
     if (stats) {
         stats->rounds = rounds;
         stats->launches = launches + 1;
