@@ -444,8 +444,8 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, double2 sig) {
 // adjacency).  Out of line so their registers do not weigh on the light path.
 __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* rec, int4* log,
                                                   const int* s_h, int hn, int L, int end,
-                                                  int* s_next, unsigned long long& fscan,
-                                                  unsigned long long& dag) {
+                                                  int* s_next, unsigned& fscan,
+                                                  unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
         const int4 it = log[s_h[h]];
@@ -487,8 +487,8 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
 
 __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec* rec, const int4* log,
                                                    const int* s_h, int hn, int Lb, int32_t src,
-                                                   unsigned long long& bscan,
-                                                   unsigned long long& dag) {
+                                                   unsigned& bscan,
+                                                   unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
         const int4 it = log[s_h[h]];
@@ -536,7 +536,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     BcRec* rec = a.rec + slot * a.n;
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
-    unsigned long long reached = 0, fscan = 0, bscan = 0, dag = 0, levels_max = 0;
+    // per-source 32-bit counters (registers are the kernel's limit), flushed
+    // to the 64-bit totals after every source
+    unsigned fscan = 0, bscan = 0, dag = 0;
     int tk = 0;
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
@@ -647,8 +649,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         cluster.sync();  // loff[levels] (written by thread 0 above) before the backward pass
         const int levels = L + 1;  // loff[0..levels] bound the levels in log
         if (tid == 0) {
-            reached += end;
-            levels_max = max(levels_max, (unsigned long long)levels);
+            atomicAdd(&a.ctr[kReached], (unsigned long long)end);
+            atomicMax(&a.ctr[kLevels], (unsigned long long)levels);
         }
         // ---- backward: iterateInReverse ----
         for (int Lb = levels - 1; Lb >= 0; --Lb) {
@@ -701,24 +703,24 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             cluster.sync();
             bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
         }
+        {
+            unsigned long long f = fscan, b = bscan, d = dag;
+            for (int o = 16; o; o >>= 1) {
+                f += __shfl_xor_sync(0xffffffffu, f, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+                d += __shfl_xor_sync(0xffffffffu, d, o);
+            }
+            if ((ltid & 31) == 0) {
+                atomicAdd(&a.ctr[kFwdScan], f);
+                atomicAdd(&a.ctr[kBwdScan], b);
+                atomicAdd(&a.ctr[kDag], d);
+            }
+            fscan = bscan = dag = 0;
+        }
         // restore `level` for the slot's next source
         for (int i = tid; i < end; i += kStride) rec[log[i].x].level = -1;
         cluster.sync();
         bc_trace(a, slot, tid, tk, 1 << 30);  // restore step
-    }
-    for (int o = 16; o; o >>= 1) {
-        fscan += __shfl_xor_sync(0xffffffffu, fscan, o);
-        bscan += __shfl_xor_sync(0xffffffffu, bscan, o);
-        dag += __shfl_xor_sync(0xffffffffu, dag, o);
-    }
-    if ((ltid & 31) == 0) {
-        atomicAdd(&a.ctr[kFwdScan], fscan);
-        atomicAdd(&a.ctr[kBwdScan], bscan);
-        atomicAdd(&a.ctr[kDag], dag);
-    }
-    if (tid == 0) {
-        atomicAdd(&a.ctr[kReached], reached);
-        atomicMax(&a.ctr[kLevels], levels_max);
     }
 }
 
