@@ -416,25 +416,60 @@ __device__ inline void bc_trace(const BcCtaArgs& a, int64_t slot, int tid, int& 
     ++k;
 }
 
-__device__ inline void rec_level_sigma(const BcRec* r, int32_t& level, double2& sig) {
+// The CTA kernel carries sigma as {mantissa, int exponent} (3 registers, no
+// int<->double conversions); same values as the double2 form above.
+struct XF {
+    double m;  // in [1, 2), or 0
+    int e;
+};
+
+__device__ inline XF xf_add(XF a, XF b) {
+    if (a.m == 0.0) return b;
+    if (b.m == 0.0) return a;
+    if (a.e == b.e) {  // common case: same binade exponent, exact renormalisation
+        const double s = a.m + b.m;
+        return s < 2.0 ? XF{s, a.e} : XF{s * 0.5, a.e + 1};
+    }
+    const int e = max(a.e, b.e);
+    const double s = ldexp(a.m, a.e - e) + ldexp(b.m, b.e - e);
+    const int k = ilogb(s);
+    return XF{ldexp(s, -k), e + k};
+}
+
+__device__ inline double xf_ratio(XF a, XF b) {
+    const double q = a.m / b.m;
+    return a.e == b.e ? q : ldexp(q, a.e - b.e);
+}
+
+__device__ inline XF xf_warp_sum(XF a) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        XF b;
+        b.m = __shfl_xor_sync(0xffffffffu, a.m, o);
+        b.e = __shfl_xor_sync(0xffffffffu, a.e, o);
+        a = xf_add(a, b);
+    }
+    return a;
+}
+
+__device__ inline void rec_level_sigma(const BcRec* r, int32_t& level, XF& sig) {
     const int4 q = *reinterpret_cast<const int4*>(r);
     level = q.x;
-    sig = make_double2(__hiloint2double(q.w, q.z), double(q.y));
+    sig = XF{__hiloint2double(q.w, q.z), q.y};
 }
-__device__ inline void rec_all(const BcRec* r, int32_t& level, double2& sig, double& delta) {
+__device__ inline void rec_all(const BcRec* r, int32_t& level, XF& sig, double& delta) {
     int32_t x[8];
     asm("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
           "=r"(x[7])
         : "l"(r));
     level = x[0];
-    sig = make_double2(__hiloint2double(x[3], x[2]), double(x[1]));
+    sig = XF{__hiloint2double(x[3], x[2]), x[1]};
     delta = __hiloint2double(x[5], x[4]);
 }
-__device__ inline void rec_store_sigma(BcRec* r, int32_t level, double2 sig) {
-    const double m = sig.x;
+__device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
     *reinterpret_cast<int4*>(r) =
-        make_int4(level, int32_t(sig.y), __double2loint(m), __double2hiint(m));
+        make_int4(level, sig.e, __double2loint(sig.m), __double2hiint(sig.m));
 }
 
 // CS CTAs (a thread-block cluster) share one source: the level barrier is a
@@ -450,12 +485,12 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
         const int4 it = log[s_h[h]];
         const int32_t v = it.x, ob = it.y, oe = it.z;
-        double2 acc = make_double2(L == 0 && lane == 0 ? 1.0 : 0.0, 0.0);
+        XF acc{L == 0 && lane == 0 ? 1.0 : 0.0, 0};
         if (lane == 0) fscan += oe - ob;
         for (int32_t e = ob + lane; e < oe; e += 32) {
             const int32_t w = a.dests[e];
             int32_t lw;
-            double2 sg;
+            XF sg;
             rec_level_sigma(rec + w, lw, sg);
             if (a.undirected && L > 0 && lw == L - 1) {
                 acc = xf_add(acc, sg);
@@ -472,7 +507,7 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
             if (lane == 0) fscan += ie - ib;
             for (int32_t e = ib + lane; e < ie; e += 32) {
                 int32_t lp;
-                double2 sg;
+                XF sg;
                 rec_level_sigma(rec + a.in_srcs[e], lp, sg);
                 if (lp == L - 1) {
                     acc = xf_add(acc, sg);
@@ -494,16 +529,16 @@ __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec*
         const int4 it = log[s_h[h]];
         const int32_t v = it.x, ob = it.y, oe = it.z;
         int32_t lv;
-        double2 sv;
+        XF sv;
         rec_level_sigma(rec + v, lv, sv);
         double d = 0.0;
         if (lane == 0) bscan += oe - ob;
         for (int32_t e = ob + lane; e < oe; e += 32) {
             int32_t lw;
-            double2 sw;
+            XF sw;
             double dw;
             rec_all(rec + a.dests[e], lw, sw, dw);
-            if (lw == Lb + 1 && sw.x > 0.0) {
+            if (lw == Lb + 1 && sw.m > 0.0) {
                 d += xf_ratio(sv, sw) * (1.0 + dw);
                 ++dag;
             }
@@ -569,17 +604,17 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     }
                     heavy = false;  // list full: this item runs on its own thread
                 }
-                double2 acc = make_double2(L == 0 ? 1.0 : 0.0, 0.0);
+                XF acc{L == 0 ? 1.0 : 0.0, 0};
                 fscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
-                    double2 sg[kNb];
+                    XF sg[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {  // level and sigma in one 16 B load
                         lw[k] = -2;
-                        sg[k] = make_double2(0.0, 0.0);
+                        sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
                     bool par[kNb], got[kNb];
@@ -607,13 +642,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     fscan += ie - ib;
                     for (int32_t e = ib; e < ie; e += kNb) {
                         int32_t p[kNb], lp[kNb];
-                        double2 sg[kNb];
+                        XF sg[kNb];
 #pragma unroll
                         for (int k = 0; k < kNb; ++k) p[k] = e + k < ie ? a.in_srcs[e + k] : -1;
 #pragma unroll
                         for (int k = 0; k < kNb; ++k) {
                             lp[k] = -2;
-                            sg[k] = make_double2(0.0, 0.0);
+                            sg[k] = XF{0.0, 0};
                             if (p[k] >= 0) rec_level_sigma(rec + p[k], lp[k], sg[k]);
                         }
 #pragma unroll
@@ -668,26 +703,26 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     }
                 }
                 int32_t lv;
-                double2 sv;
+                XF sv;
                 rec_level_sigma(rec + v, lv, sv);
                 double d = 0.0;
                 bscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
-                    double2 sw[kNb];
+                    XF sw[kNb];
                     double dw[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {  // level, sigma and delta in one 32 B load
                         lw[k] = -2;
-                        sw[k] = make_double2(1.0, 0.0);
+                        sw[k] = XF{1.0, 0};
                         dw[k] = 0.0;
                         if (w[k] >= 0) rec_all(rec + w[k], lw[k], sw[k], dw[k]);
                     }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k)
-                        if (lw[k] == Lb + 1 && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
+                        if (lw[k] == Lb + 1 && sw[k].m > 0.0) {  // ascending child order (oracles.cpp:60-67)
                             d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
                             ++dag;
                         }
