@@ -775,8 +775,9 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     if (CS != 1 && CS != 2 && CS != 4) CS = 1;
     int slots = std::max(1, std::min<int32_t>(nsrc, g->num_sms / CS));
     // a slot holds 52 B per vertex (record, log entry, level bound): fewer
-    // slots (each then runs several sources) when they would not fit
-    {
+    // slots (each then runs several sources) when they would not fit (queried
+    // only when the slots have to grow)
+    if (W.cta_grid < slots) {
         size_t free_b = 0, tot_b = 0;
         GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
         const size_t per_slot = size_t(n) * 52 + 8;
