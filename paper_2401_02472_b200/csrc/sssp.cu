@@ -366,9 +366,13 @@ constexpr int kShardChunk = 64;  // edges per relaxation item (C5: 23.7 ms vs 26
 
 // Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
 // distance dropped since they were last expanded (dist < prev; prev := dist).
-// One global atomic per block-chunk of 2048 vertices.
+// One global atomic per block-chunk of kFBlock * 8 vertices.
+#ifndef GDX_SSSP_FBLOCK
+#define GDX_SSSP_FBLOCK 256
+#endif
+constexpr int kFBlock = GDX_SSSP_FBLOCK;
 template <class D>
-__global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t v1,
+__global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int32_t v1,
                                                            const int32_t* __restrict__ offsets,
                                                            const D* __restrict__ dist, D* prev,
                                                            int2* queue,
@@ -376,24 +380,24 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
     constexpr int kPer = 8;  // vertices per thread per chunk
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ int s_warp[8];
+    __shared__ int s_warp[kFBlock / 32];
     __shared__ unsigned long long s_base;
-    for (int64_t c0 = v0 + int64_t(blockIdx.x) * 256 * kPer; c0 < v1;
-         c0 += int64_t(gridDim.x) * 256 * kPer) {
+    for (int64_t c0 = v0 + int64_t(blockIdx.x) * kFBlock * kPer; c0 < v1;
+         c0 += int64_t(gridDim.x) * kFBlock * kPer) {
         // all loads of the chunk are issued before any is consumed: the prev
         // stores would otherwise order each vertex's loads after the previous
         // vertex's (possible aliasing), one DRAM round trip per vertex
         D dk[kPer], pk[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             dk[k] = v < v1 ? dist[v] : D(0);
             pk[k] = v < v1 ? prev[v] : D(0);
         }
         int items[kPer], first[kPer], last[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             const bool f = dk[k] < pk[k];  // false past v1 (both 0)
             first[k] = f ? offsets[v] : 0;
             last[k] = f ? offsets[v + 1] : -1;
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
         unsigned long long vis = 0, edg = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const int64_t v = c0 + int64_t(k) * 256 + threadIdx.x;
+            const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             items[k] = 0;
             if (last[k] >= 0) {
                 prev[v] = dk[k];
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
         __syncthreads();
         if (threadIdx.x == 0) {
             int tot = 0;
-            for (int w = 0; w < 8; ++w) {
+            for (int w = 0; w < kFBlock / 32; ++w) {
                 const int x = s_warp[w];
                 s_warp[w] = tot;
                 tot += x;
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_frontier(int32_t v0, int32_t 
         unsigned long long pos = s_base + s_warp[warp] + incl - mine;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const int32_t v = int32_t(c0 + int64_t(k) * 256 + threadIdx.x);
+            const int32_t v = int32_t(c0 + int64_t(k) * kFBlock + threadIdx.x);
             // a hub's items (a degree-10^6 vertex has ~10^4) are written by the
             // whole warp, not serially by its own lane
             const bool big = items[k] > kSplitItems;
@@ -474,10 +478,10 @@ static int frontier_grid(const gdx_graph* g, int64_t cnt) {
     static const int per_sm = [] {
         if (const char* e = std::getenv("GDX_SSSP_FGRID")) return std::max(1, std::atoi(e));
         int b = 0;
-        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sssp_scan_frontier<D>, 256, 0));
+        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sssp_scan_frontier<D>, kFBlock, 0));
         return std::max(1, b);
     }();
-    return blocks_for(cnt, 256 * 8, g->num_sms * per_sm);
+    return blocks_for(cnt, kFBlock * 8, g->num_sms * per_sm);
 }
 
 // Relaxation: one warp per item (<= kShardChunk out-edges of one vertex), lanes
@@ -610,7 +614,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
     const int32_t n = g->n;
     const int fgrid = frontier_grid<D>(g, n);
     unsigned long long* ctr = w.shard_ctr.get();
-    k_sssp_scan_frontier<D><<<fgrid, 256, 0, cs>>>(0, n, g->offsets.get(), dist, prev,
+    k_sssp_scan_frontier<D><<<fgrid, kFBlock, 0, cs>>>(0, n, g->offsets.get(), dist, prev,
                                                    w.shard_queue.get(), ctr);
     auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
             : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
@@ -680,7 +684,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     for (; !use_graph; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
-            k_sssp_scan_frontier<D><<<fgrid, 256, 0, s>>>(0, n, g->offsets.get(), dist, prev,
+            k_sssp_scan_frontier<D><<<fgrid, kFBlock, 0, s>>>(0, n, g->offsets.get(), dist, prev,
                                                           w.shard_queue.get(), ctr);
         });
         GDX_CUDA(cudaMemcpyAsync(h, ctr, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -782,7 +786,7 @@ static void shard_frontier(gdx_graph* g, D* dist, D* prev, int64_t* out, int nou
     GDX_CUDA(cudaMemsetAsync(w.shard_ctr.get() + 3, 0, 2 * sizeof(unsigned long long), s));
     if (cnt > 0)
         timed_launch(g, "sssp_shard_frontier", [&] {
-            k_sssp_scan_frontier<D><<<frontier_grid<D>(g, cnt), 256, 0, s>>>(
+            k_sssp_scan_frontier<D><<<frontier_grid<D>(g, cnt), kFBlock, 0, s>>>(
                 w.shard_v0, w.shard_v1, g->offsets.get(), dist, prev, w.shard_queue.get(),
                 w.shard_ctr.get());
         });
