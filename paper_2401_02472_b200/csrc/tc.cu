@@ -213,7 +213,10 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
     }
 }
 
-constexpr int kTcStage = 512;  // ints of staged N+ lists per warp
+#ifndef GDX_TC_STAGE
+#define GDX_TC_STAGE 512
+#endif
+constexpr int kTcStage = GDX_TC_STAGE;  // ints of staged N+ lists per warp
 
 __global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, int32_t v_end,
                                                           const int32_t* __restrict__ off_plus,
@@ -559,7 +562,7 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
         const int64_t groups = (int64_t(v_end) - v_begin + 31) / 32;
         const char* cap = std::getenv("GDX_TC_GRID_CAP");  // blocks per SM (A/B)
         const int grid = blocks_for(groups * 32, kTcBlock,
-                                    (cap ? std::max(1, std::atoi(cap)) : 64) * g->num_sms);
+                                    (cap ? std::max(1, std::atoi(cap)) : 512) * g->num_sms);
         timed_launch(g, "tc", [&] {
             k_tc_oriented<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, P.off_plus.get(),
                                                     P.adj_plus.get(), P.acc.get());
