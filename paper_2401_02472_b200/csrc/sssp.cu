@@ -665,9 +665,9 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
     const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
     // 16 blocks/SM for small graphs (fewer idle blocks per short round: C1 0.33
-    // vs 0.35 ms), 64 for large ones (C5 23.6 vs 24.6 ms)
+    // vs 0.35 ms), 128 for large ones (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32)
     const int relax_grid =
-        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 64)) * g->num_sms;
+        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 128)) * g->num_sms;
     if (use_graph) {
         const int di = sizeof(D) == 4 ? 0 : 1;
         // the instantiated graph bakes in these buffers
@@ -809,7 +809,7 @@ static void shard_relax(gdx_graph* g, D* dist) {
     auto& w = *g->sssp;
     cudaStream_t s = g->stream;
     // the single-GPU rule (gdx_sssp): deeper grids for large relaxation sets
-    const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 64) * g->num_sms;
+    const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
     timed_launch(g, "sssp_shard_relax", [&] {
         k_sssp_scan_relax<D, 16><<<blocks, 256, 0, s>>>(
             w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
@@ -856,7 +856,7 @@ extern "C" int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t
         }
         SsspDelta dl{w.shard_mark.get(), changed_ids, w.shard_ctr.get() + 5, ++w.shard_round};
         GDX_CUDA(cudaMemsetAsync(dl.count, 0, sizeof(unsigned long long), s));
-        const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 64) * g->num_sms;
+        const int blocks = (w.shard_edges < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
         timed_launch(g, "sssp_shard_relax", [&] {
             k_sssp_scan_relax<int, 16, true><<<blocks, 256, 0, s>>>(
                 w.shard_queue.get(), w.shard_ctr.get(), g->offsets.get(), g->dests.get(),
