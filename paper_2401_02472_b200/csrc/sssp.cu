@@ -470,16 +470,14 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
     }
 }
 
-// Frontier-scan grid: one wave of resident blocks (a second partial wave
-// would double the chunk loop of the blocks in it); GDX_SSSP_FGRID = blocks
-// per SM overrides.
+// Frontier-scan grid: up to 64 blocks per SM (a few chunks each; same-box C5:
+// 21.0 vs 21.35 ms with one resident wave of ~44-chunk blocks);
+// GDX_SSSP_FGRID = blocks per SM overrides.
 template <class D>
 static int frontier_grid(const gdx_graph* g, int64_t cnt) {
     static const int per_sm = [] {
-        if (const char* e = std::getenv("GDX_SSSP_FGRID")) return std::max(1, std::atoi(e));
-        int b = 0;
-        GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sssp_scan_frontier<D>, kFBlock, 0));
-        return std::max(1, b);
+        const char* e = std::getenv("GDX_SSSP_FGRID");
+        return e ? std::max(1, std::atoi(e)) : 64;
     }();
     return blocks_for(cnt, kFBlock * 8, g->num_sms * per_sm);
 }
