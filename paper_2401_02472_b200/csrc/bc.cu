@@ -400,6 +400,7 @@ struct BcCtaArgs {
     bool any_heavy;    // some vertex has more than kHeavy out- (or in-) edges
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
+    int4* kids;        // [grid][n] children of each log entry (low-degree graphs) or nullptr
     double* bc;
     unsigned long long* ctr;
     unsigned long long* trace;  // optional: slot 0's (globaltimer ns, items) per level step
@@ -571,6 +572,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     BcRec* rec = a.rec + slot * a.n;
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
+    int4* kids = a.kids ? a.kids + slot * a.n : nullptr;
     // per-source 32-bit counters (registers are the kernel's limit), flushed
     // to the 64-bit totals after every source
     unsigned fscan = 0, bscan = 0, dag = 0;
@@ -618,14 +620,25 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
                     bool par[kNb], got[kNb];
-                    int32_t w0[kNb], w1[kNb];
+                    int32_t w0[kNb], w1[kNb], lnew[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
                         par[k] = a.undirected && L > 0 && lw[k] == L - 1;
                         const bool cand = lw[k] == -1;
                         w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
                         w1[k] = cand ? a.offsets[w[k] + 1] : 0;
-                        got[k] = cand && atomicCAS(&rec[w[k]].level, -1, L + 1) == -1;
+                        lnew[k] = cand ? atomicCAS(&rec[w[k]].level, -1, L + 1) : lw[k];
+                        got[k] = cand && lnew[k] == -1;
+                    }
+                    if (!HEAVY && a.kids && oe - ob <= kNb) {
+                        // the children of v: neighbours claimed at this level, by v or
+                        // not (a failed CAS returns the claimer's level) -- the
+                        // backward pass reads them here instead of the adjacency
+                        int32_t c[kNb];
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            c[k] = w[k] >= 0 && (got[k] || lnew[k] == L + 1) ? w[k] : -1;
+                        kids[i] = make_int4(c[0], c[1], c[2], c[3]);
                     }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
@@ -659,6 +672,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             }
                     }
                 }
+                if (!HEAVY && a.kids && (oe - ob > kNb || oe == ob))  // scan fallback / none
+                    kids[i] = oe == ob ? make_int4(-1, -1, -1, -1) : make_int4(-2, -2, -2, -2);
                 rec_store_sigma(rec + v, L, acc);
             }
             // heavy items of this CTA: one warp each, lanes stride over the adjacency
@@ -706,6 +721,30 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 XF sv;
                 rec_level_sigma(rec + v, lv, sv);
                 double d = 0.0;
+                const int4 kc = !HEAVY && kids ? kids[i] : make_int4(-2, 0, 0, 0);
+                if (!HEAVY && kc.x != -2) {  // the recorded children, ascending
+                    bscan += oe - ob;  // the adjacency scan this replaces (stats)
+                    const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
+                    int32_t lw[kNb];
+                    XF sw[kNb];
+                    double dw[kNb];
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k) {
+                        lw[k] = -2;
+                        sw[k] = XF{1.0, 0};
+                        dw[k] = 0.0;
+                        if (w[k] >= 0) rec_all(rec + w[k], lw[k], sw[k], dw[k]);
+                    }
+#pragma unroll
+                    for (int k = 0; k < kNb; ++k)
+                        if (w[k] >= 0) {
+                            d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
+                            ++dag;
+                        }
+                    rec[v].delta = d;
+                    if (v != src) atomicAdd(&a.bc[v], d);
+                    continue;
+                }
                 bscan += oe - ob;
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
@@ -760,7 +799,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
 }
 
 static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
-                       unsigned long long* totals, int& launches, int& max_levels) {
+                       unsigned long long* totals, int& launches, int& max_levels,
+                       bool& used_kids) {
     auto& W = *g->bc;
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
@@ -774,15 +814,21 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         while (CS < 4 && int64_t(2 * CS) * std::min<int32_t>(nsrc, g->num_sms) <= g->num_sms) CS *= 2;
     if (CS != 1 && CS != 2 && CS != 4) CS = 1;
     int slots = std::max(1, std::min<int32_t>(nsrc, g->num_sms / CS));
-    // a slot holds 52 B per vertex (record, log entry, level bound): fewer
+    // graphs without heavy vertices record each log entry's children (16 B,
+    // the backward pass then skips the adjacency); GDX_BC_KIDS=0 disables
+    const bool any_heavy = graph_max_degree(g) > kHeavy;
+    const char* kv = std::getenv("GDX_BC_KIDS");
+    const bool a_kids = !any_heavy && !(kv && std::string(kv) == "0");
+    // a slot holds 52 B per vertex (record, log entry, level bound; + 16 B of
+    // children): fewer
     // slots (each then runs several sources) when they would not fit (queried
     // only when the slots have to grow)
     if (W.cta_grid < slots) {
         size_t free_b = 0, tot_b = 0;
         GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
-        const size_t per_slot = size_t(n) * 52 + 8;
-        const size_t held =
-            W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() + pool_cached();
+        const size_t per_slot = size_t(n) * (a_kids ? 68 : 52) + 8;
+        const size_t held = W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() +
+                            W.cta_kids.bytes() + pool_cached();
         const int64_t fit = int64_t(double(free_b + held) * 0.85 / double(per_slot));
         if (fit < 1)
             fail(GDX_ERR_OUT_OF_MEMORY, "OutOfMemory: BC needs " + std::to_string(per_slot) +
@@ -797,6 +843,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.log.release();
         W.cta_log.release();
         W.cta_loff.release();
+        W.cta_kids.release();
         W.batch = 0;
         W.cta_rec.alloc(size_t(slots) * n * 4);  // 32 B BcRec per (slot, vertex)
         W.cta_log.alloc(size_t(slots) * n * 4);  // int4 entries
@@ -804,6 +851,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.cta_grid = slots;
         GDX_CUDA(cudaMemsetAsync(W.cta_rec.get(), 0xff, W.cta_rec.bytes(), s));  // level = -1
     }
+    if (a_kids) W.cta_kids.ensure(size_t(W.cta_grid) * n * 4);  // int4 per (slot, vertex)
     W.sources.ensure(size_t(nsrc));
     GDX_CUDA(cudaMemcpyAsync(W.sources.get(), hsrc.data(), size_t(nsrc) * 4,
                              cudaMemcpyHostToDevice, s));
@@ -818,7 +866,9 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.in_srcs = g->rev_srcs.get();
     a.sources = W.sources.get();
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
-    a.any_heavy = graph_max_degree(g) > kHeavy;
+    a.any_heavy = any_heavy;
+    a.kids = a_kids ? reinterpret_cast<int4*>(W.cta_kids.get()) : nullptr;
+    used_kids = a_kids;
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
@@ -900,6 +950,7 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         GDX_CUDA(cudaMemsetAsync(W.bc.get(), 0, n * sizeof(double), s));
         unsigned long long totals[kBcCtrs] = {};
         int launches = 0, max_levels = 0;
+        bool used_kids = false;
         // CTA-cluster-per-source mode when there are enough sources to fill
         // the GPU with independent BFS trees, or when no vertex has more than
         // kHeavy edges (low-degree, typically high-diameter graphs: barrier
@@ -911,12 +962,13 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
                                    : nsrc >= std::max(16, g->num_sms / 4) ||
                                          (nsrc > 0 && graph_max_degree(g) <= kHeavy);
         if (nsrc > 0 && cta_mode) {
-            run_bc_cta(g, hsrc, totals, launches, max_levels);
+            run_bc_cta(g, hsrc, totals, launches, max_levels, used_kids);
         } else if (nsrc > 0) {
             if (W.cta_grid > 0) {  // switch back from CTA mode: release its buffers
                 W.cta_rec.release();
                 W.cta_log.release();
                 W.cta_loff.release();
+                W.cta_kids.release();
                 W.cta_grid = 0;
                 W.batch = 0;
             }
@@ -1020,6 +1072,10 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             // sigma 16 + discovery log write 8 + level CAS 4; backward log 8 +
             // offsets 8 + sigma 16 + delta 8 + bc RMW 16.  Per scanned edge: dest 4 +
             // level 4.  Per DAG edge use: sigma 16 (+ delta 8 backward ~ 12 avg).
+            // The same algorithmic bytes whether or not the backward pass reads
+            // the recorded children instead of the adjacency (an implementation
+            // choice, not less work).
+            (void)used_kids;
             stats->algorithmic_bytes = 100.0 * totals[kReached] +
                                        8.0 * (totals[kFwdScan] + totals[kBwdScan]) +
                                        28.0 * totals[kDag];

@@ -113,6 +113,7 @@ struct BcWork {
     DevBuf<double> cta_rec;     // [cta_grid][n] x 32 B (level, sigma exp, mantissa, delta)
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
+    DevBuf<int32_t> cta_kids;   // [cta_grid][n] int4: children of each log entry (or -2)
 };
 
 }  // namespace gdx
