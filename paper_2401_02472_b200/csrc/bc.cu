@@ -23,6 +23,7 @@
 //     (the reference's double sigma overflows on large grids).
 //     Where the reference's sigma is finite the quotients are identical.
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -640,14 +641,25 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             c[k] = w[k] >= 0 && (got[k] || lnew[k] == L + 1) ? w[k] : -1;
                         kids[i] = make_int4(c[0], c[1], c[2], c[3]);
                     }
+                    // log positions: one DSMEM atomic per group of converged lanes
+                    // (scan of the claim counts) instead of one per claim
+                    {
+                        cg::coalesced_group act = cg::coalesced_threads();
+                        const int cnt = int(got[0]) + int(got[1]) + int(got[2]) + int(got[3]);
+                        const int excl = cg::exclusive_scan(act, cnt);
+                        const int last = int(act.size()) - 1;
+                        const int tot = act.shfl(excl + cnt, last);
+                        int base = 0;
+                        if (int(act.thread_rank()) == last && tot) base = atomicAdd(&s_next[L % 3], tot);
+                        int pos = end + act.shfl(base, last) + excl;
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) {
-                        if (par[k]) {  // ascending parent order
-                            acc = xf_add(acc, sg[k]);
-                            ++dag;
+                        for (int k = 0; k < kNb; ++k) {
+                            if (par[k]) {  // ascending parent order
+                                acc = xf_add(acc, sg[k]);
+                                ++dag;
+                            }
+                            if (got[k]) log[pos++] = make_int4(w[k], w0[k], w1[k], 0);
                         }
-                        if (got[k])
-                            log[end + atomicAdd(&s_next[L % 3], 1)] = make_int4(w[k], w0[k], w1[k], 0);
                     }
                 }
                 if (!a.undirected && L > 0) {
