@@ -80,6 +80,7 @@ __device__ inline double xf_ratio(double2 a, double2 b) {
 // before any is consumed (dests -> levels -> sigma/delta), so the per-item
 // critical path is a few dependent memory steps instead of one per neighbour.
 constexpr int kNb = 4;
+static_assert(kNb == 4, "the CTA kernel sums and records exactly kNb = 4 neighbour slots");
 
 // Items whose adjacency exceeds kHeavy edges are deferred to a warp-cooperative
 // pass at the end of the block's chunk (lanes stride over the edges, partial
