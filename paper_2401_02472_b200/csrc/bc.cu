@@ -549,7 +549,7 @@ __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec*
         d = warp_sum(d);
         if (lane == 0) {
             rec[v].delta = d;
-            if (v != src) atomicAdd(&a.bc[v], d);
+            if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
         }
     }
 }
@@ -755,7 +755,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             ++dag;
                         }
                     rec[v].delta = d;
-                    if (v != src) atomicAdd(&a.bc[v], d);
+                    if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
                     continue;
                 }
                 bscan += oe - ob;
@@ -780,7 +780,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         }
                 }
                 rec[v].delta = d;
-                if (v != src) atomicAdd(&a.bc[v], d);
+                if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
             }
             if (HEAVY && __syncthreads_count(deferred) > 0) {
                 bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, bscan, dag);
