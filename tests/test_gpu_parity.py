@@ -270,15 +270,19 @@ def test_tc(gdx, port, kind, scale, directed):
 
 # ---- Betweenness centrality ------------------------------------------------------------
 
-@pytest.fixture(params=["grid", "cta", "cta1", "cta2"])
+@pytest.fixture(params=["grid", "cta", "cta1", "cta2", "cta_nokids"])
 def bc_mode(request, monkeypatch):
     """Both BC executions: grid-wide level-synchronous kernels, and one CTA
     cluster per source (the default once there are >= max(16, #SM/4) sources)
-    with the cluster size picked from the SM count, or forced to 1 / 2."""
+    with the cluster size picked from the SM count, or forced to 1 / 2; and the
+    CTA kernel's backward pass scanning the adjacency instead of the children
+    recorded by the forward pass (GDX_BC_KIDS=0)."""
     mode = request.param
     monkeypatch.setenv("GDX_BC_MODE", "grid" if mode == "grid" else "cta")
     if mode in ("cta1", "cta2"):
         monkeypatch.setenv("GDX_BC_CLUSTER", mode[-1])
+    if mode == "cta_nokids":
+        monkeypatch.setenv("GDX_BC_KIDS", "0")
     return mode
 
 
