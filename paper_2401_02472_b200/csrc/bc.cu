@@ -482,7 +482,8 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
 // adjacency).  Out of line so their registers do not weigh on the light path.
 __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* rec, int4* log,
                                                   const int* s_h, int hn, int L, int end,
-                                                  int* s_next, unsigned& fscan,
+                                                  int* s_next, int* const* s_copy, int ncopy,
+                                                  unsigned& fscan,
                                                   unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
@@ -501,8 +502,10 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
             }
             if (lw == -1) {
                 const int32_t w0 = a.offsets[w], w1 = a.offsets[w + 1];
-                if (atomicCAS(&rec[w].level, -1, L + 1) == -1)
+                if (atomicCAS(&rec[w].level, -1, L + 1) == -1) {
                     log[end + atomicAdd(&s_next[L % 3], 1)] = make_int4(w, w0, w1, 0);
+                    for (int q = 0; q < ncopy; ++q) atomicAdd(&s_copy[q][L % 3], 1);
+                }
             }
         }
         if (!a.undirected && L > 0) {
@@ -565,6 +568,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = int(cluster.block_rank());
     int* s_next = cluster.map_shared_rank(s_next_local, 0);
+    // every other CTA keeps a copy of the tails (count-only reds from all
+    // CTAs), so after the barrier each thread reads its own shared memory
+    int* s_copy[CS > 1 ? CS - 1 : 1];
+#pragma unroll
+    for (int q = 1; q < CS; ++q) s_copy[q - 1] = cluster.map_shared_rank(s_next_local, q);
     const int tid = crank * kBcCta + int(threadIdx.x);
     const int ltid = threadIdx.x;
     if (ltid == 0) s_hn = 0;
@@ -587,6 +595,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             loff[0] = 0;
             s_next[0] = s_next[1] = s_next[2] = 0;
         }
+        if (ltid == 0) s_next_local[0] = s_next_local[1] = s_next_local[2] = 0;
         cluster.sync();
         // ---- forward: iterateInBFS ----
         int beg = 0, end = 1, L = 0;
@@ -651,7 +660,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         const int last = int(act.size()) - 1;
                         const int tot = act.shfl(excl + cnt, last);
                         int base = 0;
-                        if (int(act.thread_rank()) == last && tot) base = atomicAdd(&s_next[L % 3], tot);
+                        if (int(act.thread_rank()) == last && tot) {
+                            base = atomicAdd(&s_next[L % 3], tot);
+#pragma unroll
+                            for (int q = 0; q < CS - 1; ++q) atomicAdd(&s_copy[q][L % 3], tot);
+                        }
                         int pos = end + act.shfl(base, last) + excl;
 #pragma unroll
                         for (int k = 0; k < kNb; ++k) {
@@ -692,19 +705,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             // heavy items of this CTA: one warp each, lanes stride over the adjacency
             // (graphs without a vertex above kHeavy skip the extra barrier)
             if (HEAVY && __syncthreads_count(deferred) > 0) {
-                bc_cta_heavy_forward(a, rec, log, s_h, min(s_hn, kBcCta), L, end, s_next, fscan, dag);
+                bc_cta_heavy_forward(a, rec, log, s_h, min(s_hn, kBcCta), L, end, s_next, s_copy,
+                                     CS - 1, fscan, dag);
                 __syncthreads();
                 if (ltid == 0) s_hn = 0;
             }
             // one barrier per level: level L pushes to tail L % 3; the tail of
             // level L+2 (last read right after the previous barrier) is reset now
             cluster.sync();
-            const int next = s_next[L % 3];
+            const int next = s_next_local[L % 3];  // this CTA's copy (CTA 0: the tail itself)
             bc_trace(a, slot, tid, tk, end - beg);
-            if (tid == 0) {
-                s_next[(L + 2) % 3] = 0;
-                loff[L + 1] = end;
-            }
+            if (ltid == 0) s_next_local[(L + 2) % 3] = 0;
+            if (tid == 0) loff[L + 1] = end;
             if (next == 0) break;
             beg = end;
             end += next;
