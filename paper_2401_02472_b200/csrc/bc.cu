@@ -376,7 +376,10 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
 // concurrently with no grid-wide synchronisation at all.  Same arithmetic and
 // summation orders as the grid kernels.
 // ---------------------------------------------------------------------------
-constexpr int kBcCta = 1024;
+#ifndef GDX_BC_CTA
+#define GDX_BC_CTA 1024
+#endif
+constexpr int kBcCta = GDX_BC_CTA;
 
 // Per-(slot, vertex) state of the CTA kernel, packed so one 16 B load returns
 // a neighbour's level and sigma together and one 32 B load adds its delta:
