@@ -148,7 +148,7 @@ __global__ void k_max_degree(int32_t n, const int32_t* __restrict__ off, int32_t
 int32_t graph_max_degree(gdx_graph* g) {
     if (g->max_degree >= 0) return g->max_degree;
     int32_t best = 0;
-    for (const int32_t* off : {g->offsets.get(), g->directed ? g->rev_offsets.get() : nullptr}) {
+    for (const int32_t* off : {static_cast<const int32_t*>(g->offsets.get()), g->directed ? g->in_offsets() : nullptr}) {
         if (!off || g->n == 0) continue;
         DevBuf<int32_t> d(1);
         GDX_CUDA(cudaMemsetAsync(d.get(), 0, 4, g->stream));
@@ -348,8 +348,14 @@ int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* 
                 GDX_CUDA(cudaStreamSynchronize(g->stream));
             }
         }
-        need(rev_offsets, g->rev_offsets, nb, "rev_offsets");
-        need(rev_srcs, g->rev_srcs, mb, "rev_srcs");
+        auto need_ptr = [&](void* dst, const int32_t* src, size_t bytes, const char* what) {
+            if (!dst) return;
+            if (!src && bytes) fail(GDX_ERR_UNSUPPORTED, std::string("Unsupported: graph has no ") + what);
+            copy_out(g, dst, src, bytes);
+        };
+        need_ptr(rev_offsets, g->in_offsets(), nb, "rev_offsets");
+        need_ptr(rev_srcs, g->in_srcs(), mb, "rev_srcs");
+        if (rev_eid && !g->rev_eid.get()) build_rev_eid_symmetric(g);  // undirected: on demand
         need(rev_eid, g->rev_eid, mb, "rev_eid");
         GDX_CUDA(cudaStreamSynchronize(g->stream));
     });

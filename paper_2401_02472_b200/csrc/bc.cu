@@ -890,8 +890,8 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.undirected = !g->directed;
     a.offsets = g->offsets.get();
     a.dests = g->dests.get();
-    a.in_offsets = g->rev_offsets.get();
-    a.in_srcs = g->rev_srcs.get();
+    a.in_offsets = g->in_offsets();
+    a.in_srcs = g->in_srcs();
     a.sources = W.sources.get();
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
     a.any_heavy = any_heavy;
@@ -1045,8 +1045,8 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             a.undirected = !g->directed;
             a.offsets = g->offsets.get();
             a.dests = g->dests.get();
-            a.in_offsets = g->rev_offsets.get();
-            a.in_srcs = g->rev_srcs.get();
+            a.in_offsets = g->in_offsets();
+            a.in_srcs = g->in_srcs();
             a.sources = W.sources.get();
             a.level = W.level.get();
             a.sig = reinterpret_cast<double2*>(W.sig.get());

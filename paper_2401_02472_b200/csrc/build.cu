@@ -185,6 +185,9 @@ void build_reverse_device(gdx_graph* g) {
     const int32_t n = g->n;
     const int64_t m = g->m;
     cudaStream_t s = g->stream;
+    // undirected: the reverse CSR is the forward one (gdx_graph::in_offsets /
+    // in_srcs); the mirror ids are built on demand (build_rev_eid_symmetric)
+    if (!g->directed) return;
     g->rev_offsets.alloc(size_t(n) + 1);
     g->rev_srcs.alloc(m);
     g->rev_eid.alloc(m);
@@ -193,16 +196,6 @@ void build_reverse_device(gdx_graph* g) {
         return;
     }
     if (!g->dests.get()) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no forward adjacency");
-    if (!g->directed) {
-        GDX_CUDA(cudaMemcpyAsync(g->rev_offsets.get(), g->offsets.get(), (size_t(n) + 1) * 4,
-                                 cudaMemcpyDeviceToDevice, s));
-        GDX_CUDA(cudaMemcpyAsync(g->rev_srcs.get(), g->dests.get(), size_t(m) * 4,
-                                 cudaMemcpyDeviceToDevice, s));
-        k_rev_eid_symmetric<<<grid_for(g, int64_t(n) * 32), 256, 0, s>>>(
-            n, g->offsets.get(), g->dests.get(), g->rev_eid.get());
-        GDX_LAUNCH_CHECK();
-        return;
-    }
     const int b = key_bits(n);
     DevBuf<uint64_t> k0(m), k1(m);
     DevBuf<int32_t> e0(m);
@@ -216,6 +209,17 @@ void build_reverse_device(gdx_graph* g) {
     k_low_bits<<<grid_for(g, m), 256, 0, s>>>(m, b, k1.get(), g->rev_srcs.get());
     GDX_LAUNCH_CHECK();
     GDX_CUDA(cudaStreamSynchronize(s));  // temporaries die at scope exit
+}
+
+// rev_eid of an undirected graph (mirror edge ids), on demand.
+void build_rev_eid_symmetric(gdx_graph* g) {
+    if (g->directed || g->rev_eid.get()) return;
+    g->rev_eid.alloc(size_t(g->m));
+    if (g->m == 0) return;
+    if (!g->dests.get()) fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
+    k_rev_eid_symmetric<<<grid_for(g, int64_t(g->n) * 32), 256, 0, g->stream>>>(
+        g->n, g->offsets.get(), g->dests.get(), g->rev_eid.get());
+    GDX_LAUNCH_CHECK();
 }
 
 // Core builder from device-resident edge arrays.

@@ -166,6 +166,16 @@ struct gdx_graph {
     cudaStream_t stream = nullptr;
 
     gdx::DevBuf<int32_t> offsets, dests, weights, rev_offsets, rev_srcs, rev_eid;
+    // The reverse CSR.  An undirected graph is stored symmetrically with sorted
+    // rows, so its reverse CSR *is* the forward one: unless the caller uploaded
+    // reverse arrays, these return the forward arrays (no copy, no memory);
+    // rev_eid is then built on demand (gdx_graph_download).
+    const int32_t* in_offsets() const {
+        return rev_offsets.get() ? rev_offsets.get() : directed ? nullptr : offsets.get();
+    }
+    const int32_t* in_srcs() const {
+        return rev_srcs.get() ? rev_srcs.get() : directed ? nullptr : dests.get();
+    }
 
     gdx::Profiler prof;
     std::unique_ptr<gdx::PrPlan> pr;
@@ -217,6 +227,7 @@ int32_t graph_max_degree(gdx_graph* g);
 
 // Builds the reverse CSR (csr.cpp:77-94 semantics) on the device.
 void build_reverse_device(gdx_graph* g);
+void build_rev_eid_symmetric(gdx_graph* g);
 // Upload / finish a graph whose forward arrays are resident.
 void finalize_graph(gdx_graph* g);
 

@@ -348,13 +348,13 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     const int32_t n = g->n;
     const int32_t cnt = v_end - v_begin;
     int32_t eb[2] = {0, 0};
-    GDX_CUDA(cudaMemcpyAsync(&eb[0], g->rev_offsets.get() + v_begin, 4, cudaMemcpyDeviceToHost, s));
-    GDX_CUDA(cudaMemcpyAsync(&eb[1], g->rev_offsets.get() + v_end, 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(&eb[0], g->in_offsets() + v_begin, 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(&eb[1], g->in_offsets() + v_end, 4, cudaMemcpyDeviceToHost, s));
     const int grid = blocks_for(std::max(cnt, 1), 256, g->num_sms * 16);
     DevBuf<int32_t> flag(std::max(cnt, 1)), pos(std::max(cnt, 1));
     int32_t last[2] = {0, 0};
     if (cnt > 0) {
-        k_pr_nz_flags<<<grid, 256, 0, s>>>(v_begin, cnt, g->rev_offsets.get(), flag.get());
+        k_pr_nz_flags<<<grid, 256, 0, s>>>(v_begin, cnt, g->in_offsets(), flag.get());
         GDX_LAUNCH_CHECK();
         size_t bytes = 0;
         GDX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag.get(), pos.get(), cnt, s));
@@ -372,7 +372,7 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     P.nnz = last[0] + last[1];
     P.nz.alloc(size_t(P.nnz) + 1);
     if (cnt > 0) {
-        k_pr_nz_fill<<<grid, 256, 0, s>>>(v_begin, cnt, g->rev_offsets.get(), pos.get(),
+        k_pr_nz_fill<<<grid, 256, 0, s>>>(v_begin, cnt, g->in_offsets(), pos.get(),
                                           P.nz.get());
         GDX_LAUNCH_CHECK();
     }
@@ -404,8 +404,8 @@ static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshol
     PrArgs a;
     a.n = g->n;
     a.offsets = g->offsets.get();
-    a.rev_offsets = g->rev_offsets.get();
-    a.rev_srcs = g->rev_srcs.get();
+    a.rev_offsets = g->in_offsets();
+    a.rev_srcs = g->in_srcs();
     a.rank0 = P.rank[0].get();
     a.rank1 = P.rank[1].get();
     a.contrib0 = P.contrib[0].get();
@@ -473,7 +473,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         if (!g || !rank_out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
         // pr.sp:9 evaluates 1.0 / numNodes (interpreter.cpp:454-456 raises on 0).
         if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
-        if (!g->rev_offsets.get() || !g->rev_srcs.get())
+        if (!g->in_offsets() || !g->in_srcs())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
         DeviceGuard dg(g->device);
         cudaStream_t s = g->stream;
@@ -559,7 +559,7 @@ extern "C" int gdx_pr_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end) 
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
         if (v_begin < 0 || v_end > g->n || v_begin > v_end)
             fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex range out of bounds");
-        if (!g->rev_offsets.get() || !g->rev_srcs.get())
+        if (!g->in_offsets() || !g->in_srcs())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
         DeviceGuard dg(g->device);
         g->pr_shard = std::make_unique<PrPlan>();
