@@ -61,8 +61,9 @@ typedef struct gdx_graph gdx_graph;
  * weights may be NULL (all 1).  rev_* may be NULL: the reverse CSR is then
  * rebuilt on the device with csr.cpp:77-94 semantics (a sort for directed
  * graphs; undirected graphs are stored symmetrically by CsrGraph, csr.cpp:42-45,
- * so their reverse arrays are copies of the forward ones plus the mirror edge
- * ids).  dests may be NULL only when rev_offsets/rev_srcs are given
+ * so their reverse arrays equal the forward ones: the handle reads the forward
+ * arrays and builds the mirror edge ids only when gdx_graph_download asks for
+ * rev_eid).  dests may be NULL only when rev_offsets/rev_srcs are given
  * (PageRank-only graphs). */
 typedef struct {
     int32_t n;
