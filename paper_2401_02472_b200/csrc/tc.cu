@@ -23,7 +23,10 @@
 
 namespace gdx {
 
-constexpr int kTcBlock = 256;
+#ifndef GDX_TC_BLOCK
+#define GDX_TC_BLOCK 128  // same-box C3: 4.80 vs 4.86 ms at 256, 4.99 at 512
+#endif
+constexpr int kTcBlock = GDX_TC_BLOCK;
 // degree binning: a vertex with more (oriented) neighbours than this has its
 // pairs spread over the whole grid (k_tc_heavy / k_tc_heavy_mid)
 constexpr int kTcHeavy = 256;
@@ -218,7 +221,7 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
 #endif
 constexpr int kTcStage = GDX_TC_STAGE;  // ints of staged N+ lists per warp
 
-__global__ void __launch_bounds__(kTcBlock, 6) k_tc_oriented(int32_t v_begin, int32_t v_end,
+__global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
                                                           const int32_t* __restrict__ off_plus,
                                                           const int32_t* __restrict__ adj,
                                                           unsigned long long* acc) {
