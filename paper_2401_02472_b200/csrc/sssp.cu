@@ -362,7 +362,10 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
 // with an element-wise MIN all-reduce (distributed.py sharded_sssp).
 // ---------------------------------------------------------------------------
 constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-cooperatively
-constexpr int kShardChunk = 64;  // edges per relaxation item (C5: 23.7 ms vs 26.1 at 128, 25.6 at 32)
+#ifndef GDX_SSSP_CHUNK
+#define GDX_SSSP_CHUNK 64
+#endif
+constexpr int kShardChunk = GDX_SSSP_CHUNK;  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
 
 // Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
 // distance dropped since they were last expanded (dist < prev; prev := dist).
