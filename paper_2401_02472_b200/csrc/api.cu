@@ -21,6 +21,9 @@ gdx_graph::~gdx_graph() {
     sssp.reset();
     tc.reset();
     bc.reset();
+    // the CSR goes back to the pool while the stream its release is ordered on
+    // still exists
+    for (auto* b : {&offsets, &dests, &weights, &rev_offsets, &rev_srcs, &rev_eid}) b->release();
     if (pinned) gdx::pinned_free(pinned);
     if (own_stream) cudaStreamDestroy(own_stream);
 }
@@ -28,10 +31,21 @@ gdx_graph::~gdx_graph() {
 namespace gdx {
 
 // ---- device memory pool ------------------------------------------------------
+// Stream-ordered caching: a block released inside a GraphScope records an event
+// on that handle's stream instead of synchronising the device; the next user
+// of the block makes its own stream wait for that event (or, outside any
+// scope, waits on the host).  Distinct handles on distinct streams therefore
+// never stall each other through the pool.
 namespace {
+struct Block {
+    int device;
+    void* ptr;
+    cudaEvent_t ready;  // released-at point on the releasing stream (or null)
+};
 struct Pool {
     std::mutex mu;
-    std::multimap<size_t, std::pair<int, void*>> free;  // bytes -> (device, ptr)
+    std::multimap<size_t, Block> free;  // bytes -> block
+    std::multimap<int, cudaEvent_t> events;  // device -> spare event
     size_t cached = 0;
 };
 Pool& pool() {
@@ -39,23 +53,46 @@ Pool& pool() {
     return *p;
 }
 constexpr size_t kPoolCap = size_t(48) << 30;  // cached bytes kept per process
+thread_local cudaStream_t t_stream = nullptr;
+thread_local bool t_stream_set = false;
 }  // namespace
+
+StreamScope::StreamScope(cudaStream_t s) : prev(t_stream), prev_set(t_stream_set) {
+    t_stream = s;
+    t_stream_set = true;
+}
+StreamScope::~StreamScope() {
+    t_stream = prev;
+    t_stream_set = prev_set;
+}
 
 void* pool_alloc(size_t bytes, size_t* got) {
     int dev = 0;
     GDX_CUDA(cudaGetDevice(&dev));
     auto& P = pool();
+    Block hit{-1, nullptr, nullptr};
     {
         std::lock_guard<std::mutex> lk(P.mu);
         const size_t hi = bytes + bytes / 4 + (size_t(2) << 20);
         for (auto it = P.free.lower_bound(bytes); it != P.free.end() && it->first <= hi; ++it)
-            if (it->second.first == dev) {
-                void* p = it->second.second;
+            if (it->second.device == dev) {
+                hit = it->second;
                 *got = it->first;
                 P.cached -= it->first;
                 P.free.erase(it);
-                return p;
+                break;
             }
+    }
+    if (hit.ptr) {
+        if (hit.ready) {
+            if (t_stream_set)
+                GDX_CUDA(cudaStreamWaitEvent(t_stream, hit.ready, 0));
+            else
+                GDX_CUDA(cudaEventSynchronize(hit.ready));
+            std::lock_guard<std::mutex> lk(P.mu);
+            P.events.emplace(dev, hit.ready);
+        }
+        return hit.ptr;
     }
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
@@ -73,14 +110,31 @@ void pool_free(void* p, size_t bytes) {
     if (!p) return;
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceSynchronize();  // no kernel may still use the block (cudaFree's guarantee)
     auto& P = pool();
+    cudaEvent_t ev = nullptr;
+    if (t_stream_set) {
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            auto it = P.events.find(dev);
+            if (it != P.events.end()) {
+                ev = it->second;
+                P.events.erase(it);
+            }
+        }
+        if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) ev = nullptr;
+        if (ev && cudaEventRecord(ev, t_stream) != cudaSuccess) {
+            cudaEventDestroy(ev);
+            ev = nullptr;
+        }
+    }
+    if (!ev) cudaDeviceSynchronize();  // outside any scope: cudaFree's guarantee
     std::lock_guard<std::mutex> lk(P.mu);
     if (P.cached + bytes > kPoolCap) {
-        cudaFree(p);
+        cudaFree(p);  // synchronises
+        if (ev) P.events.emplace(dev, ev);
         return;
     }
-    P.free.emplace(bytes, std::make_pair(dev, p));
+    P.free.emplace(bytes, Block{dev, p, ev});
     P.cached += bytes;
 }
 
@@ -127,11 +181,17 @@ size_t pool_trim() {
     int cur = 0;
     cudaGetDevice(&cur);
     for (auto& kv : P.free) {
-        cudaSetDevice(kv.second.first);
-        cudaFree(kv.second.second);
+        cudaSetDevice(kv.second.device);
+        cudaFree(kv.second.ptr);
+        if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+    }
+    for (auto& kv : P.events) {
+        cudaSetDevice(kv.first);
+        cudaEventDestroy(kv.second);
     }
     cudaSetDevice(cur);
     P.free.clear();
+    P.events.clear();
     P.cached = 0;
     return n;
 }
@@ -225,6 +285,51 @@ __global__ void k_max_weight(const int32_t* __restrict__ w, int64_t m, int32_t* 
     }
 }
 
+// An undirected CsrGraph stores every edge both ways (csr.cpp:42-45) and the
+// handle reads its forward arrays as the reverse CSR; a view that claims
+// directed = 0 with asymmetric rows is rejected.  One warp per vertex u, lanes
+// over N(u), a binary search for u in N(v).
+__global__ void k_check_symmetric(int32_t n, const int32_t* __restrict__ off,
+                                  const int32_t* __restrict__ dst, int64_t* bad) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n;
+         u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t b = off[u], e = off[u + 1];
+        for (int32_t i = b + lane; i < e; i += 32) {
+            const int32_t v = dst[i];
+            bool found = false;
+            if (v >= 0 && v < n) {
+                int32_t lo = off[v], hi = off[v + 1];
+                while (lo < hi) {
+                    const int32_t mid = lo + ((hi - lo) >> 1);
+                    const int32_t x = dst[mid];
+                    if (x == int32_t(u)) { found = true; break; }
+                    if (x < int32_t(u)) lo = mid + 1; else hi = mid;
+                }
+            }
+            if (!found) atomicCAS(reinterpret_cast<unsigned long long*>(bad), ~0ull,
+                                  (unsigned long long)(int64_t(u) << 32 | uint32_t(v)));
+        }
+    }
+}
+
+static void check_symmetric(gdx_graph* g) {
+    if (g->directed || g->m == 0 || !g->dests.get()) return;
+    DevBuf<int64_t> bad(1);
+    GDX_CUDA(cudaMemsetAsync(bad.get(), 0xff, 8, g->stream));
+    k_check_symmetric<<<blocks_for(int64_t(g->n) * 32, 256, g->num_sms * 16), 256, 0, g->stream>>>(
+        g->n, g->offsets.get(), g->dests.get(), bad.get());
+    GDX_LAUNCH_CHECK();
+    int64_t h = -1;
+    GDX_CUDA(cudaMemcpyAsync(&h, bad.get(), 8, cudaMemcpyDeviceToHost, g->stream));
+    GDX_CUDA(cudaStreamSynchronize(g->stream));
+    if (h != -1)
+        fail(GDX_ERR_INVALID_ARGUMENT,
+             "InvalidArgument: undirected graph is not stored symmetrically (edge " +
+                 std::to_string(h >> 32) + " -> " + std::to_string(int32_t(h & 0xffffffff)) +
+                 " has no mirror)");
+}
+
 // Computes max_weight (SSSP chooses 32- or 64-bit distances from it) and
 // rejects negative weights (csr.cpp:36-39 NegativeWeight).
 void finalize_graph(gdx_graph* g) {
@@ -265,7 +370,7 @@ int gdx_graph_create(const gdx_csr_view* v, int device, gdx_graph** out) {
         if (!v->dests && !has_rev)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: dests or rev_offsets/rev_srcs required");
         std::unique_ptr<gdx_graph> g(make_graph(device));
-        DeviceGuard dg(device);
+        GraphScope dg(g.get());
         g->n = v->n;
         g->m = v->m;
         g->directed = v->directed != 0;
@@ -291,9 +396,10 @@ int gdx_graph_create(const gdx_csr_view* v, int device, gdx_graph** out) {
                 g->rev_eid.alloc(v->m);
                 GDX_CUDA(cudaMemcpyAsync(g->rev_eid.get(), v->rev_eid, mb, cudaMemcpyDefault, s));
             }
-        } else {
+        } else if (g->directed) {
             build_reverse_device(g.get());
         }
+        check_symmetric(g.get());
         finalize_graph(g.get());
         GDX_CUDA(cudaStreamSynchronize(s));
         *out = g.release();
@@ -310,7 +416,7 @@ int gdx_pool_trim(int64_t* released_bytes) {
 int gdx_graph_destroy(gdx_graph* g) {
     return guard_impl([&] {
         if (!g) return;
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         cudaStreamSynchronize(g->stream);
         delete g;
     });
@@ -329,7 +435,7 @@ int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* 
                        int32_t* rev_offsets, int32_t* rev_srcs, int32_t* rev_eid) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         const size_t nb = (size_t(g->n) + 1) * 4, mb = size_t(g->m) * 4;
         auto need = [&](void* dst, const DevBuf<int32_t>& b, size_t bytes, const char* what) {
             if (!dst) return;
@@ -364,7 +470,7 @@ int gdx_graph_download(gdx_graph* g, int32_t* offsets, int32_t* dests, int32_t* 
 int gdx_graph_set_stream(gdx_graph* g, void* stream) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         GDX_CUDA(cudaStreamSynchronize(g->stream));
         g->stream = stream ? static_cast<cudaStream_t>(stream) : g->own_stream;
     });
@@ -387,7 +493,7 @@ int gdx_profile_enable(gdx_graph* g, int enable) {
 int gdx_profile_reset(gdx_graph* g) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         g->prof.drain();
         g->prof.totals.clear();
     });
@@ -397,7 +503,7 @@ int gdx_profile_read(gdx_graph* g, char* names, double* ms, int64_t* launches, i
                      int32_t* count) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         g->prof.drain();
         int32_t i = 0;
         for (auto& kv : g->prof.totals) {

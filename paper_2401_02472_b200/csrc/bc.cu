@@ -968,7 +968,7 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         if (!g->dests.get() && g->m > 0)
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
         if (g->n == 0) return;
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         cudaStream_t s = g->stream;
         if (!g->bc) g->bc = std::make_unique<BcWork>();
         auto& W = *g->bc;

@@ -417,7 +417,7 @@ int gdx_graph_build_from_edges(int32_t n, int64_t nedges, const int32_t* u, cons
         if (nedges < 0 || (nedges > 0 && (!u || !v)))
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad edge arrays");
         std::unique_ptr<gdx_graph> g(make_graph(device));
-        DeviceGuard dg(device);
+        GraphScope dg(g.get());
         cudaStream_t s = g->stream;
         // Stage host inputs on the device (device inputs are used in place).
         auto on_device = [](const void* p) {
@@ -460,7 +460,7 @@ int gdx_graph_generate(const gdx_gen_params* p, int device, gdx_graph** out) {
     return guard_impl([&] {
         if (!p || !out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
         std::unique_ptr<gdx_graph> g(make_graph(device));
-        DeviceGuard dg(device);
+        GraphScope dg(g.get());
         cudaStream_t s = g->stream;
         DevBuf<int32_t> u, v;
         int64_t E = 0;
@@ -535,7 +535,7 @@ int gdx_graph_set_hash_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t se
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
         if (!g->dests.get() && g->m > 0)
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         set_hash_weights(g, lo, hi, seed);
         GDX_CUDA(cudaStreamSynchronize(g->stream));
     });

@@ -50,9 +50,20 @@ struct DeviceGuard {
 
 // Device memory pool (api.cu): freed blocks are kept per device and handed
 // back to allocations of similar size, so repeated graph create/destroy
-// cycles (the C-ABI e2e path) do not pay cudaMalloc/cudaFree.  pool_free
-// synchronises the device first (the guarantee cudaFree gives), and an
-// allocation that fails releases the cache and retries.
+// cycles (the C-ABI e2e path) do not pay cudaMalloc/cudaFree.  Inside a
+// StreamScope (every entry point that holds a graph opens one) a release is
+// stream-ordered: it records an event on the scope's stream and the block's
+// next user waits for it on its own stream; outside any scope a release
+// synchronises the device (cudaFree's guarantee).  An allocation that fails
+// releases the cache and retries.
+struct StreamScope {
+    cudaStream_t prev;
+    bool prev_set;
+    explicit StreamScope(cudaStream_t s);
+    ~StreamScope();
+    StreamScope(const StreamScope&) = delete;
+    StreamScope& operator=(const StreamScope&) = delete;
+};
 void* pool_alloc(size_t bytes, size_t* got);
 void pool_free(void* p, size_t bytes);
 size_t pool_trim();
@@ -192,6 +203,14 @@ struct gdx_graph {
 };
 
 namespace gdx {
+
+// The device and stream scope of an entry point working on graph g: sets the
+// thread's device and makes pool releases stream-ordered on g's stream.
+struct GraphScope {
+    DeviceGuard dev;
+    StreamScope str;
+    explicit GraphScope(gdx_graph* g) : dev(g->device), str(g->stream) {}
+};
 
 // Launch helper: brackets a kernel launch with profiler events.
 template <class F>

@@ -34,6 +34,8 @@
 namespace gdx {
 
 constexpr int kPrBlock = 256;
+constexpr int32_t kFlagRing = 256;  // per-round vote slots (a ring; see clear_flags)
+__host__ __device__ inline int32_t flag_slot(int32_t round) { return round & (kFlagRing - 1); }
 
 struct PrArgs {
     int32_t n;
@@ -68,7 +70,7 @@ struct PrArgs {
 
 __device__ inline bool round_skipped(const PrArgs& a, int round) {
     return !a.shard && round > 0 &&
-           *reinterpret_cast<const volatile int32_t*>(&a.flags[round - 1]) == 0;
+           *reinterpret_cast<const volatile int32_t*>(&a.flags[flag_slot(round - 1)]) == 0;
 }
 
 template <int BLOCK = kPrBlock>
@@ -79,7 +81,7 @@ __device__ inline void block_flush(const PrArgs& a, int round, double dang_local
     int any = __syncthreads_or(unsettled);
     if (threadIdx.x == 0) {
         if (tot != 0.0) atomicAdd(&a.dangling[(round + 1) % 3], tot);
-        if (any) atomicOr(&a.flags[round], 1);
+        if (any) atomicOr(&a.flags[flag_slot(round)], 1);
     }
 }
 
@@ -399,8 +401,23 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
 
 static void build_plan(gdx_graph* g) { build_edge_plan(g, *g->pr, 0, g->n); }
 
+// The per-round "unsettled" votes live in a ring of kFlagRing slots (a round
+// reads only its predecessor's slot; the host reads a batch of at most
+// kFlagRing / 2 rounds after it completes), so maxIter does not size memory.
+static void clear_flags(PrPlan& P, int64_t first, int64_t count, cudaStream_t s) {
+    P.flags.ensure(kFlagRing);
+    while (count > 0) {
+        const int32_t slot = flag_slot(int32_t(first));
+        const int64_t run = std::min<int64_t>(count, kFlagRing - slot);
+        GDX_CUDA(cudaMemsetAsync(P.flags.get() + slot, 0, size_t(run) * 4, s));
+        first += run;
+        count -= run;
+    }
+}
+
 static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshold,
                         int32_t max_iter) {
+    P.flags.ensure(kFlagRing);
     PrArgs a;
     a.n = g->n;
     a.offsets = g->offsets.get();
@@ -460,7 +477,7 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_shard_init(PrArgs a, double* pa
 __global__ void k_pr_shard_partials(const double* dangling, const int32_t* flags, int round,
                                     double* partials) {
     partials[0] = dangling[(round + 1) % 3];
-    partials[1] = flags[round] ? 1.0 : 0.0;
+    partials[1] = flags[flag_slot(round)] ? 1.0 : 0.0;
 }
 
 }  // namespace gdx
@@ -475,7 +492,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
         if (!g->in_offsets() || !g->in_srcs())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         cudaStream_t s = g->stream;
         if (!g->pr) {
             g->pr = std::make_unique<PrPlan>();
@@ -487,13 +504,8 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         const int64_t cap = 10 * int64_t(g->n) + 100;
         const int64_t want = max_iter >= 0 ? int64_t(max_iter) + 1 : 1;
         const int64_t limit = std::min(want, cap);
-        if (P.flags_cap < limit) {
-            P.flags.alloc(size_t(limit));
-            P.flags_cap = int32_t(limit);
-        }
         PrArgs a = make_args(g, P, damping, threshold, max_iter);
 
-        GDX_CUDA(cudaMemsetAsync(P.flags.get(), 0, size_t(limit) * 4, s));
         GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
         int launches = 0;
         timed_launch(g, "pr_init", [&] {
@@ -504,6 +516,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         int64_t r = 0, rounds = -1, batch = 4;
         while (rounds < 0) {
             const int64_t lim = std::min(r + batch, limit);
+            clear_flags(P, r, lim - r, s);
             for (int64_t rr = r; rr < lim; ++rr) {
                 if (P.ngroups > 0)
                     timed_launch(g, "pr_edges", [&] {
@@ -516,10 +529,10 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
                 launches += 1 + (P.ngroups > 0);
             }
             const int64_t cnt = lim - r;
-            GDX_CUDA(cudaMemcpyAsync(hflags, P.flags.get() + r, cnt * 4, cudaMemcpyDeviceToHost, s));
+            GDX_CUDA(cudaMemcpyAsync(hflags, P.flags.get(), kFlagRing * 4, cudaMemcpyDeviceToHost, s));
             GDX_CUDA(cudaStreamSynchronize(s));
             for (int64_t i = 0; i < cnt; ++i)
-                if (hflags[i] == 0) {
+                if (hflags[flag_slot(int32_t(r + i))] == 0) {
                     rounds = r + i + 1;
                     break;
                 }
@@ -561,7 +574,7 @@ extern "C" int gdx_pr_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end) 
             fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex range out of bounds");
         if (!g->in_offsets() || !g->in_srcs())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         g->pr_shard = std::make_unique<PrPlan>();
         g->pr_shard->shard = true;
         build_edge_plan(g, *g->pr_shard, v_begin, v_end);
@@ -573,7 +586,7 @@ extern "C" int gdx_pr_shard_init(gdx_graph* g, double* contrib_slice, double* pa
     return guard_impl([&] {
         if (!g || !g->pr_shard) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
         if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         cudaStream_t s = g->stream;
         PrArgs a = make_args(g, P, 0.85, 0.0, 0);
@@ -596,21 +609,15 @@ extern "C" int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, d
     return guard_impl([&] {
         if (!g || !g->pr_shard) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
         if (round < 0) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: negative round");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         cudaStream_t s = g->stream;
-        if (P.flags_cap < round + 1) {
-            const int32_t cap = std::max(round + 1, 2 * P.flags_cap);
-            DevBuf<int32_t> nf(cap);
-            P.flags = std::move(nf);
-            P.flags_cap = cap;
-        }
         PrArgs a = make_args(g, P, damping, threshold, max_iter);
         a.contrib0 = a.contrib1 = const_cast<double*>(contrib_in);
         a.contrib_slice = contrib_slice;
         GDX_CUDA(cudaMemcpyAsync(P.dangling.get() + round % 3, dangling_in, sizeof(double),
                                  cudaMemcpyDefault, s));
-        GDX_CUDA(cudaMemsetAsync(P.flags.get() + round, 0, 4, s));
+        clear_flags(P, round, 1, s);
         if (P.ngroups > 0)
             timed_launch(g, "pr_edges", [&] {
                 k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round);
@@ -629,7 +636,7 @@ extern "C" int gdx_pr_shard_rank(gdx_graph* g, int32_t rounds, double* rank_slic
     return guard_impl([&] {
         if (!g || !g->pr_shard || !rank_slice)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         copy_out(g, rank_slice, P.rank[rounds & 1].get() + P.v_begin,
                  size_t(P.v_end - P.v_begin) * sizeof(double));
@@ -718,7 +725,7 @@ extern "C" int gdx_pr_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, void*
     return guard_impl([&] {
         if (!g || !g->pr_shard || !handle_out || world < 1 || rank < 0 || rank >= world)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad p2p setup (call gdx_pr_shard_setup first)");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto X = std::make_unique<PrP2P>();
         X->world = world;
         X->rank = rank;
@@ -735,7 +742,7 @@ extern "C" int gdx_pr_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, void*
 extern "C" int gdx_pr_p2p_open(gdx_graph* g, const void* handles) {
     return guard_impl([&] {
         if (!g || !g->pr_p2p || !handles) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p setup");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& X = *g->pr_p2p;
         X.bases.assign(X.world, nullptr);
         for (int q = 0; q < X.world; ++q) {
@@ -796,7 +803,7 @@ extern "C" int gdx_pr_p2p_init(gdx_graph* g, double* partials_out) {
         if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !partials_out)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
         if (g->n == 0) fail(GDX_ERR_RUNTIME, "RuntimeError: division by zero");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         auto& X = *g->pr_p2p;
         cudaStream_t s = g->stream;
@@ -829,16 +836,10 @@ extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, dou
         if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !partials_out)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
         if (round < 0) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: negative round");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         auto& X = *g->pr_p2p;
         cudaStream_t s = g->stream;
-        if (P.flags_cap < round + 1) {
-            const int32_t cap = std::max(round + 1, 2 * P.flags_cap);
-            DevBuf<int32_t> nf(cap);
-            P.flags = std::move(nf);
-            P.flags_cap = cap;
-        }
         const int64_t j = X.publishes;  // this round's publish; it reads publish j-1
         PrArgs a = make_args(g, P, damping, threshold, max_iter);
         a.contrib0 = a.contrib1 = X.own_contrib(int((j - 1) & 1));
@@ -846,7 +847,7 @@ extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, dou
         a.npeers = X.world;
         GDX_CUDA(cudaMemcpyAsync(P.dangling.get() + round % 3, &dangling_in, sizeof(double),
                                  cudaMemcpyHostToDevice, s));
-        GDX_CUDA(cudaMemsetAsync(P.flags.get() + round, 0, 4, s));
+        clear_flags(P, round, 1, s);
         k_p2p_wait<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)j * X.world, X.err.get());
         GDX_LAUNCH_CHECK();
         if (P.ngroups > 0)
@@ -856,7 +857,7 @@ extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, dou
                                              g->num_sms * 8),
                                   kPrBlock, 0, s>>>(a, round);
         });
-        k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + round,
+        k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + flag_slot(round),
                                       X.peer_slot.get() + (j & 1) * X.world, X.peer_ctr.get(),
                                       X.world);
         GDX_LAUNCH_CHECK();
@@ -872,27 +873,19 @@ extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, dou
         if (!g || !g->pr_shard || !g->pr_p2p || g->pr_p2p->bases.empty() || !settled_out)
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no p2p plan");
         if (first < 0 || count < 1) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad round range");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& P = *g->pr_shard;
         auto& X = *g->pr_p2p;
         cudaStream_t s = g->stream;
         const int32_t last = first + count;
-        if (P.flags_cap < last) {
-            const int32_t cap = std::max(last, 2 * P.flags_cap);
-            DevBuf<int32_t> nf(cap);
-            if (first > 0 && P.flags.get()) {  // earlier rounds' votes decide skipping
-                GDX_CUDA(cudaMemcpyAsync(nf.get(), P.flags.get(), size_t(first) * 4,
-                                         cudaMemcpyDeviceToDevice, s));
-                GDX_CUDA(cudaStreamSynchronize(s));  // before the old block returns to the pool
-            }
-            P.flags = std::move(nf);
-            P.flags_cap = cap;
-        }
+        if (count > kFlagRing / 2)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: at most " +
+                                               std::to_string(kFlagRing / 2) + " rounds per call");
         if (first == 0) {  // round 0's dangling mass comes from gdx_pr_p2p_init
             GDX_CUDA(cudaMemcpyAsync(P.dangling.get(), &dangling_in, sizeof(double),
                                      cudaMemcpyHostToDevice, s));
         }
-        GDX_CUDA(cudaMemsetAsync(P.flags.get() + first, 0, size_t(count) * 4, s));
+        clear_flags(P, first, count, s);
         for (int32_t round = first; round < last; ++round) {
             const int64_t j = X.publishes;
             PrArgs a = make_args(g, P, damping, threshold, max_iter);
@@ -907,26 +900,26 @@ extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, dou
                                                  g->num_sms * 8),
                                       kPrBlock, 0, s>>>(a, round);
             });
-            k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + round,
+            k_p2p_publish<<<1, 1, 0, s>>>(P.dangling.get() + (round + 1) % 3, P.flags.get() + flag_slot(round),
                                           X.peer_slot.get() + (j & 1) * X.world, X.peer_ctr.get(),
                                           X.world);
             GDX_LAUNCH_CHECK();
             k_p2p_combine<<<1, 1, 0, s>>>(X.own_ctr(), (unsigned long long)(j + 1) * X.world,
                                           X.err.get(), X.own_partials(int(j & 1)), X.world,
-                                          P.dangling.get() + (round + 1) % 3, P.flags.get() + round);
+                                          P.dangling.get() + (round + 1) % 3, P.flags.get() + flag_slot(round));
             GDX_LAUNCH_CHECK();
             X.publishes = j + 1;
         }
-        std::vector<int32_t> votes(static_cast<size_t>(count));
+        std::vector<int32_t> ring(kFlagRing);
         int herr = 0;
-        GDX_CUDA(cudaMemcpyAsync(votes.data(), P.flags.get() + first, size_t(count) * 4,
+        GDX_CUDA(cudaMemcpyAsync(ring.data(), P.flags.get(), kFlagRing * 4,
                                  cudaMemcpyDeviceToHost, s));
         GDX_CUDA(cudaMemcpyAsync(&herr, X.err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
         GDX_CUDA(cudaStreamSynchronize(s));
         if (herr) fail(GDX_ERR_CUDA, "CudaError: peer-memory exchange timed out");
         *settled_out = -1;
         for (int32_t i = 0; i < count; ++i)
-            if (votes[size_t(i)] == 0) {
+            if (ring[size_t(flag_slot(first + i))] == 0) {
                 *settled_out = first + i;
                 break;
             }
@@ -936,7 +929,7 @@ extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, dou
 extern "C" int gdx_pr_p2p_close(gdx_graph* g) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         GDX_CUDA(cudaStreamSynchronize(g->stream));
         g->pr_p2p.reset();
     });

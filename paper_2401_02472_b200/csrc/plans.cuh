@@ -16,7 +16,7 @@ gdx_graph* make_graph(int device);
 struct PrPlan {
     DevBuf<double> rank[2], contrib[2];
     DevBuf<double> dangling;              // 3 rotating accumulators
-    DevBuf<int32_t> flags;                // per-round "unsettled" votes
+    DevBuf<int32_t> flags;                // per-round "unsettled" votes (ring, pagerank.cu)
     // edge-aligned two-pass plan
     int32_t nnz = 0;
     DevBuf<int2> nz;                      // non-empty rows of the reverse CSR: (vertex, end)
@@ -26,7 +26,6 @@ struct PrPlan {
     int64_t e_begin = 0, e_end = 0, e_base = 0, ngroups = 0;
     bool shard = false;                   // built by gdx_pr_shard_setup
     DevBuf<double> partials;              // shard: [dangling partial, unsettled]
-    int32_t flags_cap = 0;
     int grid = 0;
     int block = 256;
 };
@@ -74,8 +73,9 @@ struct SsspWork {
     DevBuf<int32_t> shard_mark;  // delta mode: round in which a vertex was last listed as changed
     int32_t shard_round = 0;
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
+    static constexpr int kKey = 9;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    void* gkey[2][5] = {};
+    void* gkey[2][kKey] = {};
     DevBuf<unsigned long long> graph_acc;  // [rounds, vertices, edges, overflow]
     ~SsspWork() {
         for (auto& e : gexec)
@@ -92,6 +92,8 @@ struct TcPlan {
     DevBuf<int32_t> off_plus;  // oriented CSR (undirected graphs): N+(v) = N(v) ∩ (v, inf)
     DevBuf<int32_t> adj_plus;
     DevBuf<uint8_t> scan_tmp;
+    bool oriented = false;     // off+/adj+ built (once per handle: the graph is immutable)
+    double survey_pairs = 0;   // sum over oriented edges of d+(u) + d+(v)
 };
 
 // BC batched Brandes workspace (bc.cu).

@@ -366,6 +366,8 @@ constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-co
 #define GDX_SSSP_CHUNK 64
 #endif
 constexpr int kShardChunk = GDX_SSSP_CHUNK;  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
+// every relaxation kernel splits an item over LPI in {8, 16, 32} lanes
+static_assert(kShardChunk % 32 == 0 && kShardChunk >= 32, "GDX_SSSP_CHUNK must be a multiple of 32");
 
 // Frontier scan: queue relaxation items of the vertices in [v0, v1) whose
 // distance dropped since they were last expanded (dist < prev; prev := dist).
@@ -513,7 +515,8 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
         const int2 it = queue[i];
         const D dv = dist[it.x];
-        const int32_t e1 = min(it.y + kShardChunk, offsets[it.x + 1]);
+        // int64: it.y + kShardChunk passes INT32_MAX on the last items of m ~ 2^31 graphs
+        const int32_t e1 = int32_t(min(int64_t(it.y) + kShardChunk, int64_t(offsets[it.x + 1])));
         int32_t u[kU];
         D c[kU], du[kU];
 #pragma unroll
@@ -671,14 +674,18 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 128)) * g->num_sms;
     if (use_graph) {
         const int di = sizeof(D) == 4 ? 0 : 1;
-        // the instantiated graph bakes in these buffers
-        void* key[5] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get()};
+        // the instantiated graph bakes in these buffers and the CSR arrays
+        // (gdx_graph_set_hash_weights reallocates / enables the weights)
+        void* key[SsspWork::kKey] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get(),
+                                     g->offsets.get(), g->dests.get(),
+                                     g->weighted ? g->weights.get() : nullptr,
+                                     reinterpret_cast<void*>(intptr_t(lpi * 65536 + relax_grid))};
         bool same = w.gexec[di] != nullptr;
-        for (int i = 0; i < 5; ++i) same = same && w.gkey[di][i] == key[i];
+        for (int i = 0; i < SsspWork::kKey; ++i) same = same && w.gkey[di][i] == key[i];
         if (!same) {
             if (w.gexec[di]) cudaGraphExecDestroy(w.gexec[di]);
             w.gexec[di] = build_sssp_graph<D>(g, dist, prev, ovf_flag, lpi, relax_grid);
-            for (int i = 0; i < 5; ++i) w.gkey[di][i] = key[i];
+            for (int i = 0; i < SsspWork::kKey; ++i) w.gkey[di][i] = key[i];
         }
         timed_launch(g, "sssp_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.gexec[di], s)); });
     }
@@ -753,7 +760,7 @@ extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end
             fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex range out of bounds");
         if (!g->dests.get() && g->m > 0)
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
         auto& w = *g->sssp;
         int32_t eb[2] = {0, 0};
@@ -779,7 +786,7 @@ static void shard_frontier(gdx_graph* g, D* dist, D* prev, int64_t* out, int nou
     const int32_t cnt = w.shard_v1 - w.shard_v0;
     if (!out || (g->n > 0 && (!dist || !prev)))
         fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
-    DeviceGuard dg(g->device);
+    GraphScope dg(g);
     cudaStream_t s = g->stream;
     // counters 0,1 (items, improved sinks) and 3,4 (stats) restart every round;
     // 2 (overflow) accumulates over the relaxations since the previous call
@@ -806,7 +813,7 @@ static void shard_relax(gdx_graph* g, D* dist) {
     if (!g || !g->sssp || !g->sssp->shard_ready)
         fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
     if (g->n > 0 && !dist) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
-    DeviceGuard dg(g->device);
+    GraphScope dg(g);
     auto& w = *g->sssp;
     cudaStream_t s = g->stream;
     // the single-GPU rule (gdx_sssp): deeper grids for large relaxation sets
@@ -846,7 +853,7 @@ extern "C" int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
         if (!count_out || (g->n > 0 && (!dist || !changed_ids || !changed_dist)))
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         auto& w = *g->sssp;
         cudaStream_t s = g->stream;
         if (!w.shard_mark.get() || w.shard_mark.bytes() < size_t(g->n) * 4 ||
@@ -883,7 +890,7 @@ extern "C" int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t
         if (count < 0 || (count > 0 && (!dist || !ids || !vals)))
             fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
         if (count == 0) return;
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         cudaStream_t s = g->stream;
         timed_launch(g, "sssp_shard_apply", [&] {
             k_sssp_delta_apply<int><<<blocks_for(count, 256, g->num_sms * 8), 256, 0, s>>>(
@@ -901,7 +908,7 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
                                            " out of range [0, " + std::to_string(g->n) + ")");
         if (!g->dests.get() && g->m > 0)
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
-        DeviceGuard dg(g->device);
+        GraphScope dg(g);
         if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
         auto& w = *g->sssp;
         // every vertex enters a round's queue at most once: <= n + m/kChunk
@@ -910,11 +917,6 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         const size_t qcap = 2 * (size_t(g->n) + size_t(g->m) / kChunk + 1) +
                             size_t(kWarpChunk) * 64 * size_t(g->num_sms);
         w.dist.ensure(size_t(g->n));
-        w.stamp.ensure(size_t(g->n));
-        // queue[1] doubles as the int64 staging buffer for host outputs
-        w.queue[0].ensure(qcap);
-        w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
-        w.ctrs.ensure(kCtrs);
         // 32-bit distances unless a relaxation overflows them (then 64-bit):
         // the result is exact either way.  Large graphs use frontier-scan
         // rounds (bandwidth-bound), small ones the persistent kernel
@@ -936,6 +938,13 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
             if (run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
                 run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph);
         } else {
+            // the persistent kernel's queues exist only in this mode (C5 in the
+            // default graph mode would otherwise hold 2 x ~2 GB of unused items);
+            // queue[1] doubles as the int64 staging buffer for host outputs
+            w.stamp.ensure(size_t(g->n));
+            w.queue[0].ensure(qcap);
+            w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
+            w.ctrs.ensure(kCtrs);
             const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
             if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
         }

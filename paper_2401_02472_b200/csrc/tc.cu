@@ -537,13 +537,33 @@ __global__ void __launch_bounds__(256) k_tc_heavy(int32_t nh, const int32_t* __r
     }
 }
 
-static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_stats* stats) {
+// SURVEY.md 8(d) TC work measure: sum over oriented edges v->u of
+// d+(u) + d+(v) (= sum_v d+(v)^2 + sum_v sum_{u in N+(v)} d+(u)).
+__global__ void k_tc_survey_pairs(int32_t n, const int32_t* __restrict__ off_plus,
+                                  const int32_t* __restrict__ adj, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = off_plus[v], e = off_plus[v + 1];
+        acc += (unsigned long long)(e - b) * (unsigned long long)(e - b);
+        for (int32_t i = b; i < e; ++i) {
+            const int32_t u = adj[i];
+            acc += (unsigned long long)(off_plus[u + 1] - off_plus[u]);
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// The oriented CSR (off+, adj+) is a derived index of the immutable graph:
+// built by the first TC call on a handle and kept with it (like the PageRank
+// plan), sized from the scanned total -- not from m/2 + n, which only holds
+// for symmetric rows.
+static void build_oriented(gdx_graph* g, TcPlan& P) {
     cudaStream_t s = g->stream;
-    auto& P = *g->tc;
     const int32_t n = g->n;
     P.off_plus.ensure(size_t(n) + 1);
     P.hi_start.ensure(size_t(n) + 1);
-    P.adj_plus.ensure(size_t(g->m) / 2 + size_t(n) + 8);
     static const int orient_per_sm = [] {  // blocks per SM of the orientation passes
         const char* e = std::getenv("GDX_TC_ORIENT_GRID");
         return e ? std::max(1, std::atoi(e)) : 64;  // same-box C3: count 0.204 vs 0.227 ms at 16
@@ -561,10 +581,31 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
     GDX_CUDA(cudaMemsetAsync(P.off_plus.get() + n, 0, 4, s));
     GDX_CUDA(cub::DeviceScan::ExclusiveSum(P.scan_tmp.get(), bytes, P.off_plus.get(),
                                            P.off_plus.get(), n + 1, s));
+    int32_t* h = reinterpret_cast<int32_t*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h, P.off_plus.get() + n, 4, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    P.adj_plus.ensure(size_t(h[0]) + 8);
     timed_launch(g, "tc_orient_fill", [&] {
         k_tc_orient_fill<<<grid_v, 256, 0, s>>>(n, g->dests.get(), P.hi_start.get(),
                                                 P.off_plus.get(), P.adj_plus.get());
     });
+    DevBuf<unsigned long long> sp(1);
+    GDX_CUDA(cudaMemsetAsync(sp.get(), 0, 8, s));
+    k_tc_survey_pairs<<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, P.off_plus.get(),
+                                                                         P.adj_plus.get(), sp.get());
+    GDX_LAUNCH_CHECK();
+    unsigned long long* h64 = reinterpret_cast<unsigned long long*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h64, sp.get(), 8, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    P.survey_pairs = double(h64[0]);
+    P.oriented = true;
+}
+
+static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_stats* stats) {
+    cudaStream_t s = g->stream;
+    auto& P = *g->tc;
+    const bool built_now = !P.oriented;
+    if (built_now) build_oriented(g, P);
     if (v_end > v_begin) {
         const int64_t groups = (int64_t(v_end) - v_begin + 31) / 32;
         const char* cap = std::getenv("GDX_TC_GRID_CAP");  // blocks per SM (A/B)
@@ -587,14 +628,14 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
         });
         heavy_launches = 1;
     }
-    if (stats) stats->launches = 2 + (v_end > v_begin) + heavy_launches;
+    if (stats) stats->launches = (built_now ? 3 : 0) + (v_end > v_begin) + heavy_launches;
 }
 
 static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_out,
                    gdx_stats* stats) {
     if (!g->dests.get() && g->m > 0)
         fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
-    DeviceGuard dg(g->device);
+    GraphScope dg(g);
     cudaStream_t s = g->stream;
     if (!g->tc) g->tc = std::make_unique<TcPlan>();
     auto& P = *g->tc;
@@ -636,10 +677,13 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
         // Oriented kernel: orientation (offsets 4(n+1) read, dests 4m read,
         // adj+ 2m + off+ 4(n+1) written) + N+ staging 2m + per pair the off+
         // pair of u (8) and 4 per element of both merged lists.
+        // Oriented kernel over the whole graph: SURVEY.md 8(d) exactly,
+        // 4(n+1) + 4m + 4 * sum over oriented edges of (d+(u) + d+(v)).
         const double frac = g->n ? double(int64_t(v_end) - v_begin) / g->n : 0.0;
-        if (oriented)
-            stats->algorithmic_bytes = 8.0 * (g->n + 1) + 6.0 * g->m + frac * 2.0 * g->m +
-                                       4.0 * double(h[1]);
+        if (oriented && v_begin == 0 && v_end == g->n)
+            stats->algorithmic_bytes = 4.0 * (g->n + 1) + 4.0 * g->m + 4.0 * P.survey_pairs;
+        else if (oriented)
+            stats->algorithmic_bytes = frac * (4.0 * (g->n + 1) + 4.0 * g->m) + 4.0 * double(h[1]);
         else
             stats->algorithmic_bytes =
                 frac * (4.0 * (g->n + 1) + 4.0 * g->m) + 4.0 * double(h[1]);
