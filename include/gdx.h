@@ -145,6 +145,25 @@ int gdx_graph_generate(const gdx_gen_params* p, int device, gdx_graph** out);
 /* Counter-hash weights in [lo, hi] (symmetric for undirected graphs). */
 int gdx_graph_set_hash_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t seed);
 
+/* ---- the reference's sequential streams (host side; refstream.cu) -----------
+ * Exactly the reference's std::mt19937_64 streams, for feeding the device path
+ * the reference's own inputs (parity configs, `graphdsl run --weight-*`):
+ *   genUniformEdges (core/src/graphgen.cpp:8-16)   gdx_gen_uniform_edges_ref
+ *   genRmatEdges    (core/src/graphgen.cpp:18-56)  gdx_gen_rmat_edges_ref
+ *   CsrGraph::withRandomWeights (core/src/csr.cpp:172-195)
+ *                                      gdx_random_weights_host (host CSR arrays)
+ *                                      gdx_graph_set_random_weights (a handle)
+ * u, v, weights_out are host arrays of the given lengths.  Errors mirror the
+ * reference's std::invalid_argument messages ("node count must be positive",
+ * "weight range is empty", ...). */
+int gdx_gen_uniform_edges_ref(int32_t nodes, int64_t edges, uint64_t seed, int32_t* u, int32_t* v);
+int gdx_gen_rmat_edges_ref(int32_t nodes, int64_t edges, uint64_t seed, double a, double b,
+                           double c, double d, int32_t* u, int32_t* v);
+int gdx_random_weights_host(int32_t n, int32_t m, int32_t directed, const int32_t* offsets,
+                            const int32_t* dests, int32_t lo, int32_t hi, uint64_t seed,
+                            int32_t* weights_out);
+int gdx_graph_set_random_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t seed);
+
 /* ---- the four entry points -------------------------------------------------
  * ComputeSSSP: dist_out[n] int64, unreachable = INT64_MAX/2 (oracles.hpp:12).
  * The corpus postconditions hold on return: `modified` is all false and

@@ -76,6 +76,13 @@ SIGNATURES = {
     "gdx_graph_write_edge_list": ([C.c_void_p, C.c_char_p, C.c_int], C.c_int),
     "gdx_graph_generate": ([C.POINTER(GdxGenParams), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "gdx_graph_set_hash_weights": ([C.c_void_p, C.c_int32, C.c_int32, C.c_uint64], C.c_int),
+    "gdx_gen_uniform_edges_ref": ([C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p],
+                                  C.c_int),
+    "gdx_gen_rmat_edges_ref": ([C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_double,
+                               C.c_double, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_random_weights_host": ([C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                C.c_int32, C.c_int32, C.c_uint64, C.c_void_p], C.c_int),
+    "gdx_graph_set_random_weights": ([C.c_void_p, C.c_int32, C.c_int32, C.c_uint64], C.c_int),
     "gdx_sssp": ([C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),
     "gdx_pagerank": ([C.c_void_p, C.c_double, C.c_double, C.c_int32, C.c_void_p, i32p,
                       C.POINTER(GdxStats)], C.c_int),

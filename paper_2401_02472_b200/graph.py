@@ -140,6 +140,11 @@ class DeviceGraph:
         check(_lib.load().gdx_graph_write_edge_list(self.handle, str(path).encode(),
                                                     int(bool(with_weights))))
 
+    def set_random_weights(self, lo: int, hi: int, seed: int) -> None:
+        """CsrGraph::withRandomWeights (csr.cpp:172-195): the reference's
+        mt19937_64 weights, drawn on the host side of libgdx, uploaded."""
+        check(_lib.load().gdx_graph_set_random_weights(self.handle, int(lo), int(hi), int(seed)))
+
     def set_hash_weights(self, lo: int, hi: int, seed: int) -> None:
         check(_lib.load().gdx_graph_set_hash_weights(self._h, lo, hi, seed))
 
@@ -361,6 +366,35 @@ class DeviceGraph:
             nm = names.raw[64 * i:64 * (i + 1)].split(b"\0", 1)[0].decode()
             out[nm] = (ms[i], ln[i])
         return out
+
+
+def gen_uniform_edges(nodes: int, edges: int, seed: int):
+    """genUniformEdges (graphgen.cpp:8-16): the reference's edge stream."""
+    u = np.empty(int(edges), np.int32)
+    v = np.empty(int(edges), np.int32)
+    check(_lib.load().gdx_gen_uniform_edges_ref(int(nodes), int(edges), int(seed), _ptr(u), _ptr(v)))
+    return u, v
+
+
+def gen_rmat_edges(nodes: int, edges: int, seed: int, a: float = 0.57, b: float = 0.19,
+                   c: float = 0.19, d: float = 0.05):
+    """genRmatEdges (graphgen.cpp:18-56): the reference's edge stream."""
+    u = np.empty(int(edges), np.int32)
+    v = np.empty(int(edges), np.int32)
+    check(_lib.load().gdx_gen_rmat_edges_ref(int(nodes), int(edges), int(seed), a, b, c, d,
+                                             _ptr(u), _ptr(v)))
+    return u, v
+
+
+def random_weights(g, lo: int, hi: int, seed: int) -> np.ndarray:
+    """withRandomWeights (csr.cpp:172-195) over host CSR arrays."""
+    off = np.ascontiguousarray(g.offsets, np.int32)
+    dst = np.ascontiguousarray(g.dests, np.int32)
+    w = np.empty(int(g.m), np.int32)
+    check(_lib.load().gdx_random_weights_host(int(g.n), int(g.m), int(bool(g.directed)),
+                                              _ptr(off), _ptr(dst), int(lo), int(hi), int(seed),
+                                              _ptr(w)))
+    return w
 
 
 def device_count() -> int:
