@@ -3,19 +3,27 @@
 
 Headline (the `value` of the JSON line): config 2 of BASELINE.json --
 PageRank pull (d=0.85, tol 1e-6, maxIter 100) on an RMAT scale-24 graph
-(2^28 edge draws, ~268M directed edges), one gdx_pagerank call per step, graph
-resident in HBM.  The other configs are reported under "per_algorithm"
-(SSSP RMAT-18 C1, TC uniform 2^24 C3, BC 64 sources on a 4899^2 grid C4,
-SSSP RMAT-26 C5 with ~2.1e9 stored edges, checked by an on-device certificate).
+(2^28 edge draws, ~263M directed edges), one gdx_pagerank call per step, graph
+resident in HBM.  The other configs are reported under "per_algorithm":
+C1 SSSP on the reference's own RMAT-18 graph and weights, C3 TC uniform 2^24,
+C4 BC 64 sources on a 4899^2 grid, C5 SSSP RMAT-26 with ~2.1e9 stored edges.
+
+Every config is checked after its timed region against the oracle on the same
+graph ("parity": C1/C5 exact distances -- C1 also against the reference's own
+interp::run, C5 also by an on-device certificate --, C2 ranks <= 1e-6 relative
+with the same round count, C3 exact count, C4 all 64 sources <= 1e-6) and
+carries a CPU baseline timed on the host's cores ("cpu_baseline").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--algos sssp,tc,bc,sssp26] [--no-cpu-baseline]
+                  [--algos sssp,tc,bc,sssp26] [--no-cpu-baseline] [--no-c5-cpu]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL): PageRank (headline),
-TC, BC and C5 SSSP run partitioned across the ranks (distributed.py; strong
-scaling -- the graph is fixed), timing is the max over ranks.  `--impl reference` times the reference's own CPU path
-(oracle/_ref: interp::run in parallel mode on all host cores) on a bounded
-sample of the same workload.
+`--gpus N` > 1 runs one rank per GPU (self-launched through torch.distributed.run
+when WORLD_SIZE is unset; fails if fewer than N GPUs are visible): PageRank
+(headline), TC, BC and C5 SSSP run partitioned across the ranks (distributed.py;
+strong scaling -- the graph is fixed), timing is the max over ranks.
+`--impl reference` times the reference's own CPU path (oracle/_ref:
+interp::run(ComputePR) in parallel mode on all host cores) on the same C2 graph,
+one fixedPoint round per step.
 """
 from __future__ import annotations
 
@@ -47,15 +55,14 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch from the committed `ncu --set full` summary."""
+def ncu_summary() -> dict:
+    """The committed ncu figures (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
-        return None
+        return {}
 
 
 class Clocks:
@@ -178,29 +185,83 @@ def timed_steps(torch, dist, step, steps: int, warmup: int, flush, keep_all: boo
     return [a.elapsed_time(b) for a, b in evs], wall, results
 
 
-def roofline(prof: dict, kernel: str, algo_bytes: float, pk: dict, work_launches=None) -> dict:
+def roofline(prof: dict, kernel: str, algo_bytes: float, pk: dict, work_launches=None,
+             traffic_key=None) -> dict:
     """achieved = algorithmic bytes / summed device time of `kernel` (CUDA events
     around every launch, recorded by the library on the launching stream).
     `kernel` may be "a+b": kernels that together make one unit of work (a PR
-    round), timed and counted together.  `work_launches` excludes launches that
-    exit immediately (settled PR rounds)."""
+    round, an SSSP call), timed and counted together.  `work_launches` = the
+    number of units (PR: rounds that did work; others: calls).  traffic = DRAM
+    bytes per unit from the committed ncu captures (profiles/ncu_summary.json:
+    `traffic_key` -> dram_bytes_per_unit, else the per-kernel launch figures)."""
     parts = kernel.split("+")
     ms = sum(prof.get(k, (0.0, 0))[0] for k in parts)
     launches = prof.get(parts[0], (0.0, 0))[1]
     if work_launches:
         launches = work_launches
     achieved = algo_bytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-    tr = {k: ncu_traffic(k) for k in parts}
-    known = [k for k, t in tr.items() if t is not None]
-    traffic = sum(tr[k] for k in known) if known else None
+    traffic, known = None, []
+    summ = ncu_summary()
+    if traffic_key and traffic_key in summ and "dram_bytes_per_unit" in summ[traffic_key]:
+        traffic, known = summ[traffic_key]["dram_bytes_per_unit"], [traffic_key]
+    else:
+        tr = {k: summ.get(k, {}).get("dram_bytes_per_launch") for k in parts}
+        known = [k for k, t in tr.items() if t is not None]
+        traffic = sum(tr[k] for k in known) if known else None
     return {"kernel": kernel, "bound": "hbm", "achieved": round(achieved, 1),
             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "peak_source": pk["source"], "traffic": traffic, "traffic_kernels": known,
-            "kernel_ms_avg": round(ms / max(launches, 1), 4), "launches": launches,
-            "algorithmic_bytes_per_launch": round(algo_bytes / max(launches, 1), 1)}
+            "peak_source": pk["source"], "traffic": traffic, "traffic_source": known,
+            "kernel_ms_per_unit": round(ms / max(launches, 1), 4), "units": launches,
+            "algorithmic_bytes_per_unit": round(algo_bytes / max(launches, 1), 1)}
 
 
-def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
+# ------------------------------------------------------------------ parity + CPU legs
+# The oracle (oracle/, test infrastructure) is the checker here and the CPU
+# baseline: it runs after a config's timed region, on the same graph, and is
+# never the thing measured.
+
+CORES = os.cpu_count() or 1
+
+
+def _port():
+    from oracle import Port
+    return Port()
+
+
+def _ref():
+    from oracle import Ref, ref_available
+    return Ref() if ref_available() else None
+
+
+def rel_err(a, b) -> float:
+    import numpy as np
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    scale = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-12)
+    return float(np.max(np.abs(a - b) / scale))
+
+
+def timed_cpu(fn, budget_s: float):
+    """Whole runs of fn() until >= budget_s; returns (last result, runs, seconds)."""
+    runs, t0, res = 0, time.perf_counter(), None
+    while True:
+        res = fn()
+        runs += 1
+        t = time.perf_counter() - t0
+        if t >= budget_s:
+            return res, runs, t
+
+
+def _to_host(x):
+    import numpy as np
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+# ------------------------------------------------------------------------ our arm
+
+def bench_pr(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
     scale, draws = 24, 1 << 28
     dg = gdx.DeviceGraph.generate("rmat", 1 << scale, draws, seed=1, directed=True,
                                   device=dist.local)
@@ -228,13 +289,15 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
         "workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 tol=1e-6 maxIter=100",
         "n": n, "m": m, "rounds": rounds[-1], "gteps": edges * dist.world / (total_ms * 1e-3) / 1e9,
         "ms_per_step": total_ms / args.steps, "wall_ms": wall,
-        "roofline": roofline(prof, "pr_edges+pr_vertices", sum(rounds) * (12.0 * m + 32.0 * n), pk,
-                             work_launches=sum(rounds)),
+        "roofline": roofline(prof, "pr_edges+pr_vertices", sum(rounds) * (12.0 * m + 24.0 * n), pk,
+                             work_launches=sum(rounds), traffic_key="pr_round"),
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
     }
+    res["roofline"]["bytes_formula"] = "per round 12 m + 24 n (SURVEY.md 8(d))"
+    ranks = _to_host(out)
     # ---- e2e: host CSR arrays -> C ABI (upload) -> PR -> host rank --------------
-    h = dg.download()
+    h = dg.download(("offsets", "rev_offsets", "rev_srcs"))
     pin = {k: torch.from_numpy(getattr(h, k)).pin_memory() for k in ("offsets", "rev_offsets", "rev_srcs")}
     rank_host = torch.empty(n, dtype=torch.float64).pin_memory()
 
@@ -259,36 +322,34 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_baseline: bool) -> dict:
     t0 = time.perf_counter()
     rr = []
     for _ in range(args.steps):
-        t1 = time.perf_counter()
         rr.append(e2e_step())
-        print(f"e2e step {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr)
     e2e_s = dist.max(torch, time.perf_counter() - t0)
     res["e2e"] = {"value": float(m) * sum(rr) * dist.world / e2e_s / 1e9, "unit": "GTEPS",
                   "h2d_bytes_per_step": int(sum(t.numel() * 4 for t in pin.values())),
                   "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3 / args.steps,
                   "path": "gdx_graph_create(host CSR) + gdx_pagerank(host out) + destroy"}
-    if cpu_baseline:
-        res["cpu_baseline"] = cpu_pr_baseline(h)
-    return res
+    if cpu_legs:
+        port = _port()
 
-
-def cpu_pr_baseline(h, budget_s: float = 10.0) -> dict:
-    """The oracle port (pr.sp semantics, per-node ascending gathers) on the same
-    C2 graph on all host cores, repeated whole runs until >= budget_s."""
-    from oracle import Port
-    port = Port()
-    cores = os.cpu_count() or 1
-    runs, edges = 0, 0.0
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        _, rounds = port.pr(h, 0.85, 1e-6, 100, threads=cores)
-        runs += 1
-        edges += float(h.m) * rounds
-    t = time.perf_counter() - t0
-    return {"value": edges / t / 1e9, "unit": "GTEPS", "cores": cores, "kind": "port",
+        class HG:  # the port reads the reverse CSR for the gather
+            pass
+        hg = HG()
+        hg.n, hg.m, hg.directed = n, m, True
+        hg.offsets, hg.rev_offsets, hg.rev_srcs = h.offsets, h.rev_offsets, h.rev_srcs
+        hg.dests = hg.weights = hg.rev_eid = None
+        (ranks_cpu, r_cpu), runs, t = timed_cpu(
+            lambda: port.pr(hg, 0.85, 1e-6, 100, threads=CORES), args.cpu_budget)
+        res["cpu_baseline"] = {
+            "value": float(m) * r_cpu * runs / t / 1e9, "unit": "GTEPS", "cores": CORES,
+            "kind": "port",
             "sample": f"oracle port (oracle/gdx_oracle.cpp orc_pr: ComputePR d=0.85 tol=1e-6 "
-                      f"maxIter=100) on the same C2 graph, {runs} full runs x {rounds} rounds on "
-                      f"{cores} threads in {t:.1f}s"}
+                      f"maxIter=100, per-node ascending gathers) on the same C2 graph, {runs} "
+                      f"full runs x {r_cpu} rounds on {CORES} threads in {t:.1f}s"}
+        err = rel_err(ranks, ranks_cpu)
+        res["parity"] = {"ok": bool(err <= 1e-6 and r_cpu == rounds[-1]), "vs": "oracle port pr",
+                         "max_rel_err": err, "tolerance": "1e-6 relative per node",
+                         "rounds": rounds[-1], "rounds_oracle": r_cpu}
+    return res
 
 
 def sssp_certificate(torch, dg, d) -> bool:
@@ -319,9 +380,37 @@ def sssp_certificate(torch, dg, d) -> bool:
     return ok
 
 
-def bench_sssp(torch, gdx, dist, args, pk, scale: int = 18) -> dict:
-    dg = gdx.DeviceGraph.generate("rmat", 1 << scale, 16 << scale, seed=1, directed=False,
-                                  weights=(1, 100), device=dist.local)
+def sssp_roofline(prof, sts, pk, n, traffic_key):
+    kern = ("sssp_graph" if "sssp_graph" in prof else
+            "sssp_relax+sssp_frontier" if "sssp_relax" in prof else "sssp_rounds")
+    r = roofline(prof, kern, sum(s["algorithmic_bytes"] for s in sts), pk,
+                 traffic_key=traffic_key, work_launches=len(sts))
+    r["bytes_formula"] = "16 V_vis + 12 E_vis + 8 U (SURVEY.md 8(d))"
+    s = sts[-1]
+    r["counters_per_call"] = {"V_vis": s["vertices_visited"], "E_vis": s["edges_visited"],
+                              "U": s["updates"], "rounds": s["rounds"]}
+    # the frontier scan reads dist + prev for all n vertices per round (+ the
+    # final empty round): work the formula does not count
+    r["scan_bytes_per_call"] = float((s["rounds"] + 1) * 2 * 4 * n)
+    return r
+
+
+def bench_sssp(torch, gdx, dist, args, pk, scale: int, cpu_legs: bool) -> dict:
+    if scale == 18:
+        # C1 on the reference's own graph: genRmatEdges(2^18,
+        # 2^22, 1) undirected, withRandomWeights(1, 100, 1) -- the reference's
+        # mt19937_64 streams from libgdx's host side, the CSR built on the GPU
+        u, v = gdx.gen_rmat_edges(1 << 18, 1 << 22, 1)
+        dg = gdx.DeviceGraph.build_from_edges(1 << 18, u, v, None, directed=False,
+                                              device=dist.local)
+        dg.set_random_weights(1, 100, 1)
+        cfg, recipe = "C1", ("genRmatEdges(2^18, 2^22, seed 1) undirected + withRandomWeights(1, "
+                             "100, seed 1): the reference's own graph")
+    else:
+        dg = gdx.DeviceGraph.generate("rmat", 1 << scale, 16 << scale, seed=1, directed=False,
+                                      weights=(1, 100), device=dist.local)
+        cfg, recipe = "C5", (f"counter-based RMAT-{scale} twin, 2^{scale + 4} draws, undirected, "
+                             "counter-hash weights U[1,100]")
     dg.set_stream(torch.cuda.current_stream().cuda_stream)
     out = torch.empty(dg.n, dtype=torch.int64, device="cuda")
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
@@ -341,25 +430,57 @@ def bench_sssp(torch, gdx, dist, args, pk, scale: int = 18) -> dict:
     ms, wall, sts = timed_steps(torch, dist, step, args.steps, 0, flush)
     prof = dg.profile_read()
     total = dist.max(torch, sum(ms))
-    cfg = "C1" if scale == 18 else "C5" if scale == 26 else f"RMAT-{scale}"
     res = {"workload": f"{cfg} SSSP RMAT-{scale} ef16 undirected, weights U[1,100], src 0",
-           "n": dg.n, "m": dg.m, "rounds": sts[-1]["rounds"],
+           "graph": recipe, "n": dg.n, "m": dg.m, "rounds": sts[-1]["rounds"],
            "edges_visited_over_m": sts[-1]["edges_visited"] / dg.m,
            "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / args.steps,
-           "roofline": roofline(prof, "sssp_graph" if "sssp_graph" in prof
-                                else "sssp_relax+sssp_frontier" if "sssp_relax" in prof
-                                else "sssp_rounds", sum(s["algorithmic_bytes"] for s in sts), pk),
-           "gpu_launches": int(sum(v[1] for v in prof.values()))}
-    if scale > 18:  # C1 is checked bit-exactly by the tests; larger graphs by certificate
+           "roofline": sssp_roofline(prof, sts, pk, dg.n, f"sssp_{cfg.lower()}_call"),
+           "gpu_launches": int(sum(s["launches"] for s in sts))}
+    if scale > 18:
         res["certificate_ok"] = sssp_certificate(torch, dg, out)
-    del out, flush
-    dg.close()
+    if cpu_legs:
+        port = _port()
+        d = _to_host(out)
+        h = dg.download(("offsets", "dests", "weights"))
+        dg.close()
+        del out, flush
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        exp = port.sssp(h, 0)
+        t_dij = time.perf_counter() - t0
+        par = {"ok": bool((d == exp).all()), "vs": "oracle port sssp (Dijkstra, oracles.cpp:10-31)",
+               "mismatches": int((d != exp).sum()), "tolerance": "exact int64"}
+        if scale == 18:
+            ref = _ref()
+            if ref is not None:  # the reference itself: interp::run(ComputeSSSP), parallel
+                rg = ref.build_from_host(h)
+                (di, mod, fin), runs, t = timed_cpu(
+                    lambda: rg.interp_sssp(0, parallel=True, threads=CORES), args.cpu_budget)
+                par["interp_ok"] = bool((di == d).all() and not mod.any() and fin)
+                par["ok"] = par["ok"] and par["interp_ok"]
+                res["cpu_baseline"] = {
+                    "value": dg_m(h) * runs / t / 1e9, "unit": "GTEPS", "cores": CORES,
+                    "kind": "reference",
+                    "sample": f"interp::run(ComputeSSSP, src 0) ExecMode::Parallel on {CORES} "
+                              f"threads (oracle/_ref), same C1 graph, {runs} runs in {t:.1f}s"}
+        if "cpu_baseline" not in res:
+            res["cpu_baseline"] = {
+                "value": dg_m(h) / t_dij / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
+                "sample": f"oracle port Dijkstra (oracles.cpp:10-31) on the same {cfg} graph, "
+                          f"one full run in {t_dij:.1f}s"}
+        res["parity"] = par
+    else:
+        dg.close()
     torch.cuda.empty_cache()
     return res
 
 
-def bench_tc(torch, gdx, dist, args, pk) -> dict:
+def dg_m(h) -> float:
+    return float(h.m)
+
+
+def bench_tc(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
     dg = gdx.DeviceGraph.generate("uniform", 1 << 24, 1 << 27, seed=1, directed=False,
                                   device=dist.local)
     dg.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -373,6 +494,10 @@ def bench_tc(torch, gdx, dist, args, pk) -> dict:
         return c
 
     dg.profile(True)
+    t0 = time.perf_counter()
+    step()  # first call on the handle: builds the oriented CSR (a cached plan)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    plan_prof = dg.profile_read()
     for _ in range(args.warmup):
         step()
     dg.profile_reset()
@@ -380,25 +505,45 @@ def bench_tc(torch, gdx, dist, args, pk) -> dict:
     ms, wall, counts = timed_steps(torch, dist, step, args.steps, 0, flush)
     prof = dg.profile_read()
     total = dist.max(torch, sum(ms))
+    kern = "+".join(k for k in ("tc", "tc_heavy") if k in prof)
     res = {"workload": "C3 TC uniform 2^24 vertices, 2^27 draws, undirected",
            "n": dg.n, "m": dg.m, "triangles": counts[-1],
            "gteps": dg.m * args.steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / args.steps,
-           "roofline": roofline(prof, "tc+tc_orient+tc_orient_fill",
-                                sum(s["algorithmic_bytes"] for s in sts), pk),
+           "roofline": roofline(prof, kern, sum(s["algorithmic_bytes"] for s in sts), pk,
+                                traffic_key="tc_call", work_launches=len(sts)),
+           "plan": {"first_call_ms": round(plan_ms, 2),
+                    "orientation_kernels_ms": round(sum(plan_prof.get(k, (0, 0))[0] for k in
+                                                        ("tc_orient", "tc_orient_fill")), 3),
+                    "note": "the oriented CSR (off+, adj+) is built by the first call on a "
+                            "handle and cached with it, like the PageRank plan"},
            "gpu_launches": int(sum(v[1] for v in prof.values())),
            "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()}}
-    dg.close()
+    res["roofline"]["bytes_formula"] = ("4(n+1) + 4m + 4 * sum over oriented edges u->v of "
+                                        "(d+(u) + d+(v)) (SURVEY.md 8(d))")
+    if cpu_legs:
+        port = _port()
+        h = dg.download(("offsets", "dests"))
+        dg.close()
+        c_cpu, runs, t = timed_cpu(lambda: port.tc(h, threads=CORES), 0.0)
+        res["cpu_baseline"] = {
+            "value": float(h.m) * runs / t / 1e9, "unit": "GTEPS", "cores": CORES, "kind": "port",
+            "sample": f"oracle port TC (tc.sp:6-18 semantics) on the same C3 graph, {runs} full "
+                      f"run(s) on {CORES} threads in {t:.1f}s"}
+        res["parity"] = {"ok": bool(c_cpu == counts[-1]), "vs": "oracle port tc",
+                         "triangles_oracle": int(c_cpu), "tolerance": "exact int64"}
+    else:
+        dg.close()
     return res
 
 
-def bench_bc(torch, gdx, dist, args, pk) -> dict:
+def bench_bc(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
     import numpy as np
     side = 4899
     dg = gdx.DeviceGraph.generate("grid", side, seed=1, keep=0.55, directed=False,
                                   device=dist.local)
     dg.set_stream(torch.cuda.current_stream().cuda_stream)
-    h = dg.download()
+    h = dg.download(("offsets", "dests"))
     deg = np.diff(h.offsets)
     cand = np.flatnonzero(deg > 0)
     rng = np.random.default_rng(1)
@@ -422,15 +567,41 @@ def bench_bc(torch, gdx, dist, args, pk) -> dict:
     ms, wall, _ = timed_steps(torch, dist, step, steps, 0, flush)
     prof = dg.profile_read()
     total = dist.max(torch, sum(ms))
+    kern = "bc_cta" if "bc_cta" in prof else "bc_forward+bc_backward"
     res = {"workload": f"C4 BC {len(sources)} sources, {side}^2 grid keep 0.55 undirected",
            "n": dg.n, "m": dg.m, "levels": sts[-1]["rounds"], "steps": steps,
            "gteps": dg.m * len(sources) * steps * dist.world / (total * 1e-3) / 1e9,
            "ms_per_step": total / steps,
-           "roofline": roofline(prof, "bc_cta" if "bc_cta" in prof else "bc_forward",
-                                sum(s["algorithmic_bytes"] for s in sts)
-                                / (1 if "bc_cta" in prof else 2), pk),
+           "roofline": roofline(prof, kern, sum(s["algorithmic_bytes"] for s in sts), pk,
+                                traffic_key="bc_call", work_launches=len(sts)),
            "gpu_launches": int(sum(v[1] for v in prof.values()))}
-    dg.close()
+    s = sts[-1]
+    res["roofline"]["bytes_formula"] = ("per source 48 n_reached + 16 m_scanned + 24 m_dag "
+                                        "(SURVEY.md 8(d))")
+    res["roofline"]["counters_per_call"] = {"n_reached": s["vertices_visited"],
+                                            "m_scanned_fwd_plus_bwd": s["edges_visited"],
+                                            "m_dag": s["updates"]}
+    if cpu_legs:
+        port = _port()
+        b = _to_host(out)
+        dg.close()
+        del out, flush
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        exp = port.bc(h, sources, threads=CORES)
+        t = time.perf_counter() - t0
+        err = rel_err(b, exp)
+        res["cpu_baseline"] = {
+            "value": float(h.m) * len(sources) / t / 1e9, "unit": "GTEPS", "cores": CORES,
+            "kind": "port",
+            "sample": f"oracle port Brandes (oracles.cpp:33-71, sources in parallel on {CORES} "
+                      f"threads, summed in source order) on the same C4 graph and all "
+                      f"{len(sources)} sources in {t:.1f}s"}
+        res["parity"] = {"ok": bool(err <= 1e-6 and np.isfinite(b).all()), "vs": "oracle port bc",
+                         "sources_compared": len(sources), "max_rel_err": err,
+                         "tolerance": "1e-6 relative per node"}
+    else:
+        dg.close()
     return res
 
 
@@ -489,7 +660,7 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
         "gteps": float(m) * sum(rounds) / (total_ms * 1e-3) / 1e9,
         "ms_per_step": total_ms / args.steps, "wall_ms": wall,
         "roofline": _shard_roofline(prof, "pr_edges+pr_vertices",
-                                    sum(rounds) * (12.0 * e_r + 32.0 * (v1 - v0)), pk, sum(rounds)),
+                                    sum(rounds) * (12.0 * e_r + 24.0 * (v1 - v0)), pk, sum(rounds)),
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
         "partition": {"ranges": ranges, "rank0_edges": e_r},
@@ -616,14 +787,19 @@ def run_ours(args) -> None:
         head = bench_pr(torch, gdx, dist, args, pk, cpu)
     for a in algos:
         if a == "sssp":
-            per["sssp"] = bench_sssp(torch, gdx, dist, args, pk)
+            per["sssp"] = bench_sssp(torch, gdx, dist, args, pk, 18, cpu)
         elif a == "sssp26":
-            per["sssp_c5"] = bench_sssp(torch, gdx, dist, args, pk, scale=26)
+            per["sssp_c5"] = bench_sssp(torch, gdx, dist, args, pk, 26, cpu and not args.no_c5_cpu)
         elif a == "tc":
-            per["tc"] = bench_tc(torch, gdx, dist, args, pk)
+            per["tc"] = bench_tc(torch, gdx, dist, args, pk, cpu)
         elif a == "bc":
-            per["bc"] = bench_bc(torch, gdx, dist, args, pk)
-    per["pr"] = {k: head[k] for k in ("workload", "gteps", "ms_per_step", "rounds", "roofline")}
+            per["bc"] = bench_bc(torch, gdx, dist, args, pk, cpu)
+    per["pr"] = {k: head[k] for k in ("workload", "gteps", "ms_per_step", "rounds", "roofline",
+                                      "cpu_baseline", "parity") if k in head}
+    parity = {k: v["parity"]["ok"] for k, v in per.items() if "parity" in v}
+    for k, v in per.items():
+        if "certificate_ok" in v:
+            parity[k + "_certificate"] = v["certificate_ok"]
     line = {
         "metric": METRIC, "value": round(head["gteps"], 3), "unit": "GTEPS",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -638,6 +814,7 @@ def run_ours(args) -> None:
                    "l2": "flushed (512 MB write) before every timed step"},
         "roofline": head["roofline"], "e2e": head["e2e"], "clocks": head["clocks"],
         "gpu_launches": head["gpu_launches"], "kernels": head["kernels"],
+        "parity": {"all_ok": all(parity.values()) if parity else None, **parity},
         "per_algorithm": per,
     }
     if "cpu_baseline" in head:
@@ -650,47 +827,80 @@ def run_ours(args) -> None:
 # ------------------------------------------------------------------ reference arm
 
 def run_reference(args) -> None:
-    """The reference's own CPU path (oracle/_ref = reference sources compiled
-    unchanged): interp::run(ComputePR) in ExecMode::Parallel on all host
-    cores.  Rank 0 only; other ranks exit without work."""
+    """The reference's own CPU path on the headline config: interp::run(ComputePR)
+    in ExecMode::Parallel on all host cores (oracle/_ref = the reference's sources
+    compiled unchanged), over the same C2 graph our arm runs -- the counter-based
+    RMAT-24 twin (2^28 draws, directed), its edges generated on the host by the
+    oracle port (tested array-for-array against the device generator) and built
+    into a CsrGraph by the reference's own buildFromEdges.  One step = one
+    fixedPoint round (maxIter = 0 runs exactly one round, pr.sp:25), so the GTEPS
+    (m * rounds / t) is per round like ours.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from oracle import Ref, ref_available
+    from oracle import Port, Ref, ref_available
     if not ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    ref = Ref()
-    cores = os.cpu_count() or 1
+    ref, port = Ref(), Port()
     scale = args.ref_scale
-    u, v = ref.gen_rmat_edges(1 << scale, 16 << scale, 1)
+    t0 = time.perf_counter()
+    u, v = port.gen_rmat_ctr(1 << scale, 16 << scale, 1, threads=CORES)
     g = ref.build(1 << scale, u, v, None, True)
-    times, rounds = [], []
+    del u, v
+    build_s = time.perf_counter() - t0
+    times = []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        _, it = g.interp_pr(0.85, 1e-6, 100, parallel=True, threads=cores)
-        dt = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        _, it = g.interp_pr(0.85, 1e-6, 0, parallel=True, threads=CORES)
+        dt = time.perf_counter() - t1
+        assert it == 1, it
         if i >= args.warmup:
             times.append(dt)
-            rounds.append(it)
+        print(f"reference step {i}: {dt:.2f} s", file=sys.stderr, flush=True)
     total = sum(times)
-    value = g.m * sum(rounds) / total / 1e9
-    sample = (f"interp::run(ComputePR, d=0.85 tol=1e-6 maxIter=100) ExecMode::Parallel on {cores} "
-              f"threads, RMAT scale-{scale} (genRmatEdges, 2^{scale + 4} draws, directed, "
-              f"m={g.m}, {rounds[-1]} rounds) per step -- the reference's tree-walking executor "
-              f"cannot run RMAT-24 within the bench budget")
+    value = g.m * len(times) / total / 1e9
+    cfg = "C2" if scale == 24 else f"sample RMAT-{scale}"
+    sample = (f"interp::run(ComputePR, d=0.85 tol=1e-6, maxIter=0 -> 1 fixedPoint round per "
+              f"step) ExecMode::Parallel on {CORES} threads; {cfg} graph: counter-based RMAT-"
+              f"{scale} twin, 2^{scale + 4} draws, directed, m={g.m}, built by the reference's "
+              f"CsrGraph::buildFromEdges in {build_s:.0f}s (not timed)")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference genRmatEdges)",
-        "config": {"workload": "C2 PageRank pull RMAT (bounded CPU sample)", "graph": f"rmat-{scale}",
-                   "m": g.m},
-        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": "reference",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: counter-based RMAT generator (a,b,c,d=.57,.19,.19,.05), seed 1",
+        "config": {"workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 "
+                               "tol=1e-6 (one fixedPoint round per step)" if scale == 24 else cfg,
+                   "graph": f"rmat-{scale}", "m": g.m, "same_config": scale == 24,
+                   "parallelism": f"{CORES} host threads"},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": CORES, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run, or fail loudly if fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # ranks / NVLS / P2P transport in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main() -> None:
@@ -701,8 +911,14 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algos", default="sssp,tc,bc,sssp26")
     ap.add_argument("--bc-sources", type=int, default=64)
-    ap.add_argument("--ref-scale", type=int, default=18)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-scale", type=int, default=24,
+                    help="reference arm graph scale (24 = C2 itself)")
+    ap.add_argument("--cpu-budget", type=float, default=10.0,
+                    help="seconds of repeated whole CPU runs per baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true",
+                    help="skip the oracle parity checks and CPU baselines")
+    ap.add_argument("--no-c5-cpu", action="store_true",
+                    help="skip the C5 Dijkstra comparison (the device certificate still runs)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded path even at N=1 (torchrun, NCCL)")
     args = ap.parse_args()
@@ -710,8 +926,13 @@ def main() -> None:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
+    run_ours(args)
 
 
 if __name__ == "__main__":

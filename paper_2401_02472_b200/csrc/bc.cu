@@ -1096,17 +1096,16 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             stats->vertices_visited = int64_t(totals[kReached]);
             stats->edges_visited = int64_t(totals[kFwdScan] + totals[kBwdScan]);
             stats->updates = int64_t(totals[kDag]);
-            // per reached (s,v): forward log 8 + offsets 8 +
-            // sigma 16 + discovery log write 8 + level CAS 4; backward log 8 +
-            // offsets 8 + sigma 16 + delta 8 + bc RMW 16.  Per scanned edge: dest 4 +
-            // level 4.  Per DAG edge use: sigma 16 (+ delta 8 backward ~ 12 avg).
-            // The same algorithmic bytes whether or not the backward pass reads
-            // the recorded children instead of the adjacency (an implementation
-            // choice, not less work).
+            // SURVEY.md 8(d), per source: 48 n_reached + 16 m_scanned + 24 m_dag.
+            // Per reached vertex: offsets, level, sigma, delta, bc read-modify-
+            // write; per scanned edge (m_scanned = edges the forward pass
+            // scanned): dest + level in each direction; per DAG edge: the sigma
+            // atomic forward, sigma / delta reads backward.  Charged the same
+            // whether or not the backward pass reads recorded children instead
+            // of rescanning the adjacency (an implementation choice).
             (void)used_kids;
-            stats->algorithmic_bytes = 100.0 * totals[kReached] +
-                                       8.0 * (totals[kFwdScan] + totals[kBwdScan]) +
-                                       28.0 * totals[kDag];
+            stats->algorithmic_bytes = 48.0 * totals[kReached] + 16.0 * totals[kFwdScan] +
+                                       24.0 * totals[kDag];
         }
     });
 }

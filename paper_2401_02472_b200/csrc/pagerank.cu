@@ -555,9 +555,10 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             stats->vertices_visited = int64_t(g->n) * rounds;
             stats->edges_visited = int64_t(g->m) * rounds;
             stats->updates = 0;
-            // per round rev_srcs 4m + contrib gather 8m +
-            // rev_offsets 4n + offsets 4n + rank in 8n + rank out 8n + contrib out 8n.
-            stats->algorithmic_bytes = double(rounds) * (12.0 * g->m + 32.0 * g->n);
+            // SURVEY.md 8(d), per round 12 m + 24 n: rev_srcs 4m + contrib
+            // gather 8m; rev_offsets 4n + rank read 8n + new rank / contrib
+            // write 8n + out-degree 4n.
+            stats->algorithmic_bytes = double(rounds) * (12.0 * g->m + 24.0 * g->n);
         }
     });
 }

@@ -345,11 +345,8 @@ static bool run_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
         stats->vertices_visited = int64_t(h[kVvis]);
         stats->edges_visited = int64_t(h[kEvis]);
         stats->updates = int64_t(h[kUpd]);
-        // per frontier vertex offsets pair 8 + dist + work item 8;
-        // per edge dest 4 + weight 4 + dist[nbr]; per improvement atomicMin + stamp 4 + push 8.
-        const double sd = sizeof(D), sw = g->weighted ? 4.0 : 0.0;
-        stats->algorithmic_bytes = (16.0 + sd) * h[kVvis] + (4.0 + sw + sd) * h[kEvis] +
-                                   (12.0 + sd) * h[kUpd];
+        // 16 V_vis + 12 E_vis + 8 U
+        stats->algorithmic_bytes = 16.0 * h[kVvis] + 12.0 * h[kEvis] + 8.0 * h[kUpd];
     }
     return h[kOvf] != 0;
 }
@@ -365,6 +362,7 @@ constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-co
 #ifndef GDX_SSSP_CHUNK
 #define GDX_SSSP_CHUNK 64
 #endif
+constexpr int kUpdSlot = 6;  // shard_ctr slot counting issued relaxations (U)
 constexpr int kShardChunk = GDX_SSSP_CHUNK;  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
 // every relaxation kernel splits an item over LPI in {8, 16, 32} lanes
 static_assert(kShardChunk % 32 == 0 && kShardChunk >= 32, "GDX_SSSP_CHUNK must be a multiple of 32");
@@ -506,9 +504,11 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
                                                         const int32_t* __restrict__ dests,
                                                         const int32_t* __restrict__ weights,
                                                         D* dist, unsigned long long* ovf,
-                                                        SsspDelta dl = {}) {
+                                                        SsspDelta dl = {},
+                                                        unsigned long long* upd = nullptr) {
     // LPI lanes per item: lane groups of LPI take one item each
     const int sub = threadIdx.x & (LPI - 1);
+    unsigned int issued = 0;  // relaxations that issued an atomicMin
     constexpr int kU = kShardChunk / LPI;  // edges per lane per item, all loads issued together
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
@@ -535,6 +535,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
 #pragma unroll
         for (int k = 0; k < kU; ++k)
             if (u[k] >= 0 && c[k] < du[k]) {
+                ++issued;
                 if (DELTA) {
                     if (c[k] < atomicMin(&dist[u[k]], c[k]) &&
                         atomicMax(&dl.mark[u[k]], dl.round) < dl.round)
@@ -543,6 +544,10 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
                     atomicMin(&dist[u[k]], c[k]);
                 }
             }
+    }
+    if (upd) {
+        issued = __reduce_add_sync(0xffffffffu, issued);
+        if ((threadIdx.x & 31) == 0 && issued) atomicAdd(upd, (unsigned long long)issued);
     }
 }
 
@@ -623,7 +628,8 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
     auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
             : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
     fn<<<relax_grid, 256, 0, cs>>>(w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
-                                   g->weighted ? g->weights.get() : nullptr, dist, ovf, SsspDelta{});
+                                   g->weighted ? g->weights.get() : nullptr, dist, ovf, SsspDelta{},
+                                   ctr + kUpdSlot);
     k_sssp_graph_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), h);
     cudaGraph_t captured;
     GDX_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -649,7 +655,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
     const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
     w.shard_queue.ensure(items_cap);
-    w.shard_ctr.ensure(5);
+    w.shard_ctr.ensure(kUpdSlot + 1);
     unsigned long long* ctr = w.shard_ctr.get();
     // graph path: round counters, [rounds, vertices, edges, overflow] in
     // graph_acc; host loop: its own overflow flag
@@ -658,7 +664,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     unsigned long long* ovf_flag = use_graph ? w.graph_acc.get() + 3 : ovf.get();
     timed_launch(g, "sssp_init", [&] {
         k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-            n, src, inf, dist, prev, ctr, 5, use_graph ? w.graph_acc.get() : ovf.get(),
+            n, src, inf, dist, prev, ctr, kUpdSlot + 1, use_graph ? w.graph_acc.get() : ovf.get(),
             use_graph ? 4 : 1);
     });
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
@@ -707,7 +713,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
             fn<<<relax_grid, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
                                                g->dests.get(),
                                                g->weighted ? g->weights.get() : nullptr, dist,
-                                               ovf.get(), SsspDelta{});
+                                               ovf.get(), SsspDelta{}, ctr + kUpdSlot);
         });
         ++launches;
     }
@@ -725,7 +731,10 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     GDX_CUDA(cudaMemcpyAsync(h, use_graph ? w.graph_acc.get() : ovf.get(),
                              (use_graph ? 4 : 1) * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaMemcpyAsync(h + 4, ctr + kUpdSlot, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long upd = h[4];
     const bool overflow = (use_graph ? h[3] : h[0]) != 0;
     if (use_graph) {
         rounds = int(h[0]);
@@ -738,13 +747,13 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         stats->launches = launches + 1;
         stats->vertices_visited = int64_t(vvis);
         stats->edges_visited = int64_t(evis);
-        stats->updates = 0;
-        // per round: frontier scan dist + prev (2 sizeof(D) n); per frontier
-        // vertex: offsets pair 8 + prev write + item 8 + dist[v]; per edge:
-        // dest 4 + weight 4 + dist[nbr]
-        const double sd = sizeof(D), sw = g->weighted ? 4.0 : 0.0;
-        stats->algorithmic_bytes = (rounds + 1) * 2.0 * sd * n + (16.0 + 2 * sd) * vvis +
-                                   (4.0 + sw + sd) * evis;
+        stats->updates = int64_t(upd);
+        // 16 V_vis + 12 E_vis + 8 U (offsets pair 8 + dist[v] 4 +
+        // queue entry 4 per frontier vertex; dest 4 + weight 4 + dist[nbr] 4 per
+        // edge; atomicMin 4 + push 4 per relaxation that issued an atomicMin).
+        // The frontier scan's full-V read (2 sizeof(D) n per round) is work the
+        // formula does not count; bench.py reports it beside the roofline.
+        stats->algorithmic_bytes = 16.0 * vvis + 12.0 * evis + 8.0 * upd;
     }
     return overflow;
 }
@@ -770,7 +779,7 @@ extern "C" int gdx_sssp_shard_setup(gdx_graph* g, int32_t v_begin, int32_t v_end
         w.shard_v1 = v_end;
         w.shard_edges = int64_t(eb[1]) - eb[0];
         w.shard_queue.ensure(size_t(v_end - v_begin) + size_t(eb[1] - eb[0]) / kShardChunk + 1);
-        w.shard_ctr.ensure(6);
+        w.shard_ctr.ensure(kUpdSlot + 1);
         w.shard_ready = true;
     });
 }

@@ -148,13 +148,16 @@ class DeviceGraph:
     def set_hash_weights(self, lo: int, hi: int, seed: int) -> None:
         check(_lib.load().gdx_graph_set_hash_weights(self._h, lo, hi, seed))
 
-    def download(self) -> HostCsr:
+    def download(self, arrays: Optional[Sequence[str]] = None) -> HostCsr:
+        """Host copy of the CSR; ``arrays`` limits it to the named arrays (the
+        others are None) -- e.g. ("offsets", "dests", "weights") for a
+        billion-edge graph whose reverse arrays alias the forward ones."""
         n, m = self.n, self.m
-        a = {k: np.empty(n + 1 if "offsets" in k else m, np.int32)
-             for k in ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")}
-        check(_lib.load().gdx_graph_download(
-            self._h, *[_ptr(a[k]) for k in ("offsets", "dests", "weights", "rev_offsets",
-                                              "rev_srcs", "rev_eid")]))
+        order = ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")
+        want = order if arrays is None else tuple(arrays)
+        a = {k: (np.empty(n + 1 if "offsets" in k else m, np.int32) if k in want else None)
+             for k in order}
+        check(_lib.load().gdx_graph_download(self._h, *[_ptr(a[k]) for k in order]))
         return HostCsr(n, m, self.directed, **a)
 
     def device_arrays(self, names: Sequence[str]):
