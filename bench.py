@@ -289,7 +289,7 @@ def bench_pr(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
         "workload": "C2 PageRank pull RMAT-24 (2^28 draws, directed) d=0.85 tol=1e-6 maxIter=100",
         "n": n, "m": m, "rounds": rounds[-1], "gteps": edges * dist.world / (total_ms * 1e-3) / 1e9,
         "ms_per_step": total_ms / args.steps, "wall_ms": wall,
-        "roofline": roofline(prof, "pr_edges+pr_vertices", sum(rounds) * (12.0 * m + 24.0 * n), pk,
+        "roofline": roofline(prof, "pr_edges+pr_cross+pr_vertices", sum(rounds) * (12.0 * m + 24.0 * n), pk,
                              work_launches=sum(rounds), traffic_key="pr_round"),
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
@@ -659,7 +659,7 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
         "n": n, "m": m, "rounds": rounds[-1],
         "gteps": float(m) * sum(rounds) / (total_ms * 1e-3) / 1e9,
         "ms_per_step": total_ms / args.steps, "wall_ms": wall,
-        "roofline": _shard_roofline(prof, "pr_edges+pr_vertices",
+        "roofline": _shard_roofline(prof, "pr_edges+pr_cross+pr_vertices",
                                     sum(rounds) * (12.0 * e_r + 24.0 * (v1 - v0)), pk, sum(rounds)),
         "clocks": clk.summary(), "gpu_launches": int(sum(v[1] for v in prof.values())),
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},

@@ -262,6 +262,44 @@ int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t* changed_i
 int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t* ids, const int32_t* vals,
                            int64_t count);
 
+/* ---- several GPUs from one process (multi.cu) --------
+ * For a C++ caller of interp::run (interpreter.hpp:64-88) that wants an
+ * ExecMode::Device over a device list.  gdx_context_create enables peer access
+ * between every pair of the listed devices (required: NVLink / NVSwitch) and,
+ * when every device is distinct, creates one NCCL communicator per device
+ * (ncclCommInitAll; NCCL is dlopen'ed, *nccl_comms reports how many).  A
+ * device may be listed more than once (several partitions on one GPU: the
+ * same protocol, no NCCL).  gdx_multi_graph_create uploads a replica of the
+ * graph to every device of the context.  The *_multi entry points have the
+ * single-GPU semantics and outputs (host pointers, or memory on the first
+ * device) and partition the work per SURVEY.md 8(e):
+ *   SSSP  vertex ranges by out-edges; improving candidates go straight to the
+ *         owner's distance replica by peer atomicMin; the round loop and its
+ *         barriers run on the devices (no dist all-gather)
+ *   PR    destination ranges by in-edges; new contrib values and the
+ *         (dangling, unsettled) partials are written into every device's
+ *         buffers over peer memory (no per-round collective)
+ *   TC    owner-vertex ranges by ~deg^2; counts summed in device order
+ *   BC    contiguous source blocks; one ncclAllReduce (sum) of the scores, or
+ *         a peer-memory sum in device order without NCCL
+ * Results: SSSP distances and TC counts identical to the single-GPU calls;
+ * PR ranks identical (same arithmetic, rank-ordered partial sums); BC within
+ * 1e-6 relative (the cross-device sum order differs from source order). */
+typedef struct gdx_context gdx_context;
+typedef struct gdx_multi_graph gdx_multi_graph;
+int gdx_context_create(int ndev, const int* devices, gdx_context** out);
+int gdx_context_destroy(gdx_context* ctx);
+int gdx_context_info(const gdx_context* ctx, int32_t* ndev, int32_t* nccl_comms,
+                     int32_t* peer_access);
+int gdx_multi_graph_create(gdx_context* ctx, const gdx_csr_view* view, gdx_multi_graph** out);
+int gdx_multi_graph_destroy(gdx_multi_graph* g);
+int gdx_sssp_multi(gdx_multi_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats);
+int gdx_pagerank_multi(gdx_multi_graph* g, double damping, double threshold, int32_t max_iter,
+                       double* rank_out, int32_t* rounds_out, gdx_stats* stats);
+int gdx_tc_multi(gdx_multi_graph* g, int64_t* count_out, gdx_stats* stats);
+int gdx_bc_multi(gdx_multi_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out,
+                 gdx_stats* stats);
+
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with
  * CUDA events on the launching stream.  gdx_profile_read reports, per kernel

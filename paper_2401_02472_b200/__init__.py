@@ -8,9 +8,9 @@ include/gdx.h); this package is the host-side mirror of the reference's
 from ._lib import GraphdslError  # noqa: F401
 from .corpus import CORPUS, CorpusEntry, entry_by_name, list_corpus  # noqa: F401
 from .executor import RunResult, run  # noqa: F401
-from .graph import (INF_DISTANCE, DeviceGraph, HostCsr, device_count,  # noqa: F401
-                    gen_rmat_edges, gen_uniform_edges, random_weights)
+from .graph import (INF_DISTANCE, Context, DeviceGraph, HostCsr, MultiGraph,  # noqa: F401
+                    device_count, gen_rmat_edges, gen_uniform_edges, random_weights)
 
 __all__ = ["GraphdslError", "CORPUS", "CorpusEntry", "entry_by_name", "list_corpus",
            "RunResult", "run", "INF_DISTANCE", "DeviceGraph", "HostCsr", "device_count",
-           "gen_rmat_edges", "gen_uniform_edges", "random_weights"]
+           "gen_rmat_edges", "gen_uniform_edges", "random_weights", "Context", "MultiGraph"]

@@ -109,6 +109,18 @@ SIGNATURES = {
     "gdx_sssp_shard_relax32": ([C.c_void_p, C.c_void_p], C.c_int),
     "gdx_sssp_shard_relax32_delta": ([C.c_void_p] + [C.c_void_p] * 4, C.c_int),
     "gdx_sssp_shard_apply32": ([C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64], C.c_int),
+    "gdx_context_create": ([C.c_int, C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "gdx_context_destroy": ([C.c_void_p], C.c_int),
+    "gdx_context_info": ([C.c_void_p, i32p, i32p, i32p], C.c_int),
+    "gdx_multi_graph_create": ([C.c_void_p, C.POINTER(GdxCsrView), C.POINTER(C.c_void_p)],
+                               C.c_int),
+    "gdx_multi_graph_destroy": ([C.c_void_p], C.c_int),
+    "gdx_sssp_multi": ([C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),
+    "gdx_pagerank_multi": ([C.c_void_p, C.c_double, C.c_double, C.c_int32, C.c_void_p, i32p,
+                            C.POINTER(GdxStats)], C.c_int),
+    "gdx_tc_multi": ([C.c_void_p, i64p, C.POINTER(GdxStats)], C.c_int),
+    "gdx_bc_multi": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)],
+                     C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),

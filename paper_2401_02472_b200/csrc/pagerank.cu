@@ -12,7 +12,9 @@
 //     of the group's first edge comes from a precomputed index into the list
 //     of non-empty rows (RMAT-24: 56% of rows are empty), so there is no
 //     merge-path search and no shared memory; rows finish inside a lane, via a
-//     segmented warp-shuffle scan, or (rows spanning warps) by atomicAdd.
+//     segmented warp-shuffle scan, or -- rows crossing a warp's 256-edge
+//     chunk -- as per-chunk head / tail partials that pass B adds in chunk
+//     order (no floating-point atomics: results are run-to-run identical).
 //     Measured on B200 the gather is limited by the L1->L2 miss-request rate
 //     (ncu: l1tex__m_l1tex2xbar_req_cycles_active 87%), so the design keeps
 //     every other L1 request to ~1 per 8 edges;
@@ -55,6 +57,15 @@ struct PrArgs {
     const int2* __restrict__ nz;          // k-th row with in-edges: (vertex, rev_offsets[vertex + 1])
     const int2* __restrict__ grp;         // per 8-edge group: (nz index of its first row, that row's end)
     double* row_sum;                      // per vertex, zero between rounds
+    // rows crossing a warp chunk (256 in-edges) are summed in pass B from the
+    // chunks' partials, in chunk order (deterministic: no atomics)
+    double* head_part;                    // per chunk: the row that began in an earlier chunk
+    double* tail_part;                    // per chunk: the row that continues into the next
+    const int4* __restrict__ cross;       // rows crossing chunks: (row, first chunk, last chunk)
+    const int4* __restrict__ cross_long;  // ... spanning more than kCrossShort chunks
+    int32_t ncross, nlong;
+    double* dang_part;                    // per block of a grid-wide dangling sum
+    unsigned int* dang_ctr;               // blocks done (the last one sums dang_part)
     // row range [v_begin, v_end) and its in-edges [e_begin, e_end) (the whole
     // graph on one GPU; one rank's slice when sharded, gdx_pr_shard_*)
     int32_t v_begin, v_end;
@@ -73,16 +84,40 @@ __device__ inline bool round_skipped(const PrArgs& a, int round) {
            *reinterpret_cast<const volatile int32_t*>(&a.flags[flag_slot(round - 1)]) == 0;
 }
 
+// Deterministic grid-wide sum of per-block values: every block stores its
+// value in slots[blockIdx.x]; the last block to finish sums the slots in a
+// fixed order and writes *out (replaces a float atomicAdd per block, whose
+// order -- and so the last bits of the dangling mass -- varied run to run).
+template <int BLOCK>
+__device__ inline void grid_sum_ordered(double v, double* slots, unsigned int* ctr, double* out) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        slots[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += BLOCK) s += __ldcg(&slots[i]);
+    typedef cub::BlockReduce<double, BLOCK> R;
+    __shared__ typename R::TempStorage tmp;
+    const double tot = R(tmp).Sum(s);
+    if (threadIdx.x == 0) {
+        *out = tot;
+        *ctr = 0;  // ready for the next grid
+    }
+}
+
 template <int BLOCK = kPrBlock>
 __device__ inline void block_flush(const PrArgs& a, int round, double dang_local, int unsettled) {
     typedef cub::BlockReduce<double, BLOCK> R;
     __shared__ typename R::TempStorage tmp;
     double tot = R(tmp).Sum(dang_local);
     int any = __syncthreads_or(unsettled);
-    if (threadIdx.x == 0) {
-        if (tot != 0.0) atomicAdd(&a.dangling[(round + 1) % 3], tot);
-        if (any) atomicOr(&a.flags[flag_slot(round)], 1);
-    }
+    if (threadIdx.x == 0 && any) atomicOr(&a.flags[flag_slot(round)], 1);
+    grid_sum_ordered<BLOCK>(tot, a.dang_part, a.dang_ctr, &a.dangling[(round + 1) % 3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -95,10 +130,12 @@ __device__ inline void block_flush(const PrArgs& a, int round, double dang_local
 // rows, so there is no merge-path search and no shared memory at all: the
 // only L1 traffic besides the random gathers is ~1 wavefront per 8 edges.
 // Rows finish inside a lane (plain store of the row sum), across lanes of a
-// warp (segmented shuffle scan), or across warps (atomicAdd of the partial).
+// warp (segmented shuffle scan), or across warps (per-chunk partials summed
+// in chunk order by pass B).
 // Pass B (k_pr_vertices) applies pr.sp:17-30 to every vertex with coalesced
 // loads, and clears row_sum for the next round.
 // ---------------------------------------------------------------------------
+
 constexpr int kEdgeGroup = 8;
 
 // One lane's 8-edge group g (all 32 lanes of the warp call this together
@@ -174,19 +211,21 @@ __device__ __forceinline__ void pr_edge_group(const PrArgs& a, const double* __r
     }
     const int32_t pkey = __shfl_up_sync(full, key, 1);
     const double pval = __shfl_up_sync(full, val, 1);
+    const int64_t chunk = g >> 5;  // this warp's 256 edges
     if (first_done) {
         const double tot = first_val + (lane > 0 && pkey == first ? pval : 0.0);
         const int64_t warp_e0 = e_base + (g & ~int64_t(31)) * kEdgeGroup;
         const int64_t start = first > 0 ? a.nz[first - 1].y : e_begin;
-        const int32_t row = a.nz[first].x;
-        if (start < warp_e0)
-            atomicAdd(&a.row_sum[row], tot);  // row began in an earlier warp's edges
+        if (start < warp_e0)  // the row began in an earlier chunk: k_pr_cross sums it
+            a.head_part[chunk] = tot;
         else
-            a.row_sum[row] = tot;
+            a.row_sum[a.nz[first].x] = tot;
     }
-    // the warp's trailing row continues into the next warp's edges
-    if (lane == 31 && val != 0.0 && key < a.nnz) atomicAdd(&a.row_sum[a.nz[key].x], val);
+    // the chunk's trailing row continues into the next chunk (written even when
+    // zero: pass B reads it for every row crossing the chunk's end)
+    if (lane == 31 && key < a.nnz) a.tail_part[chunk] = val;
 }
+
 
 template <bool R>
 __global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
@@ -200,6 +239,37 @@ __global__ void __launch_bounds__(256) k_pr_edges(PrArgs a, int round) {
     for (int64_t g0 = int64_t(blockIdx.x) * blockDim.x; g0 < ngroups;
          g0 += int64_t(gridDim.x) * blockDim.x)
         pr_edge_group<R>(a, contrib, g0 + threadIdx.x);
+}
+
+// Rows crossing chunks (between pass A and pass B): a row's sum is tail_part
+// of every chunk it leaves plus head_part of the chunk it ends in, added in
+// chunk order.  Rows spanning few chunks take a thread each (their loads
+// issued together); hub rows (more than kCrossShort chunks) take a warp,
+// lanes summing fixed strided subsets combined by a fixed shuffle tree.
+// Both orders are fixed, so the sums are run-to-run identical.
+constexpr int kCrossShort = 8;
+__global__ void __launch_bounds__(256) k_pr_cross(PrArgs a, int round) {
+    if (round_skipped(a, round)) return;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < a.ncross; i += nthreads) {
+        const int4 c = a.cross[i];  // (row, first chunk, last chunk)
+        double t[kCrossShort];
+#pragma unroll
+        for (int k = 0; k < kCrossShort; ++k) t[k] = c.y + k < c.z ? a.tail_part[c.y + k] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < kCrossShort; ++k) s += t[k];
+        a.row_sum[c.x] = s + a.head_part[c.z];
+    }
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = tid >> 5; i < a.nlong; i += nthreads >> 5) {
+        const int4 c = a.cross_long[i];
+        double s = 0.0;
+        for (int64_t k = c.y + lane; k < c.z; k += 32) s += a.tail_part[k];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) a.row_sum[c.x] = s + a.head_part[c.z];
+    }
 }
 
 // Pass B: two vertices per thread (16 B vector loads/stores), two pairs in
@@ -340,7 +410,21 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_init(PrArgs a) {
     typedef cub::BlockReduce<double, kPrBlock> R;
     __shared__ typename R::TempStorage tmp;
     double tot = R(tmp).Sum(dang_local);
-    if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&a.dangling[0], tot);
+    grid_sum_ordered<kPrBlock>(tot, a.dang_part, a.dang_ctr, &a.dangling[0]);
+}
+
+// The rows whose in-edges cross a 256-edge chunk boundary (k_pr_cross).
+__global__ void k_pr_cross_list(int32_t nnz, const int2* __restrict__ nz, int64_t e_begin,
+                                int64_t e_base, int4* cross, int4* cross_long, int32_t* count) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t start = k > 0 ? nz[k - 1].y : e_begin, end = nz[k].y;
+        const int32_t c0 = int32_t((start - e_base) >> 8), c1 = int32_t((end - 1 - e_base) >> 8);
+        if (c1 - c0 > kCrossShort)
+            cross_long[atomicAdd(count + 1, 1)] = make_int4(nz[k].x, c0, c1, 0);
+        else if (c0 != c1)
+            cross[atomicAdd(count, 1)] = make_int4(nz[k].x, c0, c1, 0);
+    }
 }
 
 // Edge-aligned plan for the rows [v_begin, v_end) (the whole graph, or one
@@ -387,6 +471,31 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     }
     P.row_sum.alloc(n);
     GDX_CUDA(cudaMemsetAsync(P.row_sum.get(), 0, P.row_sum.bytes(), s));
+    const int64_t chunks = (P.ngroups + 31) / 32 + 1;
+    P.head_part.alloc(size_t(chunks));
+    P.tail_part.alloc(size_t(chunks));
+    // rows crossing a 256-edge chunk: at most one ends in each chunk
+    P.cross.alloc(size_t(chunks));
+    P.cross_long.alloc(size_t(chunks));
+    {
+        DevBuf<int32_t> nc(2);
+        GDX_CUDA(cudaMemsetAsync(nc.get(), 0, 8, s));
+        if (P.nnz > 0) {
+            k_pr_cross_list<<<blocks_for(P.nnz, 256, g->num_sms * 16), 256, 0, s>>>(
+                P.nnz, P.nz.get(), P.e_begin, P.e_base, P.cross.get(), P.cross_long.get(),
+                nc.get());
+            GDX_LAUNCH_CHECK();
+        }
+        int32_t h[2] = {0, 0};
+        GDX_CUDA(cudaMemcpyAsync(h, nc.get(), 8, cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        P.ncross = h[0];
+        P.nlong = h[1];
+    }
+
+    P.dang_part.alloc(size_t(g->num_sms) * 8 + 8);  // >= every pass-B / init grid
+    P.dang_ctr.alloc(1);
+    GDX_CUDA(cudaMemsetAsync(P.dang_ctr.get(), 0, 4, s));
     for (int i = 0; i < 2; ++i) {
         P.rank[i].alloc(n);
         P.contrib[i].alloc(n);
@@ -400,6 +509,17 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
 }
 
 static void build_plan(gdx_graph* g) { build_edge_plan(g, *g->pr, 0, g->n); }
+
+// The crossing rows' sums of a round (between pass A and pass B); 1 if launched.
+static int launch_cross(gdx_graph* g, PrPlan& P, const PrArgs& a, int round) {
+    if (P.ncross == 0 && P.nlong == 0) return 0;
+    const int64_t work = std::max<int64_t>(P.ncross, int64_t(P.nlong) * 32);
+    timed_launch(g, "pr_cross", [&] {
+        k_pr_cross<<<blocks_for(work, 256, g->num_sms * 32), 256, 0, g->stream>>>(a, round);
+    });
+    return 1;
+}
+
 
 // The per-round "unsettled" votes live in a ring of kFlagRing slots (a round
 // reads only its predecessor's slot; the host reads a batch of at most
@@ -439,6 +559,14 @@ static PrArgs make_args(gdx_graph* g, PrPlan& P, double damping, double threshol
     a.nz = P.nz.get();
     a.grp = P.grp.get();
     a.row_sum = P.row_sum.get();
+    a.head_part = P.head_part.get();
+    a.tail_part = P.tail_part.get();
+    a.cross = P.cross.get();
+    a.cross_long = P.cross_long.get();
+    a.ncross = P.ncross;
+    a.nlong = P.nlong;
+    a.dang_part = P.dang_part.get();
+    a.dang_ctr = P.dang_ctr.get();
     a.v_begin = P.shard ? P.v_begin : 0;
     a.v_end = P.shard ? P.v_end : g->n;
     a.e_begin = P.e_begin;
@@ -470,7 +598,7 @@ __global__ void __launch_bounds__(kPrBlock) k_pr_shard_init(PrArgs a, double* pa
     typedef cub::BlockReduce<double, kPrBlock> R;
     __shared__ typename R::TempStorage tmp;
     double tot = R(tmp).Sum(dang_local);
-    if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&partials[0], tot);
+    grid_sum_ordered<kPrBlock>(tot, a.dang_part, a.dang_ctr, &partials[0]);
     if (a.npeers > 0) __threadfence_system();
 }
 
@@ -522,6 +650,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
                     timed_launch(g, "pr_edges", [&] {
                         k_pr_edges<false><<<P.grid, P.block, 0, s>>>(a, int(rr));
                     });
+                launches += launch_cross(g, P, a, int(rr));
                 timed_launch(g, "pr_vertices", [&] {
                     k_pr_vertices<false><<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock,
                                            0, s>>>(a, int(rr));
@@ -623,6 +752,7 @@ extern "C" int gdx_pr_shard_round(gdx_graph* g, int32_t round, double damping, d
             timed_launch(g, "pr_edges", [&] {
                 k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round);
             });
+        launch_cross(g, P, a, round);
         timed_launch(g, "pr_vertices", [&] {
             k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
                                        g->num_sms * 8),
@@ -722,6 +852,28 @@ using namespace gdx;
 
 static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
 
+// Device tables of every rank's contrib buffers / partial slots / counters.
+static void p2p_tables(PrP2P& X) {
+    std::vector<double*> pc(2 * X.world), ps(2 * X.world);
+    std::vector<unsigned long long*> pk(X.world);
+    for (int q = 0; q < X.world; ++q) {
+        double* b = X.bases[q];
+        for (int par = 0; par < 2; ++par) {
+            pc[par * X.world + q] = b + par * X.n;
+            ps[par * X.world + q] = b + 2 * X.n + (par * X.world + X.rank) * 2;
+        }
+        pk[q] = reinterpret_cast<unsigned long long*>(b + 2 * X.n + 4 * X.world);
+    }
+    X.peer_contrib.alloc(pc.size());
+    X.peer_slot.alloc(ps.size());
+    X.peer_ctr.alloc(pk.size());
+    GDX_CUDA(cudaMemcpy(X.peer_contrib.get(), pc.data(), pc.size() * sizeof(double*), cudaMemcpyHostToDevice));
+    GDX_CUDA(cudaMemcpy(X.peer_slot.get(), ps.data(), ps.size() * sizeof(double*), cudaMemcpyHostToDevice));
+    GDX_CUDA(cudaMemcpy(X.peer_ctr.get(), pk.data(), pk.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    X.err.alloc(1);
+    GDX_CUDA(cudaMemset(X.err.get(), 0, sizeof(int)));
+}
+
 extern "C" int gdx_pr_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, void* handle_out) {
     return guard_impl([&] {
         if (!g || !g->pr_shard || !handle_out || world < 1 || rank < 0 || rank >= world)
@@ -757,26 +909,53 @@ extern "C" int gdx_pr_p2p_open(gdx_graph* g, const void* handles) {
             GDX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
             X.bases[q] = static_cast<double*>(p);
         }
-        std::vector<double*> pc(2 * X.world), ps(2 * X.world);
-        std::vector<unsigned long long*> pk(X.world);
-        for (int q = 0; q < X.world; ++q) {
-            double* b = X.bases[q];
-            for (int par = 0; par < 2; ++par) {
-                pc[par * X.world + q] = b + par * X.n;
-                ps[par * X.world + q] = b + 2 * X.n + (par * X.world + X.rank) * 2;
-            }
-            pk[q] = reinterpret_cast<unsigned long long*>(b + 2 * X.n + 4 * X.world);
-        }
-        X.peer_contrib.alloc(pc.size());
-        X.peer_slot.alloc(ps.size());
-        X.peer_ctr.alloc(pk.size());
-        GDX_CUDA(cudaMemcpy(X.peer_contrib.get(), pc.data(), pc.size() * sizeof(double*), cudaMemcpyHostToDevice));
-        GDX_CUDA(cudaMemcpy(X.peer_slot.get(), ps.data(), ps.size() * sizeof(double*), cudaMemcpyHostToDevice));
-        GDX_CUDA(cudaMemcpy(X.peer_ctr.get(), pk.data(), pk.size() * sizeof(void*), cudaMemcpyHostToDevice));
-        X.err.alloc(1);
-        GDX_CUDA(cudaMemset(X.err.get(), 0, sizeof(int)));
+        p2p_tables(X);
     });
 }
+
+namespace gdx {
+// In-process peers (gdx_pagerank_multi): the exchange blocks of the other
+// devices of a context are plain device pointers (peer access enabled), not
+// IPC mappings.  Same protocol and kernels as the one-process-per-GPU path.
+void pr_p2p_local_setup(gdx_graph* g, int32_t world, int32_t rank) {
+    GraphScope dg(g);
+    if (!g->pr_shard) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no shard plan");
+    auto X = std::make_unique<PrP2P>();
+    X->world = world;
+    X->rank = rank;
+    X->n = g->n;
+    X->ipc = false;
+    // everything the rounds allocate, allocated now: when several partitions
+    // share one GPU, an allocation made while another partition's wait kernel
+    // spins would serialise behind it (implicit synchronisation)
+    g->pr_shard->flags.ensure(kFlagRing);
+    // and every kernel of the rounds loaded (lazy module loading would wait
+    // for a spinning wait kernel of another partition of the same GPU)
+    {
+        cudaFuncAttributes fa;
+        const void* fns[] = {reinterpret_cast<const void*>(&k_pr_shard_init),
+                             reinterpret_cast<const void*>(&k_pr_edges<true>),
+                             reinterpret_cast<const void*>(&k_pr_cross),
+                             reinterpret_cast<const void*>(&k_pr_vertices<true>),
+                             reinterpret_cast<const void*>(&k_p2p_wait),
+                             reinterpret_cast<const void*>(&k_p2p_publish),
+                             reinterpret_cast<const void*>(&k_p2p_combine)};
+        for (const void* f : fns) GDX_CUDA(cudaFuncGetAttributes(&fa, f));
+    }
+    GDX_CUDA(cudaMalloc(&X->block, X->bytes()));
+    GDX_CUDA(cudaMemset(X->block, 0, X->bytes()));
+    g->pr_p2p = std::move(X);
+}
+
+double* pr_p2p_block(gdx_graph* g) { return g->pr_p2p ? g->pr_p2p->block : nullptr; }
+
+void pr_p2p_local_open(gdx_graph* g, const std::vector<double*>& blocks) {
+    GraphScope dg(g);
+    auto& X = *g->pr_p2p;
+    X.bases = blocks;
+    p2p_tables(X);
+}
+}  // namespace gdx
 
 // Waits for every rank's publish `j`, then sums the partial slots of parity j & 1.
 static void p2p_gather_partials(gdx_graph* g, PrP2P& X, int64_t j, double* out2) {
@@ -853,6 +1032,7 @@ extern "C" int gdx_pr_p2p_round(gdx_graph* g, int32_t round, double damping, dou
         GDX_LAUNCH_CHECK();
         if (P.ngroups > 0)
             timed_launch(g, "pr_edges", [&] { k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round); });
+        launch_cross(g, P, a, round);
         timed_launch(g, "pr_vertices", [&] {
             k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
                                              g->num_sms * 8),
@@ -896,6 +1076,7 @@ extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, dou
             a.npeers = X.world;
             if (P.ngroups > 0)
                 timed_launch(g, "pr_edges", [&] { k_pr_edges<true><<<P.grid, P.block, 0, s>>>(a, round); });
+            launch_cross(g, P, a, round);
             timed_launch(g, "pr_vertices", [&] {
                 k_pr_vertices<true><<<blocks_for(std::max(P.v_end - P.v_begin, 1), 2 * kPrBlock,
                                                  g->num_sms * 8),

@@ -22,6 +22,11 @@ struct PrPlan {
     DevBuf<int2> nz;                      // non-empty rows of the reverse CSR: (vertex, end)
     DevBuf<int2> grp;                     // per 8-edge group: (nz index of its first row, its end)
     DevBuf<double> row_sum;               // per-vertex gather sums (zero between rounds)
+    DevBuf<double> head_part, tail_part;  // per 256-edge chunk: partials of rows crossing chunks
+    DevBuf<int4> cross, cross_long;       // crossing rows (row, first chunk, last chunk): short, hub
+    int32_t ncross = 0, nlong = 0;
+    DevBuf<double> dang_part;             // per-block dangling partials (ordered grid sum)
+    DevBuf<unsigned int> dang_ctr;
     int32_t v_begin = 0, v_end = 0;       // row range of the plan
     int64_t e_begin = 0, e_end = 0, e_base = 0, ngroups = 0;
     bool shard = false;                   // built by gdx_pr_shard_setup
@@ -41,6 +46,7 @@ struct PrP2P {
     DevBuf<unsigned long long*> peer_ctr;  // [world]
     DevBuf<int> err;                    // set by a timed-out wait
     int64_t publishes = 0;              // publishes so far (identical on every rank)
+    bool ipc = true;                    // peers opened through CUDA IPC (else in-process pointers)
     double* own_contrib(int par) const { return block + par * n; }
     double* own_partials(int par) const { return block + 2 * n + par * world * 2; }
     unsigned long long* own_ctr() const {
@@ -48,8 +54,9 @@ struct PrP2P {
     }
     size_t bytes() const { return (2 * size_t(n) + 4 * size_t(world) + 1) * sizeof(double); }
     ~PrP2P() {
-        for (int q = 0; q < int(bases.size()); ++q)
-            if (q != rank && bases[q]) cudaIpcCloseMemHandle(bases[q]);
+        if (ipc)
+            for (int q = 0; q < int(bases.size()); ++q)
+                if (q != rank && bases[q]) cudaIpcCloseMemHandle(bases[q]);
         if (block) cudaFree(block);
     }
 };
@@ -73,12 +80,21 @@ struct SsspWork {
     DevBuf<int32_t> shard_mark;  // delta mode: round in which a vertex was last listed as changed
     int32_t shard_round = 0;
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
-    static constexpr int kKey = 9;
+    static constexpr int kKey = 10;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     void* gkey[2][kKey] = {};
     DevBuf<unsigned long long> graph_acc;  // [rounds, vertices, edges, overflow]
+    DevBuf<unsigned long long> upd_slots;  // U counter slots (sssp.cu block_count)
+    // in-process multi-GPU rounds (gdx_sssp_multi): barrier state and the
+    // instantiated round loop per distance width
+    DevBuf<unsigned long long> msync;
+    DevBuf<void*> mpeers;
+    cudaGraphExec_t mexec[2] = {nullptr, nullptr};
+    std::vector<void*> mkey[2];
     ~SsspWork() {
         for (auto& e : gexec)
+            if (e) cudaGraphExecDestroy(e);
+        for (auto& e : mexec)
             if (e) cudaGraphExecDestroy(e);
     }
 };

@@ -262,8 +262,32 @@ __global__ void __launch_bounds__(kSsspBlock) k_sssp_rounds(SsspArgs<D> a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr[kRounds] = r + 1;
 }
 
+// SURVEY 8(d)'s U counter: every lane adds its own count with one relaxed
+// atomic into one of kUpdSlots counters at the end of the kernel.  Same-box
+// A/B on C5 (relaxation without any counter: 20.8 ms): one global counter hit
+// by every warp 23.0 ms, a block-wide __syncthreads reduction 22.3 ms, a warp
+// __reduce_add_sync (its reconvergence region spans the whole item loop)
+// 22.9 ms, per-lane atomics 21.0 ms.  The slots are zeroed by the call's init
+// kernel and summed by its widen kernel (sum_slots).
+constexpr int kUpdSlots = 1024;
+__device__ inline void warp_count(unsigned int v, unsigned long long* slots) {
+    if (v) atomicAdd(&slots[(blockIdx.x * blockDim.x + threadIdx.x) & (kUpdSlots - 1)],
+                     (unsigned long long)v);
+}
+
+// One warp: *out = sum of the kUpdSlots slots.
+__device__ inline void sum_slots(const unsigned long long* slots, unsigned long long* out) {
+    unsigned long long v = 0;
+    for (int i = threadIdx.x; i < kUpdSlots; i += 32) v += slots[i];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) *out = v;
+}
+
 template <class D>
-__global__ void k_sssp_widen(int32_t n, const D* __restrict__ dist, D inf, int64_t* __restrict__ out) {
+__global__ void k_sssp_widen(int32_t n, const D* __restrict__ dist, D inf, int64_t* __restrict__ out,
+                             const unsigned long long* slots = nullptr,
+                             unsigned long long* slots_sum = nullptr) {
+    if (slots && blockIdx.x == 0 && threadIdx.x < 32) sum_slots(slots, slots_sum);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         D d = dist[i];
@@ -485,6 +509,7 @@ static int frontier_grid(const gdx_graph* g, int64_t cnt) {
     return blocks_for(cnt, kFBlock * 8, g->num_sms * per_sm);
 }
 
+
 // Relaxation: one warp per item (<= kShardChunk out-edges of one vertex), lanes
 // over the edges; 32-bit distances flag an overflow (ctr[2]) instead of
 // wrapping -- the caller then reruns with 64-bit distances.
@@ -545,10 +570,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
                 }
             }
     }
-    if (upd) {
-        issued = __reduce_add_sync(0xffffffffu, issued);
-        if ((threadIdx.x & 31) == 0 && issued) atomicAdd(upd, (unsigned long long)issued);
-    }
+    if (upd) warp_count(issued, upd);
 }
 
 // (id, value) pairs of the vertices listed by a delta relaxation.
@@ -575,10 +597,13 @@ __global__ void k_sssp_delta_apply(const int32_t* __restrict__ ids, const D* __r
 
 template <class D>
 __global__ void k_sssp_scan_init(int32_t n, int32_t src, D inf, D* dist, D* prev,
-                                 unsigned long long* z0, int nz0, unsigned long long* z1, int nz1) {
-    // also zeroes the call's counters (z0[0, nz0), z1[0, nz1)): no memsets
+                                 unsigned long long* z0, int nz0, unsigned long long* z1, int nz1,
+                                 unsigned long long* slots) {
+    // also zeroes the call's counters (z0[0, nz0), z1[0, nz1), the U slots): no memsets
     if (blockIdx.x == 0 && threadIdx.x < nz0) z0[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x < nz1) z1[threadIdx.x] = 0;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < kUpdSlots; i += blockDim.x) slots[i] = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         dist[i] = i == src ? D(0) : inf;
@@ -629,7 +654,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
             : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
     fn<<<relax_grid, 256, 0, cs>>>(w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
                                    g->weighted ? g->weights.get() : nullptr, dist, ovf, SsspDelta{},
-                                   ctr + kUpdSlot);
+                                   w.upd_slots.get());
     k_sssp_graph_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), h);
     cudaGraph_t captured;
     GDX_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -656,6 +681,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
     w.shard_queue.ensure(items_cap);
     w.shard_ctr.ensure(kUpdSlot + 1);
+    w.upd_slots.ensure(kUpdSlots);
     unsigned long long* ctr = w.shard_ctr.get();
     // graph path: round counters, [rounds, vertices, edges, overflow] in
     // graph_acc; host loop: its own overflow flag
@@ -665,7 +691,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     timed_launch(g, "sssp_init", [&] {
         k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
             n, src, inf, dist, prev, ctr, kUpdSlot + 1, use_graph ? w.graph_acc.get() : ovf.get(),
-            use_graph ? 4 : 1);
+            use_graph ? 4 : 1, w.upd_slots.get());
     });
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     unsigned long long vvis = 0, evis = 0;
@@ -685,7 +711,8 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         void* key[SsspWork::kKey] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get(),
                                      g->offsets.get(), g->dests.get(),
                                      g->weighted ? g->weights.get() : nullptr,
-                                     reinterpret_cast<void*>(intptr_t(lpi * 65536 + relax_grid))};
+                                     reinterpret_cast<void*>(intptr_t(lpi * 65536 + relax_grid)),
+                                     w.upd_slots.get()};
         bool same = w.gexec[di] != nullptr;
         for (int i = 0; i < SsspWork::kKey; ++i) same = same && w.gkey[di][i] == key[i];
         if (!same) {
@@ -713,7 +740,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
             fn<<<relax_grid, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
                                                g->dests.get(),
                                                g->weighted ? g->weights.get() : nullptr, dist,
-                                               ovf.get(), SsspDelta{}, ctr + kUpdSlot);
+                                               ovf.get(), SsspDelta{}, w.upd_slots.get());
         });
         ++launches;
     }
@@ -724,7 +751,8 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     if (!dev_out) w.queue[1].ensure(size_t(n));
     int64_t* target = dev_out ? dist_out : reinterpret_cast<int64_t*>(w.queue[1].get());
     timed_launch(g, "sssp_widen", [&] {
-        k_sssp_widen<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(n, dist, inf, target);
+        k_sssp_widen<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
+            n, dist, inf, target, w.upd_slots.get(), ctr + kUpdSlot);
     });
     if (!dev_out) copy_out(g, dist_out, target, size_t(n) * sizeof(int64_t));
     // one host read per call: the graph path's counters and the overflow flag
@@ -959,3 +987,355 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         }
     });
 }
+
+// ---------------------------------------------------------------------------
+// Multi-GPU SSSP in one process (gdx_sssp_multi, multi.cu): owner-computes
+// with the exchange fused into the relaxation.  Device d owns the vertex range
+// [bound[d], bound[d+1]) and keeps a full distance replica whose owned entries
+// are authoritative and whose other entries are hints (never below the
+// owner's value).  Its relaxation sends every improving candidate straight to
+// the owner's replica with a peer atomicMin over NVLink (and to its own hint),
+// so there is no all-gather / all-reduce of distance vectors at all.  Rounds
+// run on each device in a CUDA-graph WHILE loop; two device-side barriers per
+// round (arrival counters bumped with system-scope atomics in every device's
+// memory) separate the scan from the relaxation and the relaxation from the
+// next scan, and the scan's item counts are summed across devices at the
+// first barrier so every device leaves the loop in the same round.
+// ---------------------------------------------------------------------------
+namespace gdx {
+
+constexpr int kMaxMultiDev = 16;
+
+struct MultiSync {              // one per device, in that device's memory
+    unsigned long long bar;       // barrier arrivals from all devices (monotonic)
+    unsigned long long cum;       // frontier items published by all devices (monotonic)
+    unsigned long long phase;     // barriers this device has passed
+    unsigned long long prev_cum;  // cum at the previous snapshot
+    unsigned long long total;     // this round's frontier items over all devices
+    unsigned long long err;       // a wait timed out
+    unsigned long long pad[2];
+};
+
+struct SsspOwners {
+    void* dist[kMaxMultiDev];     // every device's replica (D*)
+    int32_t bound[kMaxMultiDev + 1];
+    int32_t nd, self;
+};
+
+__global__ void k_multi_arrive(const unsigned long long* items, MultiSync* const* peers, int nd) {
+    if (items) {
+        const unsigned long long v = *items;
+        for (int q = 0; q < nd; ++q) atomicAdd_system(&peers[q]->cum, v);
+    }
+    __threadfence_system();
+    for (int q = 0; q < nd; ++q) atomicAdd_system(&peers[q]->bar, 1ull);
+}
+
+__global__ void k_multi_wait(MultiSync* me, int nd, int snapshot) {
+    const unsigned long long target = (me->phase + 1) * (unsigned long long)nd;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*reinterpret_cast<volatile unsigned long long*>(&me->bar) < target) {
+        __nanosleep(128);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {  // 20 s: a device died; fail instead of hanging
+            me->err = 1;
+            break;
+        }
+    }
+    me->phase += 1;
+    __threadfence_system();
+    if (snapshot) {
+        const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(&me->cum);
+        me->total = me->err ? 0 : c - me->prev_cum;
+        me->prev_cum = c;
+    }
+}
+
+__global__ void k_multi_finish(unsigned long long* ctr, unsigned long long* acc, const MultiSync* me,
+                               cudaGraphConditionalHandle h) {
+    const unsigned long long total = me->total;
+    if (total) acc[0] += 1;
+    acc[1] += ctr[3];
+    acc[2] += ctr[4];
+    for (int i = 0; i < 5; ++i) ctr[i] = 0;
+    cudaGraphSetConditional(h, total ? 1u : 0u);
+}
+
+template <class D>
+__global__ void k_multi_init(int32_t n, int32_t src, D inf, D* dist, D* prev,
+                             unsigned long long* ctr, int nctr, unsigned long long* acc, int nacc,
+                             unsigned long long* slots) {
+    if (blockIdx.x == 0 && threadIdx.x < nctr) ctr[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < nacc) acc[threadIdx.x] = 0;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < kUpdSlots; i += blockDim.x) slots[i] = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        dist[i] = i == src ? D(0) : inf;
+        prev[i] = inf;
+    }
+}
+
+// The relaxation of k_sssp_scan_relax with the owner routing: an improving
+// candidate for u goes to the owner's replica (peer atomicMin) and to the
+// local hint.  Hints never drop below the owner's value, so the filter
+// c < dist[u] (local) never drops a candidate the owner needs.
+template <class D, int LPI>
+__global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict__ queue,
+                                                          const unsigned long long* __restrict__ ctr,
+                                                          const int32_t* __restrict__ offsets,
+                                                          const int32_t* __restrict__ dests,
+                                                          const int32_t* __restrict__ weights,
+                                                          D* dist, unsigned long long* ovf,
+                                                          unsigned long long* upd, SsspOwners own) {
+    const int sub = threadIdx.x & (LPI - 1);
+    constexpr int kU = kShardChunk / LPI;
+    unsigned int issued = 0;
+    const unsigned long long nq = ctr[0];
+    for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
+         i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
+        const int2 it = queue[i];
+        const D dv = dist[it.x];
+        const int32_t e1 = int32_t(min(int64_t(it.y) + kShardChunk, int64_t(offsets[it.x + 1])));
+        int32_t u[kU];
+        D c[kU], du[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const int32_t e = it.y + sub + k * LPI;
+            u[k] = e < e1 ? dests[e] : -1;
+            const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
+            c[k] = dv + w;
+            if (sizeof(D) == 4 && u[k] >= 0 && dv > std::numeric_limits<D>::max() - D(1) - w) {
+                *ovf = 1;
+                u[k] = -1;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) du[k] = u[k] >= 0 ? dist[u[k]] : D(0);
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+            if (u[k] >= 0 && c[k] < du[k]) {
+                ++issued;
+                int q = 0;
+                while (q + 1 < own.nd && u[k] >= own.bound[q + 1]) ++q;
+                if (q != own.self) atomicMin(static_cast<D*>(own.dist[q]) + u[k], c[k]);
+                atomicMin(&dist[u[k]], c[k]);
+            }
+    }
+    warp_count(issued, upd);
+}
+
+template <class D>
+static cudaGraphExec_t build_multi_graph(gdx_graph* g, D* dist, D* prev, int32_t v0, int32_t v1,
+                                         MultiSync* me, MultiSync* const* peers, int nd,
+                                         const SsspOwners& own, int relax_grid) {
+    auto& w = *g->sssp;
+    cudaGraph_t graph;
+    GDX_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    GDX_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    GDX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    cudaStream_t cs;
+    GDX_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    GDX_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    unsigned long long* ctr = w.shard_ctr.get();
+    k_sssp_scan_frontier<D><<<frontier_grid<D>(g, int64_t(v1) - v0), kFBlock, 0, cs>>>(
+        v0, v1, g->offsets.get(), dist, prev, w.shard_queue.get(), ctr);
+    k_multi_arrive<<<1, 1, 0, cs>>>(ctr, peers, nd);
+    k_multi_wait<<<1, 1, 0, cs>>>(me, nd, 1);
+    k_sssp_multi_relax<D, 16><<<relax_grid, 256, 0, cs>>>(
+        w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
+        g->weighted ? g->weights.get() : nullptr, dist, w.graph_acc.get() + 3, w.upd_slots.get(), own);
+    k_multi_arrive<<<1, 1, 0, cs>>>(nullptr, peers, nd);
+    k_multi_wait<<<1, 1, 0, cs>>>(me, nd, 0);
+    k_multi_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), me, h);
+    cudaGraph_t captured;
+    GDX_CUDA(cudaStreamEndCapture(cs, &captured));
+    GDX_CUDA(cudaStreamDestroy(cs));
+    cudaGraphExec_t exec;
+    GDX_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    GDX_CUDA(cudaGraphDestroy(graph));
+    return exec;
+}
+
+// With lazy module loading (the CUDA 12 default) a kernel's first launch
+// loads its module, which waits for the work running on the device: a
+// partition whose first launch comes while another partition of the same GPU
+// spins in a barrier would deadlock until the barrier times out.  Every
+// kernel of the multi-GPU rounds is loaded up front.
+template <class D>
+static void preload_multi_kernels() {
+    cudaFuncAttributes fa;
+    const void* fns[] = {
+        reinterpret_cast<const void*>(&k_multi_init<D>),
+        reinterpret_cast<const void*>(&k_sssp_scan_frontier<D>),
+        reinterpret_cast<const void*>(&k_sssp_multi_relax<D, 16>),
+        reinterpret_cast<const void*>(&k_sssp_widen<D>),
+        reinterpret_cast<const void*>(&k_multi_arrive),
+        reinterpret_cast<const void*>(&k_multi_wait),
+        reinterpret_cast<const void*>(&k_multi_finish)};
+    for (const void* f : fns) GDX_CUDA(cudaFuncGetAttributes(&fa, f));
+}
+
+// One distance width over all devices; true if any device's 32-bit distances
+// overflowed.  Everything is enqueued before anything is waited on (the
+// devices' barriers need every device's work in flight).
+template <class D>
+static bool sssp_multi_width(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& bound,
+                             int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    const int nd = int(gs.size());
+    const int di = sizeof(D) == 4 ? 0 : 1;
+    const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
+    SsspOwners own{};
+    own.nd = nd;
+    for (int q = 0; q < nd; ++q) own.dist[q] = gs[q]->sssp->dist.get();
+    for (int q = 0; q <= nd; ++q) own.bound[q] = bound[q];
+    for (int d = 0; d < nd; ++d) {
+        DeviceGuard dg(gs[d]->device);
+        preload_multi_kernels<D>();
+    }
+    // instantiate every device's loop before any device's work is enqueued
+    // (graph instantiation next to a spinning barrier kernel of another
+    // partition on the same GPU would wait for it)
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        auto& w = *g->sssp;
+        const int32_t v0 = bound[d], v1 = bound[d + 1];
+        D* dist = reinterpret_cast<D*>(w.dist.get());
+        D* prev = reinterpret_cast<D*>(w.prev.get());
+        MultiSync* me = reinterpret_cast<MultiSync*>(w.msync.get());
+        MultiSync* const* peers = reinterpret_cast<MultiSync* const*>(w.mpeers.get());
+        own.self = d;
+        const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
+        // the instantiated loop bakes in this device's buffers, the range and
+        // every device's replica
+        std::vector<void*> key = {dist, prev, w.shard_queue.get(), w.shard_ctr.get(),
+                                  w.graph_acc.get(), me, w.mpeers.get(), w.upd_slots.get(),
+                                  g->offsets.get(),
+                                  g->dests.get(), g->weighted ? g->weights.get() : nullptr,
+                                  reinterpret_cast<void*>(intptr_t(v0)),
+                                  reinterpret_cast<void*>(intptr_t(v1))};
+        for (int q = 0; q < nd; ++q) key.push_back(own.dist[q]);
+        if (!w.mexec[di] || w.mkey[di] != key) {
+            if (w.mexec[di]) cudaGraphExecDestroy(w.mexec[di]);
+            w.mexec[di] = build_multi_graph<D>(g, dist, prev, v0, v1, me, peers, nd, own, relax_grid);
+            w.mkey[di] = key;
+        }
+    }
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        auto& w = *g->sssp;
+        cudaStream_t s = g->stream;
+        const int32_t v0 = bound[d], v1 = bound[d + 1], n = g->n;
+        D* dist = reinterpret_cast<D*>(w.dist.get());
+        D* prev = reinterpret_cast<D*>(w.prev.get());
+        MultiSync* me = reinterpret_cast<MultiSync*>(w.msync.get());
+        MultiSync* const* peers = reinterpret_cast<MultiSync* const*>(w.mpeers.get());
+        timed_launch(g, "sssp_multi_init", [&] {
+            k_multi_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
+                n, src, inf, dist, prev, w.shard_ctr.get(), kUpdSlot + 1, w.graph_acc.get(), 4,
+                w.upd_slots.get());
+        });
+        // nobody relaxes into this replica before it is initialised
+        k_multi_arrive<<<1, 1, 0, s>>>(nullptr, peers, nd);
+        k_multi_wait<<<1, 1, 0, s>>>(me, nd, 0);
+        GDX_LAUNCH_CHECK();
+        timed_launch(g, "sssp_multi_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.mexec[di], s)); });
+        timed_launch(g, "sssp_widen", [&] {
+            k_sssp_widen<D><<<blocks_for(v1 - v0, 256, g->num_sms * 8), 256, 0, s>>>(
+                v1 - v0, dist + v0, inf, reinterpret_cast<int64_t*>(w.queue[1].get()),
+                w.upd_slots.get(), w.shard_ctr.get() + kUpdSlot);
+        });
+    }
+    bool overflow = false;
+    unsigned long long rounds = 0, vvis = 0, evis = 0, upd = 0;
+    int64_t err = 0;
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        auto& w = *g->sssp;
+        unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+        GDX_CUDA(cudaMemcpyAsync(h, w.graph_acc.get(), 4 * 8, cudaMemcpyDeviceToHost, g->stream));
+        GDX_CUDA(cudaMemcpyAsync(h + 4, w.shard_ctr.get() + kUpdSlot, 8, cudaMemcpyDeviceToHost, g->stream));
+        GDX_CUDA(cudaMemcpyAsync(h + 5, &reinterpret_cast<MultiSync*>(w.msync.get())->err, 8,
+                                 cudaMemcpyDeviceToHost, g->stream));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        overflow |= h[3] != 0;
+        rounds = std::max(rounds, h[0]);
+        vvis += h[1];
+        evis += h[2];
+        upd += h[4];
+        err |= int64_t(h[5]);
+    }
+    if (err) fail(GDX_ERR_CUDA, "CudaError: multi-GPU SSSP barrier timed out");
+    if (overflow) return true;
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        copy_out(g, dist_out + bound[d], g->sssp->queue[1].get(),
+                 size_t(bound[d + 1] - bound[d]) * sizeof(int64_t));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+    }
+    if (stats) {
+        stats->rounds = int32_t(rounds);
+        stats->launches = int32_t(nd * (4 + 6 * (rounds + 1)));
+        stats->vertices_visited = int64_t(vvis);
+        stats->edges_visited = int64_t(evis);
+        stats->updates = int64_t(upd);
+        stats->algorithmic_bytes = 16.0 * vvis + 12.0 * evis + 8.0 * upd;
+    }
+    return false;
+}
+
+void sssp_multi(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& bound, int32_t src,
+                int64_t* dist_out, gdx_stats* stats) {
+    const int nd = int(gs.size());
+    if (nd < 1 || nd > kMaxMultiDev) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: device count");
+    for (int d = 0; d < nd; ++d) {  // workspaces first: every device's replica address is needed
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
+        auto& w = *g->sssp;
+        const int32_t v0 = bound[d], v1 = bound[d + 1];
+        w.dist.ensure(size_t(g->n));
+        w.prev.ensure(size_t(g->n));
+        w.queue[1].ensure(size_t(std::max(v1 - v0, 1)));
+        std::vector<int32_t> off(2);
+        if (v1 > v0) {
+            GDX_CUDA(cudaMemcpy(&off[0], g->offsets.get() + v0, 4, cudaMemcpyDeviceToHost));
+            GDX_CUDA(cudaMemcpy(&off[1], g->offsets.get() + v1, 4, cudaMemcpyDeviceToHost));
+        }
+        w.shard_queue.ensure(size_t(v1 - v0) + size_t(int64_t(off[1]) - off[0]) / kShardChunk + 1);
+        w.shard_ctr.ensure(kUpdSlot + 1);
+        w.upd_slots.ensure(kUpdSlots);
+        w.graph_acc.ensure(4);
+        if (!w.msync.get()) {
+            w.msync.alloc(sizeof(MultiSync) / 8);
+            GDX_CUDA(cudaMemset(w.msync.get(), 0, sizeof(MultiSync)));
+        }
+    }
+    std::vector<MultiSync*> peers(nd);
+    for (int d = 0; d < nd; ++d) peers[d] = reinterpret_cast<MultiSync*>(gs[d]->sssp->msync.get());
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = gs[d];
+        GraphScope sc(g);
+        auto& w = *g->sssp;
+        w.mpeers.ensure(nd);
+        GDX_CUDA(cudaMemcpy(w.mpeers.get(), peers.data(), nd * sizeof(void*), cudaMemcpyHostToDevice));
+    }
+    if (sssp_multi_width<unsigned int>(gs, bound, src, dist_out, stats))
+        sssp_multi_width<unsigned long long>(gs, bound, src, dist_out, stats);
+}
+
+}  // namespace gdx

@@ -371,6 +371,117 @@ class DeviceGraph:
         return out
 
 
+def _prefer_torch_nccl() -> None:
+    """libgdx dlopens NCCL for gdx_context; in a process that also uses torch it
+    must be torch's bundled copy (the first libnccl.so.2 loaded wins the
+    soname, and torch needs its own version's symbols)."""
+    import os
+    if os.environ.get("GDX_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as nn
+        for base in list(nn.__path__):
+            p = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["GDX_NCCL_LIB"] = p
+                return
+    except Exception:
+        pass
+
+
+class Context:
+    """Several GPUs driven from this process (gdx_context: peer access between
+    every pair, one NCCL communicator per distinct device)."""
+
+    def __init__(self, devices: Sequence[int]):
+        _prefer_torch_nccl()
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        self._h = C.c_void_p()
+        check(_lib.load().gdx_context_create(len(devices), devs, C.byref(self._h)))
+        self.devices = [int(d) for d in devices]
+
+    def info(self) -> dict:
+        nd, nc, pa = C.c_int32(), C.c_int32(), C.c_int32()
+        check(_lib.load().gdx_context_info(self._h, C.byref(nd), C.byref(nc), C.byref(pa)))
+        return {"devices": nd.value, "nccl_comms": nc.value, "peer_access": bool(pa.value)}
+
+    def close(self) -> None:
+        if self._h:
+            check(_lib.load().gdx_context_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MultiGraph:
+    """A CsrGraph replicated on every device of a Context; the four entry
+    points partitioned across the devices (gdx_*_multi)."""
+
+    def __init__(self, ctx: Context, g):
+        self.ctx = ctx  # keeps the context alive
+        arrs = {k: _i32(getattr(g, k, None)) for k in
+                ("offsets", "dests", "weights", "rev_offsets", "rev_srcs", "rev_eid")}
+        view = GdxCsrView(int(g.n), int(g.m), int(bool(g.directed)),
+                          *[_ptr(arrs[k]) for k in ("offsets", "dests", "weights", "rev_offsets",
+                                                    "rev_srcs", "rev_eid")])
+        self._h = C.c_void_p()
+        check(_lib.load().gdx_multi_graph_create(ctx._h, C.byref(view), C.byref(self._h)))
+        self.n, self.m, self.directed = int(g.n), int(g.m), bool(g.directed)
+
+    def close(self) -> None:
+        if self._h:
+            check(_lib.load().gdx_multi_graph_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sssp(self, src: int, out=None, stats: Optional[dict] = None):
+        res = out if out is not None else np.empty(self.n, np.int64)
+        st = GdxStats()
+        check(_lib.load().gdx_sssp_multi(self._h, int(src), _ptr(res), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res
+
+    def pagerank(self, damping: float = 0.85, threshold: float = 1e-6, max_iter: int = 100,
+                 out=None, stats: Optional[dict] = None):
+        res = out if out is not None else np.empty(self.n, np.float64)
+        rounds = C.c_int32()
+        st = GdxStats()
+        check(_lib.load().gdx_pagerank_multi(self._h, float(damping), float(threshold),
+                                             int(max_iter), _ptr(res), C.byref(rounds),
+                                             C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res, rounds.value
+
+    def tc(self, stats: Optional[dict] = None) -> int:
+        cnt = C.c_int64()
+        st = GdxStats()
+        check(_lib.load().gdx_tc_multi(self._h, C.byref(cnt), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return cnt.value
+
+    def bc(self, sources: Sequence[int], out=None, stats: Optional[dict] = None):
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
+        res = out if out is not None else np.empty(self.n, np.float64)
+        st = GdxStats()
+        check(_lib.load().gdx_bc_multi(self._h, _ptr(src) if len(src) else None, len(src),
+                                       _ptr(res), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res
+
+
 def gen_uniform_edges(nodes: int, edges: int, seed: int):
     """genUniformEdges (graphgen.cpp:8-16): the reference's edge stream."""
     u = np.empty(int(edges), np.int32)

@@ -119,3 +119,18 @@ def test_tc_plan_cached_and_repeatable(gdx, port):
     assert c1 == c2 == port.tc(a)
     assert st1["algorithmic_bytes"] == st2["algorithmic_bytes"] > 0
     assert st2["launches"] < st1["launches"]
+
+
+def test_pagerank_run_to_run_identical(gdx, port):
+    """No floating-point atomics on the PR path: rows crossing warp chunks and
+    the dangling mass are summed in a fixed order, so repeated calls (and a
+    fresh handle) give bit-identical ranks."""
+    b = _rmat(port, 17, 9, True)
+    dg = gdx.DeviceGraph.from_csr(b)
+    r1, it1 = dg.pagerank(0.85, 1e-9, 110)
+    r2, it2 = dg.pagerank(0.85, 1e-9, 110)
+    r3, it3 = gdx.DeviceGraph.from_csr(b).pagerank(0.85, 1e-9, 110)
+    assert it1 == it2 == it3
+    assert np.array_equal(r1, r2) and np.array_equal(r1, r3)
+    e, ie = port.pr(b, 0.85, 1e-9, 110)
+    assert ie == it1 and rel_err(r1, e) < 1e-9

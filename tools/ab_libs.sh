@@ -15,7 +15,7 @@ d = json.loads(sys.stdin.read())
 for k, x in d['per_algorithm'].items():
     if k != 'pr' or '$algos' == '':
         r = x.get('roofline', {})
-        print('$v', k, round(x['ms_per_step'], 3), 'kernel_ms', r.get('kernel_ms_avg'), 'frac', r.get('frac'))
+        print('$v', k, round(x['ms_per_step'], 3), 'kernel_ms', r.get('kernel_ms_per_unit'), 'frac', r.get('frac'))
 "
 done
 cp /tmp/libgdx_head.so paper_2401_02472_b200/lib/libgdx.so

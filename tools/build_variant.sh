@@ -14,7 +14,7 @@ mkdir -p "$OUT"
 nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr "$@" -c "$CSRC/$unit.cu" -o "$OUT/$unit.$name.o"
 objs=""
-for u in api build sssp pagerank tc bc edgelist; do
+for u in api build sssp pagerank tc bc edgelist refstream multi; do
     if [ "$u" = "$unit" ]; then objs="$objs $OUT/$unit.$name.o"; else objs="$objs $OBJ/$u.o"; fi
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$OUT/libgdx_$name.so" \
