@@ -150,6 +150,8 @@ int gdx_graph_set_hash_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t se
  * the reference's own inputs (parity configs, `graphdsl run --weight-*`):
  *   genUniformEdges (core/src/graphgen.cpp:8-16)   gdx_gen_uniform_edges_ref
  *   genRmatEdges    (core/src/graphgen.cpp:18-56)  gdx_gen_rmat_edges_ref
+ *   gen-graph weight column (tools/graphdsl.cpp:281-287)
+ *                                      gdx_gen_edge_weights_ref
  *   CsrGraph::withRandomWeights (core/src/csr.cpp:172-195)
  *                                      gdx_random_weights_host (host CSR arrays)
  *                                      gdx_graph_set_random_weights (a handle)
@@ -159,6 +161,10 @@ int gdx_graph_set_hash_weights(gdx_graph* g, int32_t lo, int32_t hi, uint64_t se
 int gdx_gen_uniform_edges_ref(int32_t nodes, int64_t edges, uint64_t seed, int32_t* u, int32_t* v);
 int gdx_gen_rmat_edges_ref(int32_t nodes, int64_t edges, uint64_t seed, double a, double b,
                            double c, double d, int32_t* u, int32_t* v);
+/* gen-graph's weight column (tools/graphdsl.cpp:281-287): count draws of
+ * uniform_int<int>(wmin, wmax) from mt19937_64(seed ^ 0x9e3779b97f4a7c15). */
+int gdx_gen_edge_weights_ref(int64_t count, uint64_t seed, int32_t wmin, int32_t wmax,
+                             int32_t* weights_out);
 int gdx_random_weights_host(int32_t n, int32_t m, int32_t directed, const int32_t* offsets,
                             const int32_t* dests, int32_t lo, int32_t hi, uint64_t seed,
                             int32_t* weights_out);
@@ -261,6 +267,23 @@ int gdx_sssp_shard_relax32_delta(gdx_graph* g, int32_t* dist, int32_t* changed_i
                                  int32_t* changed_dist, int64_t* count_out);
 int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t* ids, const int32_t* vals,
                            int64_t count);
+
+/* ---- textbook kernels for `graphdsl check` (textbook.cu) -------------------
+ * The reference's oracles (core/src/oracles.cpp:10-111) as plain topology-
+ * driven device kernels -- one thread per vertex per round / level, a host
+ * round trip per round, nothing shared with the fast paths -- so that `check`
+ * (tools/graphdsl.cpp:175-256) compares two independent device computations:
+ *   oracles::sssp -> gdx_textbook_sssp (Bellman-Ford rounds; same distances)
+ *   oracles::pr   -> gdx_textbook_pr   (<= max_iter iterations, stop when
+ *                                       max |delta| < eps, oracles.cpp:73-92)
+ *   oracles::tc   -> gdx_textbook_tc   (tc.sp's u < v < w by binary search;
+ *                                       no n <= 256 guard)
+ *   oracles::bc   -> gdx_textbook_bc   (level-synchronous Brandes per source)
+ * Sized for check-size graphs, not for the benchmark configurations. */
+int gdx_textbook_sssp(gdx_graph* g, int32_t src, int64_t* dist_out);
+int gdx_textbook_pr(gdx_graph* g, double damping, double eps, int32_t max_iter, double* rank_out);
+int gdx_textbook_tc(gdx_graph* g, int64_t* count_out);
+int gdx_textbook_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out);
 
 /* ---- several GPUs from one process (multi.cu) --------
  * For a C++ caller of interp::run (interpreter.hpp:64-88) that wants an

@@ -271,6 +271,9 @@ class Ref:
         L.ref_interp_pr.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int64, C.c_int,
                                     C.c_int, _f64p, _i64p]
         L.ref_interp_tc.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p]
+        L.ref_gen_graph.argtypes = [C.c_char_p, C.c_int32, C.c_int64, C.c_uint64, C.c_char_p,
+                                    C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                    C.c_double, C.c_char_p, C.c_int]
         L.ref_interp_bc.argtypes = [C.c_void_p, _i32p, C.c_int32, C.c_int, C.c_int, _f64p]
 
     def _check(self, rc):
@@ -310,6 +313,15 @@ class Ref:
         v = np.empty(edges, np.int32)
         self._check(self.lib.ref_gen_rmat_edges(nodes, edges, seed, _p(u), _p(v)))
         return u, v
+
+    def gen_graph_file(self, kind, nodes, edges, seed, path, weighted=False, wmin=1, wmax=100,
+                       a=0.57, b=0.19, c=0.19, d=0.05) -> str:
+        """graphdsl gen-graph (graphdsl.cpp:265-296): writes `path`, returns the
+        summary line it prints."""
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.ref_gen_graph(kind.encode(), nodes, edges, seed, str(path).encode(),
+                                           int(weighted), wmin, wmax, a, b, c, d, buf, 1024))
+        return buf.value.decode()
 
 
 class RefGraph:

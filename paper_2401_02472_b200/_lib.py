@@ -80,6 +80,8 @@ SIGNATURES = {
                                   C.c_int),
     "gdx_gen_rmat_edges_ref": ([C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_double,
                                C.c_double, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_gen_edge_weights_ref": ([C.c_int64, C.c_uint64, C.c_int32, C.c_int32, C.c_void_p],
+                                 C.c_int),
     "gdx_random_weights_host": ([C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_int32, C.c_int32, C.c_uint64, C.c_void_p], C.c_int),
     "gdx_graph_set_random_weights": ([C.c_void_p, C.c_int32, C.c_int32, C.c_uint64], C.c_int),
@@ -109,6 +111,10 @@ SIGNATURES = {
     "gdx_sssp_shard_relax32": ([C.c_void_p, C.c_void_p], C.c_int),
     "gdx_sssp_shard_relax32_delta": ([C.c_void_p] + [C.c_void_p] * 4, C.c_int),
     "gdx_sssp_shard_apply32": ([C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64], C.c_int),
+    "gdx_textbook_sssp": ([C.c_void_p, C.c_int32, C.c_void_p], C.c_int),
+    "gdx_textbook_pr": ([C.c_void_p, C.c_double, C.c_double, C.c_int32, C.c_void_p], C.c_int),
+    "gdx_textbook_tc": ([C.c_void_p, i64p], C.c_int),
+    "gdx_textbook_bc": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p], C.c_int),
     "gdx_context_create": ([C.c_int, C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "gdx_context_destroy": ([C.c_void_p], C.c_int),
     "gdx_context_info": ([C.c_void_p, i32p, i32p, i32p], C.c_int),

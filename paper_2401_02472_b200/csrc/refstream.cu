@@ -118,6 +118,19 @@ int gdx_gen_rmat_edges_ref(int32_t nodes, int64_t edges, uint64_t seed, double a
     });
 }
 
+int gdx_gen_edge_weights_ref(int64_t count, uint64_t seed, int32_t wmin, int32_t wmax,
+                             int32_t* weights_out) {
+    return guard_impl([&] {
+        // graphdsl.cpp:281-287: gen-graph's per-edge weight column
+        if (count < 0 || (count > 0 && !weights_out))
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad weight array");
+        if (wmin > wmax) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: weight range is empty");
+        std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ULL);
+        std::uniform_int_distribution<int> weight(wmin, wmax);
+        for (int64_t i = 0; i < count; ++i) weights_out[i] = weight(rng);
+    });
+}
+
 int gdx_random_weights_host(int32_t n, int32_t m, int32_t directed, const int32_t* offsets,
                             const int32_t* dests, int32_t lo, int32_t hi, uint64_t seed,
                             int32_t* weights_out) {

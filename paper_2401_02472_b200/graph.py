@@ -264,6 +264,30 @@ class DeviceGraph:
             stats.update(st.as_dict())
         return res
 
+    # ---- textbook kernels (oracles.cpp on the device; `check`) ------------------
+    def textbook_sssp(self, src: int) -> np.ndarray:
+        out = np.empty(self.n, np.int64)
+        check(_lib.load().gdx_textbook_sssp(self.handle, int(src), _ptr(out)))
+        return out
+
+    def textbook_pr(self, damping: float, eps: float, max_iter: int) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        check(_lib.load().gdx_textbook_pr(self.handle, float(damping), float(eps), int(max_iter),
+                                          _ptr(out)))
+        return out
+
+    def textbook_tc(self) -> int:
+        c = C.c_int64()
+        check(_lib.load().gdx_textbook_tc(self.handle, C.byref(c)))
+        return c.value
+
+    def textbook_bc(self, sources: Sequence[int]) -> np.ndarray:
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
+        out = np.empty(self.n, np.float64)
+        check(_lib.load().gdx_textbook_bc(self.handle, _ptr(src) if len(src) else None, len(src),
+                                          _ptr(out)))
+        return out
+
     # ---- multi-GPU shards (distributed.py drives the exchange) ------------------
     def pr_shard_setup(self, v_begin: int, v_end: int) -> None:
         check(_lib.load().gdx_pr_shard_setup(self.handle, int(v_begin), int(v_end)))
@@ -498,6 +522,14 @@ def gen_rmat_edges(nodes: int, edges: int, seed: int, a: float = 0.57, b: float 
     check(_lib.load().gdx_gen_rmat_edges_ref(int(nodes), int(edges), int(seed), a, b, c, d,
                                              _ptr(u), _ptr(v)))
     return u, v
+
+
+def gen_edge_weights(count: int, seed: int, wmin: int, wmax: int) -> np.ndarray:
+    """gen-graph's weight column (graphdsl.cpp:281-287)."""
+    w = np.empty(int(count), np.int32)
+    check(_lib.load().gdx_gen_edge_weights_ref(int(count), int(seed), int(wmin), int(wmax),
+                                               _ptr(w)))
+    return w
 
 
 def random_weights(g, lo: int, hi: int, seed: int) -> np.ndarray:

@@ -67,3 +67,114 @@ def test_edge_list_round_trip_and_run(tmp_path, port):
                         str(out)], capture_output=True, text=True, cwd=ROOT, timeout=300)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip().splitlines()[-1] == f"return\t{g.tc()}"
+
+
+def _cli(*args, timeout=600):
+    return subprocess.run([sys.executable, "-m", "paper_2401_02472_b200", *map(str, args)],
+                          capture_output=True, text=True, cwd=ROOT, timeout=timeout)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,weighted", [("rmat", True), ("uniform", False)])
+def test_gen_graph_byte_identical_to_reference(tmp_path, ref, kind, weighted):
+    """gen-graph writes the reference's file and summary line
+    (graphdsl.cpp:265-296; restated over the reference library by the shim)."""
+    ours, theirs = tmp_path / "ours.txt", tmp_path / "ref.txt"
+    extra = ["--weighted", "--weight-min", "3", "--weight-max", "40"] if weighted else []
+    r = _cli("gen-graph", "--kind", kind, "--nodes", 700, "--edges", 5000, "--seed", 11, "--out",
+             ours, *extra)
+    assert r.returncode == 0, r.stderr
+    summary = ref.gen_graph_file(kind, 700, 5000, 11, theirs, weighted, 3, 40)
+    assert ours.read_bytes() == theirs.read_bytes()
+    assert r.stdout == summary.replace(str(theirs), str(ours))
+
+
+@pytest.mark.gpu
+def test_run_weight_options_match_with_random_weights(tmp_path, port):
+    """run --weight-min/--weight-max/--weight-seed = CsrGraph::withRandomWeights
+    (graphdsl.cpp:148-149, csr.cpp:172-195): the distances of the reweighted graph."""
+    p = tmp_path / "g.txt"
+    assert _cli("gen-graph", "--kind", "rmat", "--nodes", 512, "--edges", 4096, "--out",
+                p).returncode == 0
+    r = _cli("run", "sssp.sp", "--graph", p, "--arg", "src=3", "--weight-min", 1, "--weight-max",
+             50, "--weight-seed", 9)
+    assert r.returncode == 0, r.stderr
+    import paper_2401_02472_b200 as gdx
+    g = gdx.DeviceGraph.load_edge_list(str(p), directed=False)
+    h = g.download()
+    from conftest import G
+    exp = port.sssp(port.with_random_weights(G(h.n, h.m, False, h.offsets, h.dests), 1, 50, 9), 3)
+    got = [int(x.split("\t")[2]) for x in r.stdout.splitlines() if x.startswith("dist\t")]
+    assert got == list(exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prog,args", [("sssp.sp", ["--arg", "src=2"]), ("tc.sp", []),
+                                       ("pr.sp", []), ("bc.sp", ["--arg", "sourceSet=0,5,9"])])
+def test_check_passes(tmp_path, prog, args):
+    """check: device fast path vs the textbook kernels, PASS at the corpus
+    tolerance (graphdsl.cpp:175-256)."""
+    p = tmp_path / "g.txt"
+    assert _cli("gen-graph", "--kind", "rmat", "--nodes", 600, "--edges", 5000, "--weighted",
+                "--out", p).returncode == 0
+    directed = ["--directed"] if prog == "pr.sp" else []
+    r = _cli("check", prog, "--graph", p, *directed, *args)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[-1].startswith("PASS (tolerance ")
+    if prog in ("sssp.sp", "tc.sp"):
+        assert lines[-1] == "PASS (tolerance exact)"
+        assert lines[0] == "sssp: max absolute distance error 0" if prog == "sssp.sp" else \
+            lines[0].split()[2] == lines[0].split()[4]
+
+
+@pytest.mark.gpu
+def test_textbook_kernels_match_oracle(gdx, port):
+    n = 1 << 11
+    u, v = port.gen_rmat_edges(n, 16 * n, 12)
+    und = port.with_random_weights(port.build_from_edges(n, u, v, None, False), 1, 100, 12)
+    dr = port.build_from_edges(n, u, v, None, True)
+    g, d = gdx.DeviceGraph.from_csr(und), gdx.DeviceGraph.from_csr(dr)
+    assert np.array_equal(g.textbook_sssp(5), port.sssp(und, 5))
+    assert g.textbook_tc() == port.tc(und) == g.tc()
+    from conftest import rel_err
+    assert rel_err(g.textbook_bc([0, 1, 2]), port.bc(und, [0, 1, 2])) < 1e-12
+    r = d.textbook_pr(0.85, 1e-9, 110)
+    e, _ = port.pr(dr, 0.85, 1e-9, 110)
+    assert np.max(np.abs(r - e)) < 1e-6
+
+
+GOLDEN_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN_DIR, "golden_tc")),
+                    reason="golden units not built (make -C oracle golden-units)")
+def test_units_match_golden_units(tmp_path):
+    """bin/*_b200 keep the emitted units' command line and output
+    (codegen_runtime.cpp:174-296): byte-identical to the reference's own
+    generated CUDA units for SSSP and TC, within 1e-9 for PR and BC."""
+    p = tmp_path / "g.txt"
+    assert _cli("gen-graph", "--kind", "rmat", "--nodes", 900, "--edges", 7000, "--weighted",
+                "--out", p).returncode == 0
+    bins = os.path.join(ROOT, "paper_2401_02472_b200", "bin")
+    cases = [("sssp", ["1", "4"]), ("tc", ["0"]), ("pr", ["1", "0.85", "1e-9", "110"]),
+             ("bc", ["0", "0,3,7,11"])]
+    for algo, args in cases:
+        a = subprocess.run([os.path.join(bins, f"{algo}_b200"), str(p), *args],
+                           capture_output=True, text=True, timeout=300)
+        b = subprocess.run([os.path.join(GOLDEN_DIR, f"golden_{algo}"), str(p), *args],
+                           capture_output=True, text=True, timeout=300)
+        assert a.returncode == 0 == b.returncode, (algo, a.stderr, b.stderr)
+        if algo in ("sssp", "tc"):
+            assert a.stdout == b.stdout, algo
+        else:
+            la, lb = a.stdout.splitlines(), b.stdout.splitlines()
+            assert len(la) == len(lb) and all(x.split("\t")[:2] == y.split("\t")[:2]
+                                              for x, y in zip(la, lb))
+            va = np.array([float(x.split("\t")[2]) for x in la])
+            vb = np.array([float(y.split("\t")[2]) for y in lb])
+            from conftest import rel_err
+            assert rel_err(va, vb) < 1e-9, algo
+    usage = subprocess.run([os.path.join(bins, "tc_b200")], capture_output=True, text=True)
+    assert usage.returncode == 2 and "usage:" in usage.stderr
