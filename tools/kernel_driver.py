@@ -39,9 +39,15 @@ def main():
             print(g.pagerank(0.85, 1e-6, 100)[1])
         graphs_pr = graphs  # noqa: F841
     elif a.algo in ("sssp", "sssp26"):
-        sc = 18 if a.algo == "sssp" else 26
-        g = gdx.DeviceGraph.generate("rmat", 1 << sc, 16 << sc, seed=1, directed=False,
-                                     weights=(1, 100))
+        if a.algo == "sssp":  # C1: the reference's own graph, as bench.py
+            u, v = gdx.gen_rmat_edges(1 << 18, 1 << 22, 1)
+            g = gdx.DeviceGraph.build_from_edges(1 << 18, u, v, None, directed=False)
+            g.profile(True)
+            graphs.append(g)
+            g.set_random_weights(1, 100, 1)
+        else:
+            g = gdx.DeviceGraph.generate("rmat", 1 << 26, 1 << 30, seed=1, directed=False,
+                                         weights=(1, 100))
         for _ in range(a.reps):
             st = {}
             t0 = time.perf_counter()
