@@ -323,6 +323,23 @@ int gdx_tc_multi(gdx_multi_graph* g, int64_t* count_out, gdx_stats* stats);
 int gdx_bc_multi(gdx_multi_graph* g, const int32_t* sources, int32_t nsrc, double* bc_out,
                  gdx_stats* stats);
 
+/* SSSP partitions with one process per GPU over peer memory (the multi-
+ * process form of gdx_sssp_multi; distributed.py sharded_sssp_p2p).  bounds:
+ * world+1 vertex-range bounds partitioning [0, n).  gdx_sssp_p2p_setup
+ * exports this rank's block {distance replica | barrier state}
+ * (handle_out: 64 bytes, a cudaIpcMemHandle_t); the caller all-gathers the
+ * handles in rank order and passes them to gdx_sssp_p2p_open.  Every rank then
+ * calls gdx_sssp_p2p_run with the same source: its partition's relaxations
+ * send improving candidates to the owners' replicas by peer atomicMin, the
+ * rounds and their barriers run on the devices (no per-round collective, no
+ * host round trip), and dist_out (n, host or device) receives the whole
+ * vector read from the owners' replicas.  Bit-exact like gdx_sssp. */
+int gdx_sssp_p2p_setup(gdx_graph* g, int32_t world, int32_t rank, const int32_t* bounds,
+                       void* handle_out);
+int gdx_sssp_p2p_open(gdx_graph* g, const void* handles /* world * 64 bytes */);
+int gdx_sssp_p2p_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats);
+int gdx_sssp_p2p_close(gdx_graph* g);
+
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with
  * CUDA events on the launching stream.  gdx_profile_read reports, per kernel

@@ -86,6 +86,36 @@ int main() {
         e = relerr(a.property(bc.symbols, "bc")->floats, b.property(bc.symbols, "bc")->floats);
         report("ComputeBC" + tag, e < 1e-9, "max rel " + std::to_string(e));
     }
+    // ExecMode::Device over a device list (gdx_context / gdx_*_multi): one GPU,
+    // and device 0 listed twice (two partitions of the same protocol)
+    for (const std::vector<int>& devs : {std::vector<int>{0}, std::vector<int>{0, 0}}) {
+        const int32_t n = 1 << 12;
+        auto edges = genRmatEdges(n, 16 * n, 7);
+        CsrGraph und = CsrGraph::buildFromEdges(n, edges, false).withRandomWeights(1, 100, 7);
+        CsrGraph dir = CsrGraph::buildFromEdges(n, edges, true);
+        gdx_graphdsl::MultiDevice ctx(devs);
+        gdx_graphdsl::MultiGraph mu(ctx, und), md(ctx, dir);
+        std::string tag = " devices x" + std::to_string(devs.size());
+        auto a = interp::run(sssp, und, {{"src", int64_t(7)}}, par);
+        auto b = gdx_graphdsl::run(sssp, mu, {{"src", int64_t(7)}});
+        report("multi ComputeSSSP dist" + tag,
+               a.property(sssp.symbols, "dist")->ints == b.property(sssp.symbols, "dist")->ints);
+        interp::ArgMap prArgs{{"damping", 0.85}, {"threshold", 1e-9}, {"maxIter", int64_t(110)}};
+        a = interp::run(pr, dir, prArgs, par);
+        b = gdx_graphdsl::run(pr, md, prArgs);
+        double e = relerr(a.property(pr.symbols, "rank")->floats, b.property(pr.symbols, "rank")->floats);
+        report("multi ComputePR" + tag,
+               e < 1e-9 && a.scalar(pr.symbols, "iter")->asInt() == b.scalar(pr.symbols, "iter")->asInt(),
+               "max rel " + std::to_string(e));
+        a = interp::run(tc, und, {}, par);
+        b = gdx_graphdsl::run(tc, mu, {});
+        report("multi ComputeTC" + tag, a.returnValue->asInt() == b.returnValue->asInt());
+        std::vector<int32_t> srcs{0, 1, 2, 3, 100, 4095};
+        a = interp::run(bc, und, {{"sourceSet", srcs}}, par);
+        b = gdx_graphdsl::run(bc, mu, {{"sourceSet", srcs}});
+        e = relerr(a.property(bc.symbols, "bc")->floats, b.property(bc.symbols, "bc")->floats);
+        report("multi ComputeBC" + tag, e < 1e-9, "max rel " + std::to_string(e));
+    }
     // interp::run-shaped overload (uploads per call) and error kinds
     CsrGraph tri = CsrGraph::buildFromEdges(3, {{0, 1, 5}, {1, 2, 1}, {0, 2, 7}}, false);
     auto r = gdx_graphdsl::run(sssp, tri, {{"src", int64_t(0)}});

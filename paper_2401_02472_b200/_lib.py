@@ -127,6 +127,10 @@ SIGNATURES = {
     "gdx_tc_multi": ([C.c_void_p, i64p, C.POINTER(GdxStats)], C.c_int),
     "gdx_bc_multi": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)],
                      C.c_int),
+    "gdx_sssp_p2p_setup": ([C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_p2p_open": ([C.c_void_p, C.c_void_p], C.c_int),
+    "gdx_sssp_p2p_run": ([C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),
+    "gdx_sssp_p2p_close": ([C.c_void_p], C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),

@@ -16,6 +16,7 @@ thread_local std::string g_last_error;
 gdx_graph::~gdx_graph() {
     // Plans hold device buffers; release them before the stream goes away.
     pr_p2p.reset();
+    sssp_p2p.reset();
     pr.reset();
     pr_shard.reset();
     sssp.reset();

@@ -159,6 +159,7 @@ struct Profiler {
 struct PrPlan;
 struct PrP2P;
 struct SsspWork;
+struct SsspP2P;
 struct TcPlan;
 struct BcWork;
 
@@ -193,6 +194,7 @@ struct gdx_graph {
     std::unique_ptr<gdx::PrPlan> pr_shard;  // gdx_pr_shard_* (one rank's vertex range)
     std::unique_ptr<gdx::PrP2P> pr_p2p;     // gdx_pr_p2p_* (peer-memory exchange)
     std::unique_ptr<gdx::SsspWork> sssp;
+    std::unique_ptr<gdx::SsspP2P> sssp_p2p;  // gdx_sssp_p2p_* (peer-memory partitions)
     std::unique_ptr<gdx::TcPlan> tc;
     std::unique_ptr<gdx::BcWork> bc;
 

@@ -99,6 +99,24 @@ struct SsspWork {
     }
 };
 
+// Multi-process SSSP partitions over peer memory (sssp.cu gdx_sssp_p2p_*):
+// this rank's exported block {distance replica (8 B per vertex) | barrier
+// state (64 B)} and every rank's block opened through CUDA IPC.
+struct SsspP2P {
+    int32_t world = 0, rank = 0;
+    std::vector<int32_t> bounds;        // world + 1 vertex-range bounds
+    int64_t n = 0;
+    char* block = nullptr;              // own block (plain cudaMalloc: IPC export)
+    std::vector<char*> bases;           // every rank's block (own + opened peers)
+    DevBuf<void*> peer_sync;            // [world] every rank's barrier state
+    size_t bytes() const { return size_t(n) * 8 + 64; }
+    ~SsspP2P() {
+        for (int q = 0; q < int(bases.size()); ++q)
+            if (q != rank && bases[q]) cudaIpcCloseMemHandle(bases[q]);
+        if (block) cudaFree(block);
+    }
+};
+
 // Triangle-counting workspace (tc.cu).
 struct TcPlan {
     DevBuf<unsigned long long> acc;

@@ -28,6 +28,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 
 #include "gdx_internal.cuh"
@@ -1013,7 +1014,8 @@ struct MultiSync {              // one per device, in that device's memory
     unsigned long long prev_cum;  // cum at the previous snapshot
     unsigned long long total;     // this round's frontier items over all devices
     unsigned long long err;       // a wait timed out
-    unsigned long long pad[2];
+    unsigned long long ovf;       // OR of every part's 32-bit overflow flag (this call)
+    unsigned long long pad;
 };
 
 struct SsspOwners {
@@ -1167,6 +1169,32 @@ static cudaGraphExec_t build_multi_graph(gdx_graph* g, D* dist, D* prev, int32_t
     return exec;
 }
 
+// After the loop: every part ORs its 32-bit overflow flag into every part's
+// MultiSync, so all parts take the same 32 -> 64-bit rerun decision.
+__global__ void k_multi_flag(const unsigned long long* ovf, MultiSync* const* peers, int nd) {
+    const unsigned long long f = *ovf ? 1ull : 0ull;
+    if (f)
+        for (int q = 0; q < nd; ++q) atomicOr_system(&peers[q]->ovf, f);
+    __threadfence_system();
+}
+
+__global__ void k_multi_reset(MultiSync* me) { me->ovf = 0; }
+
+// Full distance vector from the owners' replicas (peer loads over NVLink):
+// every range is final once the loop has ended on every part.
+template <class D>
+__global__ void k_multi_gather(int32_t n, SsspOwners own, D inf, int64_t* __restrict__ out,
+                               const unsigned long long* slots, unsigned long long* slots_sum) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) sum_slots(slots, slots_sum);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int q = 0;
+        while (q + 1 < own.nd && i >= own.bound[q + 1]) ++q;
+        const D d = static_cast<const volatile D*>(own.dist[q])[i];
+        out[i] = d == inf ? (INT64_MAX / 2) : int64_t(d);
+    }
+}
+
 // With lazy module loading (the CUDA 12 default) a kernel's first launch
 // loads its module, which waits for the work running on the device: a
 // partition whose first launch comes while another partition of the same GPU
@@ -1180,106 +1208,205 @@ static void preload_multi_kernels() {
         reinterpret_cast<const void*>(&k_sssp_scan_frontier<D>),
         reinterpret_cast<const void*>(&k_sssp_multi_relax<D, 16>),
         reinterpret_cast<const void*>(&k_sssp_widen<D>),
+        reinterpret_cast<const void*>(&k_multi_gather<D>),
         reinterpret_cast<const void*>(&k_multi_arrive),
         reinterpret_cast<const void*>(&k_multi_wait),
-        reinterpret_cast<const void*>(&k_multi_finish)};
+        reinterpret_cast<const void*>(&k_multi_finish),
+        reinterpret_cast<const void*>(&k_multi_flag),
+        reinterpret_cast<const void*>(&k_multi_reset)};
     for (const void* f : fns) GDX_CUDA(cudaFuncGetAttributes(&fa, f));
 }
 
-// One distance width over all devices; true if any device's 32-bit distances
-// overflowed.  Everything is enqueued before anything is waited on (the
-// devices' barriers need every device's work in flight).
+// One partition of a multi-GPU SSSP: its handle and vertex range, its
+// distance replica and barrier state, and this partition's view (device
+// tables) of every partition's barrier state.
+struct MultiPart {
+    gdx_graph* g;
+    int32_t v0, v1;
+    void* dist;               // 8 B per vertex, read as D
+    MultiSync* me;
+    MultiSync* const* peers;  // device table [nd]
+};
+
+// Every kernel loaded and every loop instantiated, before anything of any
+// partition is enqueued (both would wait for another partition's spinning
+// barrier on the same GPU).
 template <class D>
-static bool sssp_multi_width(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& bound,
-                             int32_t src, int64_t* dist_out, gdx_stats* stats) {
-    const int nd = int(gs.size());
+static void multi_prepare(MultiPart& p, SsspOwners own, int nd, int self) {
+    gdx_graph* g = p.g;
+    GraphScope sc(g);
+    preload_multi_kernels<D>();
+    auto& w = *g->sssp;
+    const int di = sizeof(D) == 4 ? 0 : 1;
+    own.self = self;
+    D* dist = static_cast<D*>(p.dist);
+    D* prev = reinterpret_cast<D*>(w.prev.get());
+    const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
+    // the instantiated loop bakes in this partition's buffers, its range and
+    // every partition's replica
+    std::vector<void*> key = {dist, prev, w.shard_queue.get(), w.shard_ctr.get(), w.graph_acc.get(),
+                              p.me, const_cast<MultiSync**>(p.peers), w.upd_slots.get(),
+                              g->offsets.get(), g->dests.get(),
+                              g->weighted ? g->weights.get() : nullptr,
+                              reinterpret_cast<void*>(intptr_t(p.v0)),
+                              reinterpret_cast<void*>(intptr_t(p.v1))};
+    for (int q = 0; q < nd; ++q) key.push_back(own.dist[q]);
+    if (!w.mexec[di] || w.mkey[di] != key) {
+        if (w.mexec[di]) cudaGraphExecDestroy(w.mexec[di]);
+        w.mexec[di] = build_multi_graph<D>(g, dist, prev, p.v0, p.v1, p.me, p.peers, nd, own,
+                                           relax_grid);
+        w.mkey[di] = key;
+    }
+}
+
+// A partition's whole call, enqueued without waiting: init, a barrier (no
+// relaxation lands in a replica before it is initialised), the round loop,
+// the overflow vote and a barrier, then either its own slice widened into
+// out_dev (full = false) or the whole vector gathered from the owners
+// followed by a last barrier (nobody re-initialises a replica being read).
+template <class D>
+static void multi_enqueue(MultiPart& p, SsspOwners own, int nd, int32_t src, bool full,
+                          int64_t* out_dev) {
+    gdx_graph* g = p.g;
+    GraphScope sc(g);
+    auto& w = *g->sssp;
+    cudaStream_t s = g->stream;
     const int di = sizeof(D) == 4 ? 0 : 1;
     const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
-    SsspOwners own{};
-    own.nd = nd;
-    for (int q = 0; q < nd; ++q) own.dist[q] = gs[q]->sssp->dist.get();
-    for (int q = 0; q <= nd; ++q) own.bound[q] = bound[q];
-    for (int d = 0; d < nd; ++d) {
-        DeviceGuard dg(gs[d]->device);
-        preload_multi_kernels<D>();
-    }
-    // instantiate every device's loop before any device's work is enqueued
-    // (graph instantiation next to a spinning barrier kernel of another
-    // partition on the same GPU would wait for it)
-    for (int d = 0; d < nd; ++d) {
-        gdx_graph* g = gs[d];
-        GraphScope sc(g);
-        auto& w = *g->sssp;
-        const int32_t v0 = bound[d], v1 = bound[d + 1];
-        D* dist = reinterpret_cast<D*>(w.dist.get());
-        D* prev = reinterpret_cast<D*>(w.prev.get());
-        MultiSync* me = reinterpret_cast<MultiSync*>(w.msync.get());
-        MultiSync* const* peers = reinterpret_cast<MultiSync* const*>(w.mpeers.get());
-        own.self = d;
-        const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
-        // the instantiated loop bakes in this device's buffers, the range and
-        // every device's replica
-        std::vector<void*> key = {dist, prev, w.shard_queue.get(), w.shard_ctr.get(),
-                                  w.graph_acc.get(), me, w.mpeers.get(), w.upd_slots.get(),
-                                  g->offsets.get(),
-                                  g->dests.get(), g->weighted ? g->weights.get() : nullptr,
-                                  reinterpret_cast<void*>(intptr_t(v0)),
-                                  reinterpret_cast<void*>(intptr_t(v1))};
-        for (int q = 0; q < nd; ++q) key.push_back(own.dist[q]);
-        if (!w.mexec[di] || w.mkey[di] != key) {
-            if (w.mexec[di]) cudaGraphExecDestroy(w.mexec[di]);
-            w.mexec[di] = build_multi_graph<D>(g, dist, prev, v0, v1, me, peers, nd, own, relax_grid);
-            w.mkey[di] = key;
-        }
-    }
-    for (int d = 0; d < nd; ++d) {
-        gdx_graph* g = gs[d];
-        GraphScope sc(g);
-        auto& w = *g->sssp;
-        cudaStream_t s = g->stream;
-        const int32_t v0 = bound[d], v1 = bound[d + 1], n = g->n;
-        D* dist = reinterpret_cast<D*>(w.dist.get());
-        D* prev = reinterpret_cast<D*>(w.prev.get());
-        MultiSync* me = reinterpret_cast<MultiSync*>(w.msync.get());
-        MultiSync* const* peers = reinterpret_cast<MultiSync* const*>(w.mpeers.get());
-        timed_launch(g, "sssp_multi_init", [&] {
-            k_multi_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-                n, src, inf, dist, prev, w.shard_ctr.get(), kUpdSlot + 1, w.graph_acc.get(), 4,
-                w.upd_slots.get());
-        });
-        // nobody relaxes into this replica before it is initialised
-        k_multi_arrive<<<1, 1, 0, s>>>(nullptr, peers, nd);
-        k_multi_wait<<<1, 1, 0, s>>>(me, nd, 0);
-        GDX_LAUNCH_CHECK();
-        timed_launch(g, "sssp_multi_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.mexec[di], s)); });
+    const int32_t n = g->n;
+    D* dist = static_cast<D*>(p.dist);
+    D* prev = reinterpret_cast<D*>(w.prev.get());
+    k_multi_reset<<<1, 1, 0, s>>>(p.me);
+    timed_launch(g, "sssp_multi_init", [&] {
+        k_multi_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
+            n, src, inf, dist, prev, w.shard_ctr.get(), kUpdSlot + 1, w.graph_acc.get(), 4,
+            w.upd_slots.get());
+    });
+    k_multi_arrive<<<1, 1, 0, s>>>(nullptr, p.peers, nd);
+    k_multi_wait<<<1, 1, 0, s>>>(p.me, nd, 0);
+    GDX_LAUNCH_CHECK();
+    timed_launch(g, "sssp_multi_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.mexec[di], s)); });
+    k_multi_flag<<<1, 1, 0, s>>>(w.graph_acc.get() + 3, p.peers, nd);
+    k_multi_arrive<<<1, 1, 0, s>>>(nullptr, p.peers, nd);
+    k_multi_wait<<<1, 1, 0, s>>>(p.me, nd, 0);
+    GDX_LAUNCH_CHECK();
+    if (full) {
         timed_launch(g, "sssp_widen", [&] {
-            k_sssp_widen<D><<<blocks_for(v1 - v0, 256, g->num_sms * 8), 256, 0, s>>>(
-                v1 - v0, dist + v0, inf, reinterpret_cast<int64_t*>(w.queue[1].get()),
-                w.upd_slots.get(), w.shard_ctr.get() + kUpdSlot);
+            k_multi_gather<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
+                n, own, inf, out_dev, w.upd_slots.get(), w.shard_ctr.get() + kUpdSlot);
+        });
+        k_multi_arrive<<<1, 1, 0, s>>>(nullptr, p.peers, nd);
+        k_multi_wait<<<1, 1, 0, s>>>(p.me, nd, 0);
+    } else {
+        timed_launch(g, "sssp_widen", [&] {
+            k_sssp_widen<D><<<blocks_for(p.v1 - p.v0, 256, g->num_sms * 8), 256, 0, s>>>(
+                p.v1 - p.v0, dist + p.v0, inf, out_dev, w.upd_slots.get(),
+                w.shard_ctr.get() + kUpdSlot);
         });
     }
+    GDX_LAUNCH_CHECK();
+}
+
+struct MultiResult {
     bool overflow = false;
     unsigned long long rounds = 0, vvis = 0, evis = 0, upd = 0;
-    int64_t err = 0;
-    for (int d = 0; d < nd; ++d) {
+};
+
+// Waits for a partition's call; its counters, the global overflow vote, and
+// a barrier timeout as an error.
+static void multi_collect(MultiPart& p, MultiResult& r) {
+    gdx_graph* g = p.g;
+    GraphScope sc(g);
+    auto& w = *g->sssp;
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
+    GDX_CUDA(cudaMemcpyAsync(h, w.graph_acc.get(), 4 * 8, cudaMemcpyDeviceToHost, g->stream));
+    GDX_CUDA(cudaMemcpyAsync(h + 4, w.shard_ctr.get() + kUpdSlot, 8, cudaMemcpyDeviceToHost,
+                             g->stream));
+    GDX_CUDA(cudaMemcpyAsync(h + 5, &p.me->err, 8, cudaMemcpyDeviceToHost, g->stream));
+    GDX_CUDA(cudaMemcpyAsync(h + 6, &p.me->ovf, 8, cudaMemcpyDeviceToHost, g->stream));
+    GDX_CUDA(cudaStreamSynchronize(g->stream));
+    if (h[5]) fail(GDX_ERR_CUDA, "CudaError: multi-GPU SSSP barrier timed out");
+    r.overflow |= h[6] != 0;
+    r.rounds = std::max(r.rounds, h[0]);
+    r.vvis += h[1];
+    r.evis += h[2];
+    r.upd += h[4];
+}
+
+static void multi_stats(const MultiResult& r, int nd, gdx_stats* stats) {
+    if (!stats) return;
+    stats->rounds = int32_t(r.rounds);
+    stats->launches = int32_t(nd * (8 + 6 * (r.rounds + 1)));
+    stats->vertices_visited = int64_t(r.vvis);
+    stats->edges_visited = int64_t(r.evis);
+    stats->updates = int64_t(r.upd);
+    stats->algorithmic_bytes = 16.0 * r.vvis + 12.0 * r.evis + 8.0 * r.upd;
+}
+
+// The workspaces of one partition (everything the loop bakes in).
+static void multi_workspace(gdx_graph* g, int32_t v0, int32_t v1) {
+    GraphScope sc(g);
+    if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
+    auto& w = *g->sssp;
+    w.prev.ensure(size_t(g->n));
+    std::vector<int32_t> off(2, 0);
+    if (v1 > v0) {
+        GDX_CUDA(cudaMemcpy(&off[0], g->offsets.get() + v0, 4, cudaMemcpyDeviceToHost));
+        GDX_CUDA(cudaMemcpy(&off[1], g->offsets.get() + v1, 4, cudaMemcpyDeviceToHost));
+    }
+    w.shard_queue.ensure(size_t(v1 - v0) + size_t(int64_t(off[1]) - off[0]) / kShardChunk + 1);
+    w.shard_ctr.ensure(kUpdSlot + 1);
+    w.upd_slots.ensure(kUpdSlots);
+    w.graph_acc.ensure(4);
+    w.queue[1].ensure(size_t(std::max(v1 - v0, 1)));
+}
+
+void sssp_multi(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& bound, int32_t src,
+                int64_t* dist_out, gdx_stats* stats) {
+    const int nd = int(gs.size());
+    if (nd < 1 || nd > kMaxMultiDev) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: device count");
+    std::vector<MultiPart> parts(nd);
+    for (int d = 0; d < nd; ++d) {  // workspaces first: every replica's address is needed
         gdx_graph* g = gs[d];
+        multi_workspace(g, bound[d], bound[d + 1]);
         GraphScope sc(g);
         auto& w = *g->sssp;
-        unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
-        GDX_CUDA(cudaMemcpyAsync(h, w.graph_acc.get(), 4 * 8, cudaMemcpyDeviceToHost, g->stream));
-        GDX_CUDA(cudaMemcpyAsync(h + 4, w.shard_ctr.get() + kUpdSlot, 8, cudaMemcpyDeviceToHost, g->stream));
-        GDX_CUDA(cudaMemcpyAsync(h + 5, &reinterpret_cast<MultiSync*>(w.msync.get())->err, 8,
-                                 cudaMemcpyDeviceToHost, g->stream));
-        GDX_CUDA(cudaStreamSynchronize(g->stream));
-        overflow |= h[3] != 0;
-        rounds = std::max(rounds, h[0]);
-        vvis += h[1];
-        evis += h[2];
-        upd += h[4];
-        err |= int64_t(h[5]);
+        w.dist.ensure(size_t(g->n));
+        if (!w.msync.get()) {
+            w.msync.alloc(sizeof(MultiSync) / 8);
+            GDX_CUDA(cudaMemset(w.msync.get(), 0, sizeof(MultiSync)));
+        }
+        parts[d] = MultiPart{g, bound[d], bound[d + 1], w.dist.get(),
+                             reinterpret_cast<MultiSync*>(w.msync.get()), nullptr};
     }
-    if (err) fail(GDX_ERR_CUDA, "CudaError: multi-GPU SSSP barrier timed out");
-    if (overflow) return true;
+    std::vector<MultiSync*> syncs(nd);
+    SsspOwners own{};
+    own.nd = nd;
+    for (int d = 0; d < nd; ++d) {
+        syncs[d] = parts[d].me;
+        own.dist[d] = parts[d].dist;
+    }
+    for (int q = 0; q <= nd; ++q) own.bound[q] = bound[q];
+    for (int d = 0; d < nd; ++d) {
+        GraphScope sc(gs[d]);
+        auto& w = *gs[d]->sssp;
+        w.mpeers.ensure(nd);
+        GDX_CUDA(cudaMemcpy(w.mpeers.get(), syncs.data(), nd * sizeof(void*), cudaMemcpyHostToDevice));
+        parts[d].peers = reinterpret_cast<MultiSync* const*>(w.mpeers.get());
+    }
+    auto width = [&](auto tag) {
+        using D = decltype(tag);
+        for (int d = 0; d < nd; ++d) multi_prepare<D>(parts[d], own, nd, d);
+        for (int d = 0; d < nd; ++d)
+            multi_enqueue<D>(parts[d], own, nd, src, false,
+                             reinterpret_cast<int64_t*>(gs[d]->sssp->queue[1].get()));
+        MultiResult r;
+        for (int d = 0; d < nd; ++d) multi_collect(parts[d], r);
+        if (!r.overflow) multi_stats(r, nd, stats);
+        return r.overflow;
+    };
+    if (width((unsigned int)0) && width((unsigned long long)0))
+        fail(GDX_ERR_RUNTIME, "RuntimeError: distances overflow 64 bits");
     for (int d = 0; d < nd; ++d) {
         gdx_graph* g = gs[d];
         GraphScope sc(g);
@@ -1287,55 +1414,120 @@ static bool sssp_multi_width(const std::vector<gdx_graph*>& gs, const std::vecto
                  size_t(bound[d + 1] - bound[d]) * sizeof(int64_t));
         GDX_CUDA(cudaStreamSynchronize(g->stream));
     }
-    if (stats) {
-        stats->rounds = int32_t(rounds);
-        stats->launches = int32_t(nd * (4 + 6 * (rounds + 1)));
-        stats->vertices_visited = int64_t(vvis);
-        stats->edges_visited = int64_t(evis);
-        stats->updates = int64_t(upd);
-        stats->algorithmic_bytes = 16.0 * vvis + 12.0 * evis + 8.0 * upd;
-    }
-    return false;
-}
-
-void sssp_multi(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& bound, int32_t src,
-                int64_t* dist_out, gdx_stats* stats) {
-    const int nd = int(gs.size());
-    if (nd < 1 || nd > kMaxMultiDev) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: device count");
-    for (int d = 0; d < nd; ++d) {  // workspaces first: every device's replica address is needed
-        gdx_graph* g = gs[d];
-        GraphScope sc(g);
-        if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
-        auto& w = *g->sssp;
-        const int32_t v0 = bound[d], v1 = bound[d + 1];
-        w.dist.ensure(size_t(g->n));
-        w.prev.ensure(size_t(g->n));
-        w.queue[1].ensure(size_t(std::max(v1 - v0, 1)));
-        std::vector<int32_t> off(2);
-        if (v1 > v0) {
-            GDX_CUDA(cudaMemcpy(&off[0], g->offsets.get() + v0, 4, cudaMemcpyDeviceToHost));
-            GDX_CUDA(cudaMemcpy(&off[1], g->offsets.get() + v1, 4, cudaMemcpyDeviceToHost));
-        }
-        w.shard_queue.ensure(size_t(v1 - v0) + size_t(int64_t(off[1]) - off[0]) / kShardChunk + 1);
-        w.shard_ctr.ensure(kUpdSlot + 1);
-        w.upd_slots.ensure(kUpdSlots);
-        w.graph_acc.ensure(4);
-        if (!w.msync.get()) {
-            w.msync.alloc(sizeof(MultiSync) / 8);
-            GDX_CUDA(cudaMemset(w.msync.get(), 0, sizeof(MultiSync)));
-        }
-    }
-    std::vector<MultiSync*> peers(nd);
-    for (int d = 0; d < nd; ++d) peers[d] = reinterpret_cast<MultiSync*>(gs[d]->sssp->msync.get());
-    for (int d = 0; d < nd; ++d) {
-        gdx_graph* g = gs[d];
-        GraphScope sc(g);
-        auto& w = *g->sssp;
-        w.mpeers.ensure(nd);
-        GDX_CUDA(cudaMemcpy(w.mpeers.get(), peers.data(), nd * sizeof(void*), cudaMemcpyHostToDevice));
-    }
-    if (sssp_multi_width<unsigned int>(gs, bound, src, dist_out, stats))
-        sssp_multi_width<unsigned long long>(gs, bound, src, dist_out, stats);
 }
 
 }  // namespace gdx
+
+// ---------------------------------------------------------------------------
+// The same partitioned SSSP with one process per GPU (the
+// exchange fused into the relaxation over NVLink peer memory, no NCCL per
+// round): every rank exports {replica | barrier state} through CUDA IPC,
+// opens every other rank's, and runs its partition of each call with the
+// device-side barriers of sssp_multi; the result is gathered from the owners'
+// replicas by peer loads.
+// ---------------------------------------------------------------------------
+using namespace gdx;
+
+static_assert(sizeof(MultiSync) == 64, "barrier state block");
+
+extern "C" int gdx_sssp_p2p_setup(gdx_graph* g, int32_t world, int32_t rank,
+                                  const int32_t* bounds, void* handle_out) {
+    return guard_impl([&] {
+        if (!g || !bounds || !handle_out || world < 1 || world > kMaxMultiDev || rank < 0 ||
+            rank >= world)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: bad sssp p2p setup");
+        for (int q = 0; q < world; ++q)
+            if (bounds[q] > bounds[q + 1] || bounds[0] != 0 || bounds[world] != g->n)
+                fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: vertex ranges must partition [0, n)");
+        if (!g->dests.get() && g->m > 0)
+            fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
+        GraphScope sc(g);
+        multi_workspace(g, bounds[rank], bounds[rank + 1]);
+        auto X = std::make_unique<SsspP2P>();
+        X->world = world;
+        X->rank = rank;
+        X->n = g->n;
+        X->bounds.assign(bounds, bounds + world + 1);
+        GDX_CUDA(cudaMalloc(&X->block, X->bytes()));
+        GDX_CUDA(cudaMemset(X->block, 0, X->bytes()));
+        cudaIpcMemHandle_t h;
+        GDX_CUDA(cudaIpcGetMemHandle(&h, X->block));
+        std::memcpy(handle_out, &h, sizeof(h));
+        g->sssp_p2p = std::move(X);
+    });
+}
+
+extern "C" int gdx_sssp_p2p_open(gdx_graph* g, const void* handles) {
+    return guard_impl([&] {
+        if (!g || !g->sssp_p2p || !handles)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no sssp p2p setup");
+        GraphScope sc(g);
+        auto& X = *g->sssp_p2p;
+        X.bases.assign(X.world, nullptr);
+        std::vector<void*> syncs(X.world);
+        for (int q = 0; q < X.world; ++q) {
+            if (q == X.rank) {
+                X.bases[q] = X.block;
+            } else {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, static_cast<const char*>(handles) + 64 * q, sizeof(h));
+                void* p = nullptr;
+                GDX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+                X.bases[q] = static_cast<char*>(p);
+            }
+            syncs[q] = X.bases[q] + size_t(X.n) * 8;
+        }
+        X.peer_sync.alloc(X.world);
+        GDX_CUDA(cudaMemcpy(X.peer_sync.get(), syncs.data(), X.world * sizeof(void*),
+                            cudaMemcpyHostToDevice));
+    });
+}
+
+extern "C" int gdx_sssp_p2p_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    return guard_impl([&] {
+        if (!g || !g->sssp_p2p || g->sssp_p2p->bases.empty() || !dist_out)
+            fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: no sssp p2p plan");
+        if (src < 0 || src >= g->n)
+            fail(GDX_ERR_OUT_OF_RANGE, "RuntimeError: node id " + std::to_string(src) +
+                                           " out of range [0, " + std::to_string(g->n) + ")");
+        GraphScope sc(g);
+        auto& X = *g->sssp_p2p;
+        const int nd = X.world;
+        MultiPart part{g, X.bounds[X.rank], X.bounds[X.rank + 1], X.block,
+                       reinterpret_cast<MultiSync*>(X.block + size_t(X.n) * 8),
+                       reinterpret_cast<MultiSync* const*>(X.peer_sync.get())};
+        SsspOwners own{};
+        own.nd = nd;
+        for (int q = 0; q < nd; ++q) own.dist[q] = X.bases[q];
+        for (int q = 0; q <= nd; ++q) own.bound[q] = X.bounds[q];
+        cudaPointerAttributes pa;
+        const bool dev_out = cudaPointerGetAttributes(&pa, dist_out) == cudaSuccess &&
+                             pa.type == cudaMemoryTypeDevice;
+        cudaGetLastError();
+        auto& w = *g->sssp;
+        if (!dev_out) w.queue[1].ensure(size_t(std::max(g->n, 1)));
+        int64_t* target = dev_out ? dist_out : reinterpret_cast<int64_t*>(w.queue[1].get());
+        auto width = [&](auto tag) {
+            using D = decltype(tag);
+            multi_prepare<D>(part, own, nd, X.rank);
+            multi_enqueue<D>(part, own, nd, src, true, target);
+            MultiResult r;
+            multi_collect(part, r);
+            if (!r.overflow) multi_stats(r, 1, stats);
+            return r.overflow;
+        };
+        if (width((unsigned int)0) && width((unsigned long long)0))
+            fail(GDX_ERR_RUNTIME, "RuntimeError: distances overflow 64 bits");
+        if (!dev_out) copy_out(g, dist_out, target, size_t(g->n) * sizeof(int64_t));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+    });
+}
+
+extern "C" int gdx_sssp_p2p_close(gdx_graph* g) {
+    return guard_impl([&] {
+        if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
+        GraphScope sc(g);
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        g->sssp_p2p.reset();
+    });
+}

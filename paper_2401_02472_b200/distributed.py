@@ -464,6 +464,36 @@ def sharded_sssp(ex: Executor, src: int, group=None, to_host: bool = True, stats
     return d.cpu().numpy() if to_host else d
 
 
+def sharded_sssp_p2p(ex: "DeviceExecutor", src: int, group=None, to_host: bool = True,
+                     stats=None):
+    """ComputeSSSP across ranks with the exchange fused into the relaxation
+    over peer memory (gdx_sssp_p2p_*): vertex ranges balanced by out-edges,
+    improving candidates sent to the owners' replicas by peer atomicMin, the
+    round loop and its barriers on the devices -- no collective and no host
+    round trip per round.  torch.distributed carries only the one-time IPC
+    handle exchange.  Every rank returns the whole int64 vector (read from the
+    owners' replicas); bit-exact."""
+    import torch
+    from ._lib import GraphdslError
+    dist = _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = ex.num_nodes()
+    if not 0 <= src < n:
+        raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
+    ranges = _cached_ranges(ex, "sssp", world, lambda: _partition(ex, "sssp", world))
+    g = ex.g
+    if getattr(ex, "_sssp_p2p", None) != (world, rank, tuple(ranges)):
+        bounds = [r[0] for r in ranges] + [ranges[-1][1]]
+        mine = g.sssp_p2p_setup(world, rank, bounds)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        g.sssp_p2p_open(b"".join(allh))
+        ex._sssp_p2p = (world, rank, tuple(ranges))
+    out = torch.empty(n, dtype=torch.int64, device=f"cuda:{g.device}")
+    g.sssp_p2p_run(src, out=out, stats=stats)
+    return out.cpu().numpy() if to_host else out
+
+
 def _sssp_rounds(ex, src, n, dev, dtype, group, stats, delta):
     """fixedPoint rounds of sharded_sssp over `dtype` replicas; None when an
     int32 relaxation overflowed on any rank."""

@@ -339,6 +339,27 @@ class DeviceGraph:
     def pr_p2p_close(self) -> None:
         check(_lib.load().gdx_pr_p2p_close(self.handle))
 
+    def sssp_p2p_setup(self, world: int, rank: int, bounds: Sequence[int]) -> bytes:
+        b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int32))
+        h = C.create_string_buffer(64)
+        check(_lib.load().gdx_sssp_p2p_setup(self.handle, int(world), int(rank), _ptr(b), h))
+        return h.raw
+
+    def sssp_p2p_open(self, handles: bytes) -> None:
+        buf = C.create_string_buffer(bytes(handles), len(handles))
+        check(_lib.load().gdx_sssp_p2p_open(self.handle, buf))
+
+    def sssp_p2p_run(self, src: int, out=None, stats: Optional[dict] = None):
+        res = out if out is not None else np.empty(self.n, np.int64)
+        st = GdxStats()
+        check(_lib.load().gdx_sssp_p2p_run(self.handle, int(src), _ptr(res), C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
+        return res
+
+    def sssp_p2p_close(self) -> None:
+        check(_lib.load().gdx_sssp_p2p_close(self.handle))
+
     def sssp_shard_setup(self, v_begin: int, v_end: int) -> None:
         check(_lib.load().gdx_sssp_shard_setup(self.handle, int(v_begin), int(v_end)))
 

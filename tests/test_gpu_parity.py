@@ -401,7 +401,13 @@ def _gpu_shard_worker(rank, world, port, q):
     dd = D.sharded_sssp(exu, 7, exchange="dense")
     # weights near 2^30: the int32 rounds overflow and the call reruns over int64
     gb = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1 << 29, 1 << 30, 4)
-    db = D.sharded_sssp(D.DeviceExecutor(G.DeviceGraph.from_csr(gb)), 0, stats=stb)
+    exb = D.DeviceExecutor(G.DeviceGraph.from_csr(gb))
+    db = D.sharded_sssp(exb, 0, stats=stb)
+    # the exchange fused into the relaxation over peer memory (gdx_sssp_p2p_*):
+    # twice (the barrier state carries over), then the overflow rerun
+    dp = D.sharded_sssp_p2p(exu, 7)
+    dp2 = D.sharded_sssp_p2p(exu, 7)
+    dbp = D.sharded_sssp_p2p(exb, 0)
     srcs = [0, 5, 5, 99, 4000, 17, 2048]
     bc = D.sharded_bc(exu, srcs)
     tc = D.sharded_tc(exu)
@@ -410,7 +416,7 @@ def _gpu_shard_worker(rank, world, port, q):
         q.put((r, rounds, er, erounds, d, p.sssp(gu, 7), r2, rounds2, r3, rounds3,
                bc, p.bc(gu, srcs), tc, p.tc(gu),
                (d64, st32["width"], st64["width"], db, p.sssp(gb, 0), stb["width"], dd,
-                st32["exchange"])))
+                st32["exchange"]), (dp, dp2, dbp)))
     tdist.destroy_process_group()
 
 
@@ -428,7 +434,7 @@ def test_sharded_pr_sssp_device(gdx, world):
     procs = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3, bc, ebc, tc, etc_, wide = \
+    r, rounds, er, erounds, d, ed, r2, rounds2, r3, rounds3, bc, ebc, tc, etc_, wide, p2p = \
         q.get(timeout=500)
     for pr in procs:
         pr.join(timeout=60)
@@ -442,6 +448,8 @@ def test_sharded_pr_sssp_device(gdx, world):
     assert world == 1 or exch["sparse_rounds"] > 0  # delta exchange (lists < replica)
     assert np.array_equal(db, edb) and wb == 64 and edb[edb < (2**63 - 1) // 2].max() >= 2**31 - 1
     assert rel_err(bc, ebc) < 1e-9 and tc == etc_
+    dp, dp2, dbp = p2p
+    assert np.array_equal(dp, ed) and np.array_equal(dp2, ed) and np.array_equal(dbp, edb)
 
 
 def test_tc_hub_degree_binning(gdx, port):
