@@ -381,15 +381,19 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
 #endif
 constexpr int kBcCta = GDX_BC_CTA;
 
-// Per-(slot, vertex) state of the CTA kernel, packed so one 16 B load returns
-// a neighbour's level and sigma together and one 32 B load adds its delta:
-// {level, sigma exponent, sigma mantissa, delta}.
-struct __align__(32) BcRec {
-    int32_t level;  // -1 = undiscovered (restored after each source)
+// Per-(slot, vertex) state of the CTA kernel: one 16 B record {level tag,
+// exponent, mantissa} holding sigma(v) after the forward pass and, once the
+// backward pass has visited v, q(v) = (1 + delta(v)) / sigma(v) -- the only
+// value v's parents need: delta(p) = sigma(p) * sum over children w of q(w).
+// Level tags: a slot's successive sources use disjoint, increasing tag ranges
+// (source k's level L is tag base_k + L, base_{k+1} = base_k + levels_k + 1),
+// so a record whose tag is below the current base is undiscovered -- no
+// per-source restore pass; the slot's base persists on the handle and the
+// records are cleared only when the tags would pass INT32_MAX.
+struct __align__(16) BcRec {
+    int32_t level;  // tag (< base: undiscovered in the current source)
     int32_t sexp;
     double smant;
-    double delta;
-    double pad;
 };
 
 struct BcCtaArgs {
@@ -402,6 +406,7 @@ struct BcCtaArgs {
     const int32_t* __restrict__ in_srcs;
     const int32_t* __restrict__ sources;
     BcRec* rec;        // [grid][n]
+    int32_t* base;     // [grid] level tag base of the slot's next source
     bool any_heavy;    // some vertex has more than kHeavy out- (or in-) edges
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
@@ -463,15 +468,20 @@ __device__ inline void rec_level_sigma(const BcRec* r, int32_t& level, XF& sig) 
     level = q.x;
     sig = XF{__hiloint2double(q.w, q.z), q.y};
 }
-__device__ inline void rec_all(const BcRec* r, int32_t& level, XF& sig, double& delta) {
-    int32_t x[8];
-    asm("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
-          "=r"(x[7])
-        : "l"(r));
-    level = x[0];
-    sig = XF{__hiloint2double(x[3], x[2]), x[1]};
-    delta = __hiloint2double(x[5], x[4]);
+// delta(v) = sigma(v) * S (S = sum of the children's q) and the record's new
+// value q(v) = (1 + delta(v)) / sigma(v)
+__device__ inline double xf_mul_double(XF a, XF b) {
+    if (a.m == 0.0 || b.m == 0.0) return 0.0;
+    const int e = a.e + b.e;  // the product of the mantissas is in [1, 4)
+    if (e > -1020 && e < 1020)  // 2^e is a normal double: one exact multiply
+        return a.m * b.m * __longlong_as_double((long long)(e + 1023) << 52);
+    return ldexp(a.m * b.m, e);
+}
+__device__ inline XF xf_q(double delta, XF sig) {
+    const double q = (1.0 + delta) / sig.m;  // finite, normal, in (0.5, n + 1]
+    const long long bits = __double_as_longlong(q);
+    const int k = int((bits >> 52) & 0x7ff) - 1023;
+    return XF{__longlong_as_double((bits & 0x800fffffffffffffll) | (1023ll << 52)), k - sig.e};
 }
 __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
     *reinterpret_cast<int4*>(r) =
@@ -486,7 +496,7 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
 __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* rec, int4* log,
                                                   const int* s_h, int hn, int L, int end,
                                                   int* s_next, int* const* s_copy, int ncopy,
-                                                  unsigned& fscan,
+                                                  int32_t base, unsigned& fscan,
                                                   unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
@@ -499,13 +509,13 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
             int32_t lw;
             XF sg;
             rec_level_sigma(rec + w, lw, sg);
-            if (a.undirected && L > 0 && lw == L - 1) {
+            if (a.undirected && L > 0 && lw == base + L - 1) {
                 acc = xf_add(acc, sg);
                 ++dag;
             }
-            if (lw == -1) {
+            if (lw < base) {
                 const int32_t w0 = a.offsets[w], w1 = a.offsets[w + 1];
-                if (atomicCAS(&rec[w].level, -1, L + 1) == -1) {
+                if (atomicCAS(&rec[w].level, lw, base + L + 1) == lw) {
                     log[end + atomicAdd(&s_next[L % 3], 1)] = make_int4(w, w0, w1, 0);
                     for (int q = 0; q < ncopy; ++q) atomicAdd(&s_copy[q][L % 3], 1);
                 }
@@ -518,20 +528,20 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
                 int32_t lp;
                 XF sg;
                 rec_level_sigma(rec + a.in_srcs[e], lp, sg);
-                if (lp == L - 1) {
+                if (lp == base + L - 1) {
                     acc = xf_add(acc, sg);
                     ++dag;
                 }
             }
         }
         acc = xf_warp_sum(acc);
-        if (lane == 0) rec_store_sigma(rec + v, L, acc);
+        if (lane == 0) rec_store_sigma(rec + v, base + L, acc);
     }
 }
 
 __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec* rec, const int4* log,
                                                    const int* s_h, int hn, int Lb, int32_t src,
-                                                   unsigned& bscan,
+                                                   int32_t base, unsigned& bscan,
                                                    unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
@@ -540,21 +550,21 @@ __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec*
         int32_t lv;
         XF sv;
         rec_level_sigma(rec + v, lv, sv);
-        double d = 0.0;
+        XF sum{0.0, 0};
         if (lane == 0) bscan += oe - ob;
         for (int32_t e = ob + lane; e < oe; e += 32) {
             int32_t lw;
-            XF sw;
-            double dw;
-            rec_all(rec + a.dests[e], lw, sw, dw);
-            if (lw == Lb + 1 && sw.m > 0.0) {
-                d += xf_ratio(sv, sw) * (1.0 + dw);
+            XF qw;
+            rec_level_sigma(rec + a.dests[e], lw, qw);
+            if (lw == base + Lb + 1) {
+                sum = xf_add(sum, qw);
                 ++dag;
             }
         }
-        d = warp_sum(d);
+        sum = xf_warp_sum(sum);
         if (lane == 0) {
-            rec[v].delta = d;
+            const double d = xf_mul_double(sv, sum);
+            rec_store_sigma(rec + v, lv, xf_q(d, sv));
             if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
         }
     }
@@ -590,10 +600,16 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     // to the 64-bit totals after every source
     unsigned fscan = 0, bscan = 0, dag = 0;
     int tk = 0;
+    int32_t base = a.base[slot];  // tag of the next source's level 0
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
+        if (int64_t(base) + a.n + 2 > INT32_MAX) {  // tags exhausted: clear the slot
+            for (int i = tid; i < a.n; i += kStride) rec[i].level = 0;
+            base = 1;
+            cluster.sync();
+        }
         if (tid == 0) {
-            rec[src].level = 0;
+            rec[src].level = base;
             log[0] = make_int4(src, a.offsets[src], a.offsets[src + 1], 0);
             loff[0] = 0;
             s_next[0] = s_next[1] = s_next[2] = 0;
@@ -629,7 +645,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {  // level and sigma in one 16 B load
-                        lw[k] = -2;
+                        lw[k] = -2;  // below every tag, but never a candidate (w < 0)
                         sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
@@ -637,12 +653,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     int32_t w0[kNb], w1[kNb], lnew[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
-                        par[k] = a.undirected && L > 0 && lw[k] == L - 1;
-                        const bool cand = lw[k] == -1;
+                        par[k] = a.undirected && L > 0 && lw[k] == base + L - 1;
+                        const bool cand = w[k] >= 0 && lw[k] < base;
                         w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
                         w1[k] = cand ? a.offsets[w[k] + 1] : 0;
-                        lnew[k] = cand ? atomicCAS(&rec[w[k]].level, -1, L + 1) : lw[k];
-                        got[k] = cand && lnew[k] == -1;
+                        lnew[k] = cand ? atomicCAS(&rec[w[k]].level, lw[k], base + L + 1) : lw[k];
+                        got[k] = cand && lnew[k] == lw[k];
                     }
                     if (!HEAVY && a.kids && oe - ob <= kNb) {
                         // the children of v: neighbours claimed at this level, by v or
@@ -651,7 +667,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         int32_t c[kNb];
 #pragma unroll
                         for (int k = 0; k < kNb; ++k)
-                            c[k] = w[k] >= 0 && (got[k] || lnew[k] == L + 1) ? w[k] : -1;
+                            c[k] = w[k] >= 0 && (got[k] || lnew[k] == base + L + 1) ? w[k] : -1;
                         kids[i] = make_int4(c[0], c[1], c[2], c[3]);
                     }
                     // log positions: one DSMEM atomic per group of converged lanes
@@ -695,7 +711,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         }
 #pragma unroll
                         for (int k = 0; k < kNb; ++k)
-                            if (lp[k] == L - 1) {
+                            if (p[k] >= 0 && lp[k] == base + L - 1) {
                                 acc = xf_add(acc, sg[k]);
                                 ++dag;
                             }
@@ -703,13 +719,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 if (!HEAVY && a.kids && (oe - ob > kNb || oe == ob))  // scan fallback / none
                     kids[i] = oe == ob ? make_int4(-1, -1, -1, -1) : make_int4(-2, -2, -2, -2);
-                rec_store_sigma(rec + v, L, acc);
+                rec_store_sigma(rec + v, base + L, acc);
             }
             // heavy items of this CTA: one warp each, lanes stride over the adjacency
             // (graphs without a vertex above kHeavy skip the extra barrier)
             if (HEAVY && __syncthreads_count(deferred) > 0) {
                 bc_cta_heavy_forward(a, rec, log, s_h, min(s_hn, kBcCta), L, end, s_next, s_copy,
-                                     CS - 1, fscan, dag);
+                                     CS - 1, base, fscan, dag);
                 __syncthreads();
                 if (ltid == 0) s_hn = 0;
             }
@@ -748,57 +764,53 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 int32_t lv;
                 XF sv;
                 rec_level_sigma(rec + v, lv, sv);
-                double d = 0.0;
+                // S = sum of the children's q(w) = (1 + delta(w)) / sigma(w), ascending
+                XF sum{0.0, 0};
                 const int4 kc = !HEAVY && kids ? kids[i] : make_int4(-2, 0, 0, 0);
                 if (!HEAVY && kc.x != -2) {  // the recorded children, ascending
                     bscan += oe - ob;  // the adjacency scan this replaces (stats)
                     const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
                     int32_t lw[kNb];
-                    XF sw[kNb];
-                    double dw[kNb];
+                    XF qw[kNb];
 #pragma unroll
                     for (int k = 0; k < kNb; ++k) {
-                        lw[k] = -2;
-                        sw[k] = XF{1.0, 0};
-                        dw[k] = 0.0;
-                        if (w[k] >= 0) rec_all(rec + w[k], lw[k], sw[k], dw[k]);
+                        qw[k] = XF{0.0, 0};
+                        if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], qw[k]);
                     }
 #pragma unroll
                     for (int k = 0; k < kNb; ++k)
                         if (w[k] >= 0) {
-                            d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
+                            sum = xf_add(sum, qw[k]);
                             ++dag;
                         }
-                    rec[v].delta = d;
-                    if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
-                    continue;
-                }
-                bscan += oe - ob;
-                for (int32_t e = ob; e < oe; e += kNb) {
-                    int32_t w[kNb], lw[kNb];
-                    XF sw[kNb];
-                    double dw[kNb];
+                } else {
+                    bscan += oe - ob;
+                    for (int32_t e = ob; e < oe; e += kNb) {
+                        int32_t w[kNb], lw[kNb];
+                        XF qw[kNb];
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+                        for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) {  // level, sigma and delta in one 32 B load
-                        lw[k] = -2;
-                        sw[k] = XF{1.0, 0};
-                        dw[k] = 0.0;
-                        if (w[k] >= 0) rec_all(rec + w[k], lw[k], sw[k], dw[k]);
+                        for (int k = 0; k < kNb; ++k) {  // level and q in one 16 B load
+                            lw[k] = -2;
+                            qw[k] = XF{0.0, 0};
+                            if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], qw[k]);
+                        }
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            if (w[k] >= 0 && lw[k] == base + Lb + 1) {  // ascending child order
+                                sum = xf_add(sum, qw[k]);
+                                ++dag;
+                            }
                     }
-#pragma unroll
-                    for (int k = 0; k < kNb; ++k)
-                        if (lw[k] == Lb + 1 && sw[k].m > 0.0) {  // ascending child order (oracles.cpp:60-67)
-                            d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
-                            ++dag;
-                        }
                 }
-                rec[v].delta = d;
+                const double d = xf_mul_double(sv, sum);  // delta(v)
+                rec_store_sigma(rec + v, lv, xf_q(d, sv));
                 if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
             }
             if (HEAVY && __syncthreads_count(deferred) > 0) {
-                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, bscan, dag);
+                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bscan,
+                                      dag);
                 __syncthreads();
                 if (ltid == 0) s_hn = 0;
             }
@@ -819,11 +831,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             }
             fscan = bscan = dag = 0;
         }
-        // restore `level` for the slot's next source
-        for (int i = tid; i < end; i += kStride) rec[log[i].x].level = -1;
-        cluster.sync();
-        bc_trace(a, slot, tid, tk, 1 << 30);  // restore step
+        // the next source's tags start above every tag this one wrote
+        base += levels + 1;
     }
+    if (tid == 0) a.base[slot] = base;
 }
 
 static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
@@ -847,14 +858,14 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     const bool any_heavy = graph_max_degree(g) > kHeavy;
     const char* kv = std::getenv("GDX_BC_KIDS");
     const bool a_kids = !any_heavy && !(kv && std::string(kv) == "0");
-    // a slot holds 52 B per vertex (record, log entry, level bound; + 16 B of
+    // a slot holds 36 B per vertex (record, log entry, level bound; + 16 B of
     // children): fewer
     // slots (each then runs several sources) when they would not fit (queried
     // only when the slots have to grow)
     if (W.cta_grid < slots) {
         size_t free_b = 0, tot_b = 0;
         GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
-        const size_t per_slot = size_t(n) * (a_kids ? 68 : 52) + 8;
+        const size_t per_slot = size_t(n) * (a_kids ? 52 : 36) + 8;
         const size_t held = W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() +
                             W.cta_kids.bytes() + pool_cached();
         const int64_t fit = int64_t(double(free_b + held) * 0.85 / double(per_slot));
@@ -873,11 +884,20 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.cta_loff.release();
         W.cta_kids.release();
         W.batch = 0;
-        W.cta_rec.alloc(size_t(slots) * n * 4);  // 32 B BcRec per (slot, vertex)
+        W.cta_rec.alloc(size_t(slots) * n * 2);  // 16 B BcRec per (slot, vertex)
         W.cta_log.alloc(size_t(slots) * n * 4);  // int4 entries
         W.cta_loff.alloc(size_t(slots) * (n + 2));
         W.cta_grid = slots;
-        GDX_CUDA(cudaMemsetAsync(W.cta_rec.get(), 0xff, W.cta_rec.bytes(), s));  // level = -1
+        // every tag 0 lies below the slots' first base (1)
+        GDX_CUDA(cudaMemsetAsync(W.cta_rec.get(), 0, W.cta_rec.bytes(), s));
+        W.cta_base.alloc(size_t(slots));
+        // GDX_BC_TAG_START (tests): first base of new slots, e.g. close to
+        // INT32_MAX to exercise the slot clearing when the tags run out
+        const char* ts = std::getenv("GDX_BC_TAG_START");
+        std::vector<int32_t> ones(size_t(slots), ts ? std::max(1, std::atoi(ts)) : 1);
+        GDX_CUDA(cudaMemcpyAsync(W.cta_base.get(), ones.data(), ones.size() * 4,
+                                 cudaMemcpyHostToDevice, s));
+        GDX_CUDA(cudaStreamSynchronize(s));  // `ones` is pageable and local
     }
     if (a_kids) W.cta_kids.ensure(size_t(W.cta_grid) * n * 4);  // int4 per (slot, vertex)
     W.sources.ensure(size_t(nsrc));
@@ -894,6 +914,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.in_srcs = g->in_srcs();
     a.sources = W.sources.get();
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
+    a.base = W.cta_base.get();
     a.any_heavy = any_heavy;
     a.kids = a_kids ? reinterpret_cast<int4*>(W.cta_kids.get()) : nullptr;
     used_kids = a_kids;
@@ -994,6 +1015,7 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
         } else if (nsrc > 0) {
             if (W.cta_grid > 0) {  // switch back from CTA mode: release its buffers
                 W.cta_rec.release();
+                W.cta_base.release();
                 W.cta_log.release();
                 W.cta_loff.release();
                 W.cta_kids.release();

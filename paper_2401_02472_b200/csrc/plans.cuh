@@ -81,8 +81,9 @@ struct SsspWork {
     int32_t shard_round = 0;
     // device-side round loop (CUDA graph with a conditional WHILE node), per distance width
     static constexpr int kKey = 10;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    void* gkey[2][kKey] = {};
+    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};  // u32, u64, u16 distances
+    void* gkey[3][kKey] = {};
+    bool narrow_overflowed = false;  // a 16-bit attempt on this handle overflowed
     DevBuf<unsigned long long> graph_acc;  // [rounds, vertices, edges, overflow]
     DevBuf<unsigned long long> upd_slots;  // U counter slots (sssp.cu block_count)
     // in-process multi-GPU rounds (gdx_sssp_multi): barrier state and the
@@ -146,7 +147,8 @@ struct BcWork {
     int block = 0;
     // CTA-per-source mode (k_bc_cta): one state slot per CTA
     int32_t cta_grid = 0;
-    DevBuf<double> cta_rec;     // [cta_grid][n] x 32 B (level, sigma exp, mantissa, delta)
+    DevBuf<double> cta_rec;     // [cta_grid][n] x 16 B (level tag, exponent, mantissa)
+    DevBuf<int32_t> cta_base;   // [cta_grid] level tag base of each slot's next source
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
     DevBuf<int32_t> cta_kids;   // [cta_grid][n] int4: children of each log entry (or -2)

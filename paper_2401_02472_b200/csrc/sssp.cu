@@ -388,7 +388,45 @@ constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-co
 #define GDX_SSSP_CHUNK 64
 #endif
 constexpr int kUpdSlot = 6;  // shard_ctr slot counting issued relaxations (U)
-constexpr int kShardChunk = GDX_SSSP_CHUNK;  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
+constexpr int kShardChunk = GDX_SSSP_CHUNK;
+// L2 policy of the streamed arrays (A/B knob): 1 = the relaxation's items,
+// dests and weights are loaded evict-first (ld.global.cs), 2 = also the
+// scan's prev array, so the hot dist lines of the gathers stay in L2
+#ifndef GDX_SSSP_HINT
+#define GDX_SSSP_HINT 0
+#endif
+// atomicMin over any distance width: 16-bit distances (the narrow first
+// attempt of large graphs) take a CAS loop on their aligned 32-bit word.
+__device__ __forceinline__ unsigned short dist_atomic_min(unsigned short* p, unsigned short v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
+    unsigned int old = *w, assumed;
+    do {
+        assumed = old;
+        const unsigned short cur = (unsigned short)(assumed >> sh);
+        if (cur <= v) return cur;
+        old = atomicCAS(w, assumed, (assumed & ~(0xFFFFu << sh)) | (unsigned(v) << sh));
+    } while (old != assumed);
+    return (unsigned short)(assumed >> sh);
+}
+template <class D>
+__device__ __forceinline__ D dist_atomic_min(D* p, D v) { return atomicMin(p, v); }
+
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+    if constexpr (GDX_SSSP_HINT >= 1) return __ldcs(p);
+    else return *p;
+}
+template <class T>
+__device__ __forceinline__ T ld_scan(const T* p) {
+    if constexpr (GDX_SSSP_HINT >= 2) return __ldcs(p);
+    else return *p;
+}
+template <class T>
+__device__ __forceinline__ void st_scan(T* p, T v) {
+    if constexpr (GDX_SSSP_HINT >= 2) __stcs(p, v);
+    else *p = v;
+}  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
 // every relaxation kernel splits an item over LPI in {8, 16, 32} lanes
 static_assert(kShardChunk % 32 == 0 && kShardChunk >= 32, "GDX_SSSP_CHUNK must be a multiple of 32");
 
@@ -420,7 +458,7 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
         for (int k = 0; k < kPer; ++k) {
             const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             dk[k] = v < v1 ? dist[v] : D(0);
-            pk[k] = v < v1 ? prev[v] : D(0);
+            pk[k] = v < v1 ? ld_scan(prev + v) : D(0);
         }
         int items[kPer], first[kPer], last[kPer];
 #pragma unroll
@@ -437,7 +475,7 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
             const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             items[k] = 0;
             if (last[k] >= 0) {
-                prev[v] = dk[k];
+                st_scan(prev + v, dk[k]);
                 const int32_t deg = last[k] - first[k];
                 items[k] = (deg + kShardChunk - 1) / kShardChunk;
                 sinks += deg == 0;
@@ -539,7 +577,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
-        const int2 it = queue[i];
+        const int2 it = ld_stream(queue + i);
         const D dv = dist[it.x];
         // int64: it.y + kShardChunk passes INT32_MAX on the last items of m ~ 2^31 graphs
         const int32_t e1 = int32_t(min(int64_t(it.y) + kShardChunk, int64_t(offsets[it.x + 1])));
@@ -548,10 +586,11 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
             const int32_t e = it.y + sub + k * LPI;
-            u[k] = e < e1 ? dests[e] : -1;
-            const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
+            u[k] = e < e1 ? ld_stream(dests + e) : -1;
+            const D w = e < e1 ? (weights ? D(ld_stream(weights + e)) : D(1)) : D(0);
             c[k] = dv + w;
-            if (sizeof(D) == 4 && u[k] >= 0 && dv > std::numeric_limits<D>::max() - D(1) - w) {
+            if (sizeof(D) < 8 && u[k] >= 0 &&
+                uint64_t(dv) + uint64_t(w) >= uint64_t(std::numeric_limits<D>::max())) {
                 *ovf = 1;
                 u[k] = -1;
             }
@@ -563,11 +602,11 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
             if (u[k] >= 0 && c[k] < du[k]) {
                 ++issued;
                 if (DELTA) {
-                    if (c[k] < atomicMin(&dist[u[k]], c[k]) &&
+                    if (c[k] < dist_atomic_min(&dist[u[k]], c[k]) &&
                         atomicMax(&dl.mark[u[k]], dl.round) < dl.round)
                         dl.changed[atomicAdd(dl.count, 1ull)] = u[k];
                 } else {
-                    atomicMin(&dist[u[k]], c[k]);
+                    dist_atomic_min(&dist[u[k]], c[k]);
                 }
             }
     }
@@ -623,7 +662,8 @@ __global__ void k_sssp_graph_finish(unsigned long long* ctr, unsigned long long*
     acc[1] += ctr[3];
     acc[2] += ctr[4];
     for (int i = 0; i < 5; ++i) ctr[i] = 0;
-    cudaGraphSetConditional(h, items ? 1u : 0u);
+    // a narrow-width overflow ends the loop at once (the call reruns wider)
+    cudaGraphSetConditional(h, items && !acc[3] ? 1u : 0u);
 }
 
 template <class D>
@@ -678,7 +718,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const int32_t n = g->n;
     D* dist = reinterpret_cast<D*>(w.dist.get());
     D* prev = reinterpret_cast<D*>(w.prev.get());
-    const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
+    const D inf = sizeof(D) < 8 ? std::numeric_limits<D>::max() : D(INT64_MAX / 2);
     const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
     w.shard_queue.ensure(items_cap);
     w.shard_ctr.ensure(kUpdSlot + 1);
@@ -706,7 +746,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const int relax_grid =
         (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 128)) * g->num_sms;
     if (use_graph) {
-        const int di = sizeof(D) == 4 ? 0 : 1;
+        const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
         // the instantiated graph bakes in these buffers and the CSR arrays
         // (gdx_graph_set_hash_weights reallocates / enables the weights)
         void* key[SsspWork::kKey] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get(),
@@ -973,7 +1013,20 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         const bool scan = md == "scan" || graph;
         if (scan) {
             w.prev.ensure(size_t(g->n));
-            if (run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
+            // widths: 16-bit first on large graphs (half the footprint of the
+            // gathered distance array in L2; GDX_SSSP_NARROW=0/1 overrides),
+            // unless a 16-bit attempt on this handle already overflowed; then
+            // 32-bit, then 64-bit -- each rerun exact
+            const char* ne = std::getenv("GDX_SSSP_NARROW");
+            const int narrow_env = ne ? std::atoi(ne) : -1;
+            const bool narrow = narrow_env >= 0 ? narrow_env > 0
+                                                : (g->n >= (1 << 22) && !w.narrow_overflowed);
+            bool ovf = true;
+            if (narrow) {
+                ovf = run_sssp_scan<unsigned short>(g, src, dist_out, stats, graph);
+                if (ovf) w.narrow_overflowed = true;
+            }
+            if (ovf && run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
                 run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph);
         } else {
             // the persistent kernel's queues exist only in this mode (C5 in the

@@ -195,6 +195,25 @@ def test_sssp_64bit_distances(gdx, port, mode, monkeypatch):
         assert np.array_equal(dg.sssp(src), port.sssp(g, src))
 
 
+@pytest.mark.parametrize("weights", [(1, 100), (300, 600)])
+def test_sssp_16bit_first_attempt(gdx, port, weights, monkeypatch):
+    """Large graphs try 16-bit distances first (GDX_SSSP_NARROW=1 forces it
+    here): exact when they fit (C1's weights, max distance 209), and an
+    overflow (a 100x100 grid with weights 300..600 reaches ~10^5) reruns the
+    call at 32 bits -- on this handle and on the next call too."""
+    monkeypatch.setenv("GDX_SSSP_NARROW", "1")
+    gu, gv = port.gen_grid_ctr(100, 2.0, 1)
+    g = port.build_from_edges(100 * 100, gu, gv, None, False)
+    g.weights = np.random.default_rng(3).integers(*weights, size=g.m).astype(np.int32)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for mode in ("graph", "scan"):
+        monkeypatch.setenv("GDX_SSSP_MODE", mode)
+        for src in (0, 5050, 0):
+            exp = port.sssp(g, src)
+            assert np.array_equal(dg.sssp(src), exp), (mode, src)
+    assert (exp[exp < INF].max() > 65535) == (weights[0] == 300)
+
+
 def test_sssp_zero_weights_and_unreachable(gdx, port):
     u, v = port.gen_uniform_edges(3000, 9000, 4)
     g = port.build_from_edges(3000, u, v, None, True)
@@ -311,7 +330,7 @@ def test_bc_grid_and_overflow(gdx, port, bc_mode):
 
 def test_bc_many_sources_slot_reuse(gdx, port):
     """More sources than CTAs: the default picks CTA mode and every CTA slot is
-    reused for several sources (its level array restored in between)."""
+    reused for several sources (its level tags advance in between)."""
     gu, gv = port.gen_grid_ctr(60, 0.6, 5)
     g = port.build_from_edges(3600, gu, gv, None, False)
     srcs = list(range(0, 3600, 11))  # 328 sources > #SM
@@ -320,6 +339,22 @@ def test_bc_many_sources_slot_reuse(gdx, port):
     got = dg.bc(srcs, stats=st)
     assert st["launches"] == 1  # one k_bc_cta launch
     assert rel_err(got, port.bc(g, srcs)) < 1e-9
+
+
+def test_bc_level_tags_run_out(gdx, port, monkeypatch):
+    """Level tags: a slot's sources use increasing tag ranges (no per-source
+    restore); when the tags would pass INT32_MAX the slot is cleared.  Start the
+    tags just below that limit so the clearing runs inside a call and between
+    calls on the same handle."""
+    gu, gv = port.gen_grid_ctr(60, 0.6, 5)
+    g = port.build_from_edges(3600, gu, gv, None, False)
+    monkeypatch.setenv("GDX_BC_MODE", "cta")
+    monkeypatch.setenv("GDX_BC_TAG_START", str(2**31 - 1 - 3602 - 300))
+    srcs = list(range(0, 3600, 11))  # several sources per slot
+    dg = gdx.DeviceGraph.from_csr(g)
+    exp = port.bc(g, srcs)
+    for _ in range(3):
+        assert rel_err(dg.bc(srcs), exp) < 1e-9
 
 
 # ---- GPU generators == their CPU twin ---------------------------------------------------
