@@ -319,10 +319,7 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
                         ++dag;
                     }
             }
-            if (!heavy) {
-                a.delta[sb + v] = d;
-                if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
-            }
+            if (!heavy) a.delta[sb + v] = d;
           }
           __syncthreads();
           for (int h = tid >> 5; h < s_hn; h += kBcBlock / 32) {
@@ -345,10 +342,7 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
                 }
             }
             d = warp_sum(d);
-            if (lane == 0) {
-                a.delta[sb + v] = d;
-                if (v != a.sources[s]) atomicAdd(&a.bc[v], d);
-            }
+            if (lane == 0) a.delta[sb + v] = d;
           }
           __syncthreads();
         }
@@ -365,6 +359,19 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
     }
 }
 
+
+// bc[v] += delta_s(v) over the batch's sources in source order (v reached by
+// s, v != s): a fixed summation order, so results are reproducible run to run.
+__global__ void k_bc_batch_sum(BcArgs a) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        double acc = a.bc[v];
+        for (int s = 0; s < a.S; ++s)
+            if (a.level[int64_t(s) * a.n + v] >= 0 && a.sources[s] != v)
+                acc += a.delta[int64_t(s) * a.n + v];
+        a.bc[v] = acc;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // CTA-per-source mode (high-diameter graphs, many sources).  A road-like grid
@@ -396,6 +403,9 @@ struct __align__(16) BcRec {
     double smant;
 };
 
+// slot stride of the partial scores: 64 B-aligned slots (16 B vector sums)
+__host__ __device__ inline int64_t bcs_stride(int64_t n) { return (n + 7) & ~int64_t(7); }
+
 struct BcCtaArgs {
     int32_t n;
     int32_t nsrc;
@@ -411,6 +421,7 @@ struct BcCtaArgs {
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
     int4* kids;        // [grid][n] children of each log entry (low-degree graphs) or nullptr
+    double* bcs;       // [grid][n] the slot's partial scores (its sources in order), 0 between calls
     double* bc;
     unsigned long long* ctr;
     unsigned long long* trace;  // optional: slot 0's (globaltimer ns, items) per level step
@@ -441,10 +452,13 @@ __device__ inline XF xf_add(XF a, XF b) {
         const double s = a.m + b.m;
         return s < 2.0 ? XF{s, a.e} : XF{s * 0.5, a.e + 1};
     }
-    const int e = max(a.e, b.e);
-    const double s = ldexp(a.m, a.e - e) + ldexp(b.m, b.e - e);
-    const int k = ilogb(s);
-    return XF{ldexp(s, -k), e + k};
+    // big + small * 2^d (d < 0): the sum is in [1, 3), so at most one halving;
+    // 2^d is built from its bits (the same values as ldexp / ilogb)
+    const XF big = a.e > b.e ? a : b, small = a.e > b.e ? b : a;
+    const int d = small.e - big.e;
+    if (d < -60) return big;  // below half an ulp of big: the sum rounds to big
+    const double s = big.m + small.m * __longlong_as_double((long long)(d + 1023) << 52);
+    return s < 2.0 ? XF{s, big.e} : XF{s * 0.5, big.e + 1};
 }
 
 __device__ inline double xf_ratio(XF a, XF b) {
@@ -541,7 +555,7 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
 
 __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec* rec, const int4* log,
                                                    const int* s_h, int hn, int Lb, int32_t src,
-                                                   int32_t base, unsigned& bscan,
+                                                   int32_t base, double* bcs, unsigned& bscan,
                                                    unsigned& dag) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
@@ -565,7 +579,7 @@ __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec*
         if (lane == 0) {
             const double d = xf_mul_double(sv, sum);
             rec_store_sigma(rec + v, lv, xf_q(d, sv));
-            if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
+            if (v != src && d != 0.0) bcs[v] += d;  // leaves add nothing
         }
     }
 }
@@ -596,6 +610,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
     int4* kids = a.kids ? a.kids + slot * a.n : nullptr;
+    double* bcs = a.bcs + slot * bcs_stride(a.n);
     // per-source 32-bit counters (registers are the kernel's limit), flushed
     // to the 64-bit totals after every source
     unsigned fscan = 0, bscan = 0, dag = 0;
@@ -806,11 +821,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 const double d = xf_mul_double(sv, sum);  // delta(v)
                 rec_store_sigma(rec + v, lv, xf_q(d, sv));
-                if (v != src && d != 0.0) atomicAdd(&a.bc[v], d);  // leaves add nothing
+                if (v != src && d != 0.0) bcs[v] += d;  // leaves add nothing (one thread per v)
             }
             if (HEAVY && __syncthreads_count(deferred) > 0) {
-                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bscan,
-                                      dag);
+                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bcs,
+                                      bscan, dag);
                 __syncthreads();
                 if (ltid == 0) s_hn = 0;
             }
@@ -837,6 +852,28 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     if (tid == 0) a.base[slot] = base;
 }
 
+// bc[v] = sum of the slots' partials in slot order (each slot's own sources
+// in order): reproducible; the partials are cleared for the next call.
+// Two vertices per thread (16 B loads / stores; slot stride a multiple of 8).
+__global__ void k_bc_slot_sum(int32_t n, int64_t stride, int32_t slots, double* __restrict__ bcs,
+                              double* __restrict__ bc) {
+    for (int64_t v = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); v < n;
+         v += 2 * (int64_t)gridDim.x * blockDim.x) {
+        double2 acc = make_double2(bc[v], v + 1 < n ? bc[v + 1] : 0.0);
+        for (int q = 0; q < slots; ++q) {
+            double2* p = reinterpret_cast<double2*>(bcs + q * stride + v);
+            const double2 x = *p;
+            if (x.x != 0.0 || x.y != 0.0) {
+                acc.x += x.x;
+                acc.y += x.y;
+                *p = make_double2(0.0, 0.0);
+            }
+        }
+        bc[v] = acc.x;
+        if (v + 1 < n) bc[v + 1] = acc.y;
+    }
+}
+
 static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
                        unsigned long long* totals, int& launches, int& max_levels,
                        bool& used_kids) {
@@ -858,15 +895,16 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     const bool any_heavy = graph_max_degree(g) > kHeavy;
     const char* kv = std::getenv("GDX_BC_KIDS");
     const bool a_kids = !any_heavy && !(kv && std::string(kv) == "0");
-    // a slot holds 36 B per vertex (record, log entry, level bound; + 16 B of
+    // a slot holds 44 B per vertex (record, log entry, level bound, partial score; + 16 B of
     // children): fewer
     // slots (each then runs several sources) when they would not fit (queried
     // only when the slots have to grow)
     if (W.cta_grid < slots) {
         size_t free_b = 0, tot_b = 0;
         GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
-        const size_t per_slot = size_t(n) * (a_kids ? 52 : 36) + 8;
+        const size_t per_slot = size_t(n) * (a_kids ? 60 : 44) + 8;
         const size_t held = W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() +
+                            W.cta_bcs.bytes() +
                             W.cta_kids.bytes() + pool_cached();
         const int64_t fit = int64_t(double(free_b + held) * 0.85 / double(per_slot));
         if (fit < 1)
@@ -891,6 +929,8 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         // every tag 0 lies below the slots' first base (1)
         GDX_CUDA(cudaMemsetAsync(W.cta_rec.get(), 0, W.cta_rec.bytes(), s));
         W.cta_base.alloc(size_t(slots));
+        W.cta_bcs.alloc(size_t(slots) * bcs_stride(n));
+        GDX_CUDA(cudaMemsetAsync(W.cta_bcs.get(), 0, W.cta_bcs.bytes(), s));
         // GDX_BC_TAG_START (tests): first base of new slots, e.g. close to
         // INT32_MAX to exercise the slot clearing when the tags run out
         const char* ts = std::getenv("GDX_BC_TAG_START");
@@ -921,6 +961,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
     a.bc = W.bc.get();
+    a.bcs = W.cta_bcs.get();
     a.ctr = W.ctrs.get();
     // GDX_BC_TRACE=<file>: slot 0's per-level-step (ns since the previous step, items)
     const char* trace = std::getenv("GDX_BC_TRACE");
@@ -951,7 +992,11 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
                 k_bc_cta<1, false><<<grid, kBcCta, 0, s>>>(a);
         }
     });
-    ++launches;
+    timed_launch(g, "bc_sum", [&] {
+        k_bc_slot_sum<<<blocks_for((n + 1) / 2, 256, g->num_sms * 8), 256, 0, s>>>(
+            int32_t(n), bcs_stride(n), slots, a.bcs, a.bc);
+    });
+    launches += 2;
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
@@ -1016,6 +1061,7 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             if (W.cta_grid > 0) {  // switch back from CTA mode: release its buffers
                 W.cta_rec.release();
                 W.cta_base.release();
+                W.cta_bcs.release();
                 W.cta_log.release();
                 W.cta_loff.release();
                 W.cta_kids.release();
@@ -1100,7 +1146,10 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
                                : W.block == 512 ? (void*)k_bc_backward<512> : (void*)k_bc_backward<1024>;
                     GDX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(W.grid), dim3(W.block), args, 0, s));
                 });
-                launches += 3;
+                timed_launch(g, "bc_sum", [&] {
+                    k_bc_batch_sum<<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(a);
+                });
+                launches += 4;
                 GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));
                 GDX_CUDA(cudaStreamSynchronize(s));
                 totals[kReached] += h[kTail];

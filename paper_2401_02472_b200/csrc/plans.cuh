@@ -149,6 +149,7 @@ struct BcWork {
     int32_t cta_grid = 0;
     DevBuf<double> cta_rec;     // [cta_grid][n] x 16 B (level tag, exponent, mantissa)
     DevBuf<int32_t> cta_base;   // [cta_grid] level tag base of each slot's next source
+    DevBuf<double> cta_bcs;     // [cta_grid][n] per-slot partial scores (summed in slot order)
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
     DevBuf<int32_t> cta_kids;   // [cta_grid][n] int4: children of each log entry (or -2)

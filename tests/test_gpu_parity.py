@@ -337,8 +337,30 @@ def test_bc_many_sources_slot_reuse(gdx, port):
     dg = gdx.DeviceGraph.from_csr(g)
     st = {}
     got = dg.bc(srcs, stats=st)
-    assert st["launches"] == 1  # one k_bc_cta launch
+    assert st["launches"] == 2  # one k_bc_cta launch + the ordered slot sum
     assert rel_err(got, port.bc(g, srcs)) < 1e-9
+
+
+@pytest.mark.parametrize("mode", ["grid", "cta"])
+def test_bc_and_pr_reproducible(gdx, port, mode, monkeypatch):
+    """No floating-point atomics on the score paths: BC sums the per-slot
+    (CTA mode) or per-source (grid mode) partials in a fixed order, PageRank
+    sums rows by chunk partials -- repeated calls give bit-identical results."""
+    monkeypatch.setenv("GDX_BC_MODE", mode)
+    n = 1 << 13
+    u, v = port.gen_rmat_edges(n, 16 * n, 4)
+    g = port.build_from_edges(n, u, v, None, False)
+    dg = gdx.DeviceGraph.from_csr(g)
+    srcs = list(range(0, n, 97))
+    first = dg.bc(srcs)
+    for _ in range(3):
+        assert np.array_equal(dg.bc(srcs), first)
+    assert rel_err(first, port.bc(g, srcs)) < 1e-9
+    d = gdx.DeviceGraph.from_csr(port.build_from_edges(n, u, v, None, True))
+    r0, it0 = d.pagerank(0.85, 1e-9, 100)
+    for _ in range(3):
+        r, it = d.pagerank(0.85, 1e-9, 100)
+        assert it == it0 and np.array_equal(r, r0)
 
 
 def test_bc_level_tags_run_out(gdx, port, monkeypatch):
