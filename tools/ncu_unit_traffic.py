@@ -54,9 +54,15 @@ def main():
             units.append(cur)
         if cur is not None:
             cur.append(d)
-    if len(units) >= 2:
-        units = units[:-1] if a.unit == "round" else units  # a PR call's last round may be partial
-    u = units[-1]
+    if a.unit == "round":
+        # PR: rounds enqueued after the vote settled exit at once -- report the
+        # median of the rounds that did work (>= half the longest round)
+        dur = [sum(d.get("gpu__time_duration.sum", 0.0) for d in x) for x in units]
+        work = sorted((x for x, t in zip(units, dur) if t >= 0.5 * max(dur)),
+                      key=lambda x: sum(d.get("dram__bytes_read.sum", 0.0) for d in x))
+        u = work[len(work) // 2]
+    else:
+        u = units[-1]
     rd = sum(d.get("dram__bytes_read.sum", 0.0) for d in u)
     wr = sum(d.get("dram__bytes_write.sum", 0.0) for d in u)
     t = sum(d.get("gpu__time_duration.sum", 0.0) for d in u)
