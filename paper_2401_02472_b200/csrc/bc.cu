@@ -502,6 +502,37 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
         make_int4(level, sig.e, __double2loint(sig.m), __double2hiint(sig.m));
 }
 
+// Backward-pass pipelining (GDX_BC_PIPE, graphs with recorded children): while
+// a thread works on one item of a level, its next item's log entry and
+// children list, then its own and its children's records, are copied into the
+// thread's shared-memory slot with cp.async -- no registers held across the
+// current item, so its next item starts with its data on chip.
+#ifndef GDX_BC_PIPE
+#define GDX_BC_PIPE 1
+#endif
+constexpr bool kBcPipe = GDX_BC_PIPE != 0;
+struct __align__(16) BcPf {
+    int4 log, kids, own, ch[kNb];
+};
+__device__ inline void cp16(void* sdst, const void* gsrc) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ inline void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ inline void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// stage 2: the item's own record and its recorded children's (slot's log/kids ready)
+__device__ inline void bc_pf_records(BcPf* pf, const BcRec* rec) {
+    const int4 it = pf->log, kc = pf->kids;
+    cp16(&pf->own, rec + it.x);
+    if (kc.x != -2) {
+        const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
+#pragma unroll
+        for (int k = 0; k < kNb; ++k)
+            if (w[k] >= 0) cp16(&pf->ch[k], rec + w[k]);
+    }
+    cp_commit();
+}
+
 // CS CTAs (a thread-block cluster) share one source: the level barrier is a
 // cluster barrier and the queue tail lives in CTA 0's shared memory (DSMEM
 // atomics), so a source's levels are spread over CS * 1024 threads.
@@ -592,6 +623,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     __shared__ int s_next_local[3];
     __shared__ int s_hn;
     __shared__ int s_h[kBcCta];  // this CTA's deferred heavy items (log indices) of a level
+    extern __shared__ BcPf s_pf[];  // GDX_BC_PIPE: one slot per thread (dynamic)
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = int(cluster.block_rank());
     int* s_next = cluster.map_shared_rank(s_next_local, 0);
@@ -762,6 +794,81 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             atomicMax(&a.ctr[kLevels], (unsigned long long)levels);
         }
         // ---- backward: iterateInReverse ----
+        if (!HEAVY && kBcPipe && kids) {
+            BcPf* pf = s_pf + ltid;
+            for (int Lb = levels - 1; Lb >= 0; --Lb) {
+                const int b0 = loff[Lb], b1 = loff[Lb + 1];
+                int i = b0 + tid;
+                if (i < b1) {  // the first item: both stages now
+                    cp16(&pf->log, log + i);
+                    cp16(&pf->kids, kids + i);
+                    cp_commit();
+                    cp_wait();
+                    bc_pf_records(pf, rec);
+                }
+                for (; i < b1; i += kStride) {
+                    cp_wait();
+                    const int4 it = pf->log, kc = pf->kids, ow = pf->own;
+                    const int32_t v = it.x, ob = it.y, oe = it.z;
+                    const int32_t lv = ow.x;
+                    const XF sv{__hiloint2double(ow.w, ow.z), ow.y};
+                    XF sum{0.0, 0};
+                    bscan += oe - ob;
+                    if (kc.x != -2) {  // the recorded children, ascending
+                        const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
+                        int4 r[kNb];
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k) r[k] = w[k] >= 0 ? pf->ch[k] : make_int4(0, 0, 0, 0);
+                        const int in = i + kStride;
+                        if (in < b1) {  // stage 1 of the next item
+                            cp16(&pf->log, log + in);
+                            cp16(&pf->kids, kids + in);
+                            cp_commit();
+                        }
+#pragma unroll
+                        for (int k = 0; k < kNb; ++k)
+                            if (w[k] >= 0) {
+                                sum = xf_add(sum, XF{__hiloint2double(r[k].w, r[k].z), r[k].y});
+                                ++dag;
+                            }
+                    } else {
+                        const int in = i + kStride;
+                        if (in < b1) {
+                            cp16(&pf->log, log + in);
+                            cp16(&pf->kids, kids + in);
+                            cp_commit();
+                        }
+                        for (int32_t e = ob; e < oe; e += kNb) {
+                            int32_t w[kNb], lw[kNb];
+                            XF qw[kNb];
+#pragma unroll
+                            for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
+#pragma unroll
+                            for (int k = 0; k < kNb; ++k) {
+                                lw[k] = -2;
+                                qw[k] = XF{0.0, 0};
+                                if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], qw[k]);
+                            }
+#pragma unroll
+                            for (int k = 0; k < kNb; ++k)
+                                if (w[k] >= 0 && lw[k] == base + Lb + 1) {
+                                    sum = xf_add(sum, qw[k]);
+                                    ++dag;
+                                }
+                        }
+                    }
+                    if (i + kStride < b1) {  // stage 2 of the next item
+                        cp_wait();
+                        bc_pf_records(pf, rec);
+                    }
+                    const double d = xf_mul_double(sv, sum);  // delta(v)
+                    rec_store_sigma(rec + v, lv, xf_q(d, sv));
+                    if (v != src && d != 0.0) bcs[v] += d;
+                }
+                cluster.sync();
+                bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
+            }
+        } else
         for (int Lb = levels - 1; Lb >= 0; --Lb) {
             const int b0 = loff[Lb], b1 = loff[Lb + 1];
             int deferred = 0;
@@ -984,12 +1091,23 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
             else
                 k_bc_cta<1, true><<<grid, kBcCta, 0, s>>>(a);
         } else {
+            const int dyn = kBcPipe ? int(kBcCta * sizeof(BcPf)) : 0;
+            static bool attr_set = false;
+            if (kBcPipe && !attr_set) {
+                GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<4, false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+                GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<2, false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+                GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<1, false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+                attr_set = true;
+            }
             if (CS == 4)
-                k_bc_cta<4, false><<<grid, kBcCta, 0, s>>>(a);
+                k_bc_cta<4, false><<<grid, kBcCta, dyn, s>>>(a);
             else if (CS == 2)
-                k_bc_cta<2, false><<<grid, kBcCta, 0, s>>>(a);
+                k_bc_cta<2, false><<<grid, kBcCta, dyn, s>>>(a);
             else
-                k_bc_cta<1, false><<<grid, kBcCta, 0, s>>>(a);
+                k_bc_cta<1, false><<<grid, kBcCta, dyn, s>>>(a);
         }
     });
     timed_launch(g, "bc_sum", [&] {
