@@ -663,6 +663,61 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         }
         if (ltid == 0) s_next_local[0] = s_next_local[1] = s_next_local[2] = 0;
         cluster.sync();
+        // one chunk of <= kNb neighbours of item i (level L): parents' sigma,
+        // claims (CAS) of undiscovered neighbours, the children list, the claims'
+        // log positions (one DSMEM atomic per converged lane group) and entries.
+        // mid1 / mid2 run while the CAS / the claim atomic are in flight.
+        auto fwd_chunk = [&](int i, int L, int end, int deg, const int32_t (&w)[kNb],
+                             const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc,
+                             auto&& mid1, auto&& mid2) {
+            bool par[kNb], got[kNb];
+            int32_t w0[kNb], w1[kNb], lnew[kNb];
+#pragma unroll
+            for (int k = 0; k < kNb; ++k) {
+                par[k] = a.undirected && L > 0 && lw[k] == base + L - 1;
+                const bool cand = w[k] >= 0 && lw[k] < base;
+                w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
+                w1[k] = cand ? a.offsets[w[k] + 1] : 0;
+                lnew[k] = cand ? atomicCAS(&rec[w[k]].level, lw[k], base + L + 1) : lw[k];
+                got[k] = cand && lnew[k] == lw[k];
+            }
+            mid1();  // pipelined path: the next item's dests while the CAS are in flight
+            if (!HEAVY && a.kids && deg <= kNb) {
+                // the children of v: neighbours claimed at this level, by v or
+                // not (a failed CAS returns the claimer's level) -- the
+                // backward pass reads them here instead of the adjacency
+                int32_t c[kNb];
+#pragma unroll
+                for (int k = 0; k < kNb; ++k)
+                    c[k] = w[k] >= 0 && (got[k] || lnew[k] == base + L + 1) ? w[k] : -1;
+                kids[i] = make_int4(c[0], c[1], c[2], c[3]);
+            }
+            // log positions: one DSMEM atomic per group of converged lanes
+            // (scan of the claim counts) instead of one per claim
+            {
+                cg::coalesced_group act = cg::coalesced_threads();
+                const int cnt = int(got[0]) + int(got[1]) + int(got[2]) + int(got[3]);
+                const int excl = cg::exclusive_scan(act, cnt);
+                const int last = int(act.size()) - 1;
+                const int tot = act.shfl(excl + cnt, last);
+                int qb = 0;
+                if (int(act.thread_rank()) == last && tot) {
+                    qb = atomicAdd(&s_next[L % 3], tot);
+#pragma unroll
+                    for (int q = 0; q < CS - 1; ++q) atomicAdd(&s_copy[q][L % 3], tot);
+                }
+                mid2();  // pipelined path: the next item's records while the claim atomic is in flight
+                int pos = end + act.shfl(qb, last) + excl;
+#pragma unroll
+                for (int k = 0; k < kNb; ++k) {
+                    if (par[k]) {  // ascending parent order
+                        acc = xf_add(acc, sg[k]);
+                        ++dag;
+                    }
+                    if (got[k]) log[pos++] = make_int4(w[k], w0[k], w1[k], 0);
+                }
+            }
+        };
         // ---- forward: iterateInBFS ----
         int beg = 0, end = 1, L = 0;
         for (;; ++L) {
@@ -696,51 +751,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
-                    bool par[kNb], got[kNb];
-                    int32_t w0[kNb], w1[kNb], lnew[kNb];
-#pragma unroll
-                    for (int k = 0; k < kNb; ++k) {
-                        par[k] = a.undirected && L > 0 && lw[k] == base + L - 1;
-                        const bool cand = w[k] >= 0 && lw[k] < base;
-                        w0[k] = cand ? a.offsets[w[k]] : 0;  // issued with the CAS
-                        w1[k] = cand ? a.offsets[w[k] + 1] : 0;
-                        lnew[k] = cand ? atomicCAS(&rec[w[k]].level, lw[k], base + L + 1) : lw[k];
-                        got[k] = cand && lnew[k] == lw[k];
-                    }
-                    if (!HEAVY && a.kids && oe - ob <= kNb) {
-                        // the children of v: neighbours claimed at this level, by v or
-                        // not (a failed CAS returns the claimer's level) -- the
-                        // backward pass reads them here instead of the adjacency
-                        int32_t c[kNb];
-#pragma unroll
-                        for (int k = 0; k < kNb; ++k)
-                            c[k] = w[k] >= 0 && (got[k] || lnew[k] == base + L + 1) ? w[k] : -1;
-                        kids[i] = make_int4(c[0], c[1], c[2], c[3]);
-                    }
-                    // log positions: one DSMEM atomic per group of converged lanes
-                    // (scan of the claim counts) instead of one per claim
-                    {
-                        cg::coalesced_group act = cg::coalesced_threads();
-                        const int cnt = int(got[0]) + int(got[1]) + int(got[2]) + int(got[3]);
-                        const int excl = cg::exclusive_scan(act, cnt);
-                        const int last = int(act.size()) - 1;
-                        const int tot = act.shfl(excl + cnt, last);
-                        int base = 0;
-                        if (int(act.thread_rank()) == last && tot) {
-                            base = atomicAdd(&s_next[L % 3], tot);
-#pragma unroll
-                            for (int q = 0; q < CS - 1; ++q) atomicAdd(&s_copy[q][L % 3], tot);
-                        }
-                        int pos = end + act.shfl(base, last) + excl;
-#pragma unroll
-                        for (int k = 0; k < kNb; ++k) {
-                            if (par[k]) {  // ascending parent order
-                                acc = xf_add(acc, sg[k]);
-                                ++dag;
-                            }
-                            if (got[k]) log[pos++] = make_int4(w[k], w0[k], w1[k], 0);
-                        }
-                    }
+                    fwd_chunk(i, L, end, oe - ob, w, lw, sg, acc, [] {}, [] {});
                 }
                 if (!a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
@@ -1093,7 +1104,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         } else {
             const int dyn = kBcPipe ? int(kBcCta * sizeof(BcPf)) : 0;
             static bool attr_set = false;
-            if (kBcPipe && !attr_set) {
+            if (dyn && !attr_set) {
                 GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<4, false>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
                 GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<2, false>,
