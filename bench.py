@@ -578,8 +578,10 @@ def bench_bc(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
     s = sts[-1]
     res["roofline"]["bytes_formula"] = ("per source 48 n_reached + 16 m_scanned + 24 m_dag "
                                         "(SURVEY.md 8(d))")
+    # summed over the call's sources: reached (s, v) pairs, edges the forward
+    # pass scanned, DAG edges (each counted once)
     res["roofline"]["counters_per_call"] = {"n_reached": s["vertices_visited"],
-                                            "m_scanned_fwd_plus_bwd": s["edges_visited"],
+                                            "m_scanned": s["edges_visited"],
                                             "m_dag": s["updates"]}
     if cpu_legs:
         port = _port()

@@ -316,7 +316,6 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
                 for (int k = 0; k < kNb; ++k)
                     if (ch[k] && sw[k].x > 0.0) {  // ascending child order (oracles.cpp:60-67)
                         d += xf_ratio(sv, sw[k]) * (1.0 + dw[k]);
-                        ++dag;
                     }
             }
             if (!heavy) a.delta[sb + v] = d;
@@ -337,7 +336,6 @@ __global__ void __launch_bounds__(kBcBlock) k_bc_backward(BcArgs a) {
                     const double2 sw = a.sig[sb + w];
                     if (sw.x > 0.0) {
                         d += xf_ratio(sv, sw) * (1.0 + a.delta[sb + w]);
-                        ++dag;
                     }
                 }
             }
@@ -586,8 +584,7 @@ __device__ __forceinline__ void bc_cta_heavy_forward(const BcCtaArgs& a, BcRec* 
 
 __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec* rec, const int4* log,
                                                    const int* s_h, int hn, int Lb, int32_t src,
-                                                   int32_t base, double* bcs, unsigned& bscan,
-                                                   unsigned& dag) {
+                                                   int32_t base, double* bcs) {
     const int ltid = threadIdx.x, lane = ltid & 31;
     for (int h = ltid >> 5; h < hn; h += kBcCta / 32) {
         const int4 it = log[s_h[h]];
@@ -596,14 +593,12 @@ __device__ __forceinline__ void bc_cta_heavy_backward(const BcCtaArgs& a, BcRec*
         XF sv;
         rec_level_sigma(rec + v, lv, sv);
         XF sum{0.0, 0};
-        if (lane == 0) bscan += oe - ob;
         for (int32_t e = ob + lane; e < oe; e += 32) {
             int32_t lw;
             XF qw;
             rec_level_sigma(rec + a.dests[e], lw, qw);
             if (lw == base + Lb + 1) {
                 sum = xf_add(sum, qw);
-                ++dag;
             }
         }
         sum = xf_warp_sum(sum);
@@ -645,7 +640,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     double* bcs = a.bcs + slot * bcs_stride(a.n);
     // per-source 32-bit counters (registers are the kernel's limit), flushed
     // to the 64-bit totals after every source
-    unsigned fscan = 0, bscan = 0, dag = 0;
+    unsigned fscan = 0, dag = 0;
     int tk = 0;
     int32_t base = a.base[slot];  // tag of the next source's level 0
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
@@ -824,7 +819,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     const int32_t lv = ow.x;
                     const XF sv{__hiloint2double(ow.w, ow.z), ow.y};
                     XF sum{0.0, 0};
-                    bscan += oe - ob;
                     if (kc.x != -2) {  // the recorded children, ascending
                         const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
                         int4 r[kNb];
@@ -840,7 +834,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         for (int k = 0; k < kNb; ++k)
                             if (w[k] >= 0) {
                                 sum = xf_add(sum, XF{__hiloint2double(r[k].w, r[k].z), r[k].y});
-                                ++dag;
                             }
                     } else {
                         const int in = i + kStride;
@@ -864,7 +857,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             for (int k = 0; k < kNb; ++k)
                                 if (w[k] >= 0 && lw[k] == base + Lb + 1) {
                                     sum = xf_add(sum, qw[k]);
-                                    ++dag;
                                 }
                         }
                     }
@@ -901,7 +893,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 XF sum{0.0, 0};
                 const int4 kc = !HEAVY && kids ? kids[i] : make_int4(-2, 0, 0, 0);
                 if (!HEAVY && kc.x != -2) {  // the recorded children, ascending
-                    bscan += oe - ob;  // the adjacency scan this replaces (stats)
                     const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
                     int32_t lw[kNb];
                     XF qw[kNb];
@@ -914,10 +905,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     for (int k = 0; k < kNb; ++k)
                         if (w[k] >= 0) {
                             sum = xf_add(sum, qw[k]);
-                            ++dag;
                         }
                 } else {
-                    bscan += oe - ob;
                     for (int32_t e = ob; e < oe; e += kNb) {
                         int32_t w[kNb], lw[kNb];
                         XF qw[kNb];
@@ -933,7 +922,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         for (int k = 0; k < kNb; ++k)
                             if (w[k] >= 0 && lw[k] == base + Lb + 1) {  // ascending child order
                                 sum = xf_add(sum, qw[k]);
-                                ++dag;
                             }
                     }
                 }
@@ -942,8 +930,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 if (v != src && d != 0.0) bcs[v] += d;  // leaves add nothing (one thread per v)
             }
             if (HEAVY && __syncthreads_count(deferred) > 0) {
-                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bcs,
-                                      bscan, dag);
+                bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bcs);
                 __syncthreads();
                 if (ltid == 0) s_hn = 0;
             }
@@ -951,18 +938,16 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
         }
         {
-            unsigned long long f = fscan, b = bscan, d = dag;
+            unsigned long long f = fscan, d = dag;
             for (int o = 16; o; o >>= 1) {
                 f += __shfl_xor_sync(0xffffffffu, f, o);
-                b += __shfl_xor_sync(0xffffffffu, b, o);
                 d += __shfl_xor_sync(0xffffffffu, d, o);
             }
             if ((ltid & 31) == 0) {
                 atomicAdd(&a.ctr[kFwdScan], f);
-                atomicAdd(&a.ctr[kBwdScan], b);
                 atomicAdd(&a.ctr[kDag], d);
             }
-            fscan = bscan = dag = 0;
+            fscan = dag = 0;
         }
         // the next source's tags start above every tag this one wrote
         base += levels + 1;
@@ -1294,7 +1279,10 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
             stats->rounds = max_levels;
             stats->launches = launches;
             stats->vertices_visited = int64_t(totals[kReached]);
-            stats->edges_visited = int64_t(totals[kFwdScan] + totals[kBwdScan]);
+            // m_scanned (the forward pass's scanned edges; the backward pass
+            // reads the same adjacency or the recorded children) and the DAG
+            // edges (counted once, as parents in the forward pass)
+            stats->edges_visited = int64_t(totals[kFwdScan]);
             stats->updates = int64_t(totals[kDag]);
             // SURVEY.md 8(d), per source: 48 n_reached + 16 m_scanned + 24 m_dag.
             // Per reached vertex: offsets, level, sigma, delta, bc read-modify-
