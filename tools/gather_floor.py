@@ -50,6 +50,14 @@ def main():
     print(f"index_select gather of an f32 array (L2-resident 4n bytes): {t:.3f} ms")
     t = timeit(lambda: torch.index_select(c32, 0, src2, out=o32))
     print(f"index_select gather f32, relabelled: {t:.3f} ms")
+    # sources compacted to the vertices with out-edges (order kept): the gathered
+    # array shrinks to the non-dangling vertices
+    nd = outdeg > 0
+    cidx = np.cumsum(nd) - 1
+    srcc = torch.from_numpy(cidx[h.rev_srcs].astype(np.int32)).cuda()
+    cc = torch.rand(int(nd.sum()), dtype=torch.float64, device="cuda")
+    t = timeit(lambda: torch.index_select(cc, 0, srcc, out=out))
+    print(f"index_select gather, sources compacted to {int(nd.sum())} non-dangling ({cc.numel() * 8 / 2**20:.0f} MB): {t:.3f} ms")
     indeg = np.diff(h.rev_offsets)
     print(f"in-degree: zero={np.mean(indeg == 0):.3f} max={indeg.max()} ; out-degree zero={np.mean(outdeg == 0):.3f} max={outdeg.max()}")
     hot = np.bincount(h.rev_srcs, minlength=n)
