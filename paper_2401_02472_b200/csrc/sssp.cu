@@ -448,6 +448,11 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ int s_warp[kFBlock / 32];
     __shared__ unsigned long long s_base;
+    // statistics (improved sinks, frontier vertices, their edges) accumulate in
+    // registers across the block's chunks and reach the counters with one
+    // atomic per block at the end: per-warp atomics on three single addresses
+    // serialise in L2 (262K of them per C5 round)
+    unsigned long long t_vis = 0, t_edg = 0, t_sinks = 0;
     for (int64_t c0 = v0 + int64_t(blockIdx.x) * kFBlock * kPer; c0 < v1;
          c0 += int64_t(gridDim.x) * kFBlock * kPer) {
         // all loads of the chunk are issued before any is consumed: the prev
@@ -484,16 +489,9 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
             }
             mine += items[k];
         }
-        if (sinks) atomicAdd(&ctr[1], (unsigned long long)sinks);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            vis += __shfl_xor_sync(full, vis, o);
-            edg += __shfl_xor_sync(full, edg, o);
-        }
-        if (lane == 0 && vis) {
-            atomicAdd(&ctr[3], vis);
-            atomicAdd(&ctr[4], edg);
-        }
+        t_sinks += sinks;
+        t_vis += vis;
+        t_edg += edg;
         int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -533,6 +531,26 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
             pos += items[k];
         }
         __syncthreads();
+    }
+    {
+        __shared__ unsigned long long s_red[3][kFBlock / 32];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            t_vis += __shfl_xor_sync(full, t_vis, o);
+            t_edg += __shfl_xor_sync(full, t_edg, o);
+            t_sinks += __shfl_xor_sync(full, t_sinks, o);
+        }
+        if (lane == 0) {
+            s_red[0][warp] = t_vis;
+            s_red[1][warp] = t_edg;
+            s_red[2][warp] = t_sinks;
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            unsigned long long x = 0;
+            for (int w = 0; w < kFBlock / 32; ++w) x += s_red[threadIdx.x][w];
+            if (x) atomicAdd(&ctr[threadIdx.x == 0 ? 3 : threadIdx.x == 1 ? 4 : 1], x);
+        }
     }
 }
 

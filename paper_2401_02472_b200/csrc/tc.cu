@@ -30,6 +30,8 @@ constexpr int kTcBlock = GDX_TC_BLOCK;
 // degree binning: a vertex with more (oriented) neighbours than this has its
 // pairs spread over the whole grid (k_tc_heavy / k_tc_heavy_mid)
 constexpr int kTcHeavy = 256;
+// acc layout: [count, work, work slots...] (the slots are summed on the host)
+constexpr int kTcSlots = 256;
 
 // first index in [lo, hi) with a[i] > x
 __device__ inline int32_t upper_bound_dev(const int32_t* __restrict__ a, int32_t lo, int32_t hi,
@@ -374,7 +376,9 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
     }
     if (lane == 0) {
         if (count) atomicAdd(&acc[0], count);
-        if (scanned) atomicAdd(&acc[1], scanned);
+        // the work counter is spread over kTcSlots addresses: ~300K warps
+        // adding to one address serialise in L2
+        if (scanned) atomicAdd(&acc[2 + (blockIdx.x & (kTcSlots - 1))], scanned);
     }
 }
 
@@ -639,8 +643,8 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
     cudaStream_t s = g->stream;
     if (!g->tc) g->tc = std::make_unique<TcPlan>();
     auto& P = *g->tc;
-    P.acc.ensure(2);
-    GDX_CUDA(cudaMemsetAsync(P.acc.get(), 0, 2 * sizeof(unsigned long long), s));
+    P.acc.ensure(2 + kTcSlots);
+    GDX_CUDA(cudaMemsetAsync(P.acc.get(), 0, (2 + kTcSlots) * sizeof(unsigned long long), s));
     v_begin = std::max(v_begin, 0);
     v_end = std::min(v_end, g->n);
     const bool oriented = !g->directed && std::getenv("GDX_TC_MIDDLE") == nullptr;
@@ -663,9 +667,12 @@ static void run_tc(gdx_graph* g, int32_t v_begin, int32_t v_end, int64_t* count_
             });
     }
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
-    GDX_CUDA(cudaMemcpyAsync(h, P.acc.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    static_assert((2 + kTcSlots) * sizeof(unsigned long long) <= 4096, "pinned staging page");
+    GDX_CUDA(cudaMemcpyAsync(h, P.acc.get(), (2 + kTcSlots) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
     *count_out = int64_t(h[0]);
+    for (int q = 0; q < kTcSlots; ++q) h[1] += h[2 + q];
     if (stats) {
         stats->rounds = 1;
         if (!oriented) stats->launches = v_end > v_begin ? 1 : 0;
