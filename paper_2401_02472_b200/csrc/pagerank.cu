@@ -400,6 +400,40 @@ __global__ void k_pr_grp_rows(int64_t ngroups, int64_t e_base, int64_t e_begin, 
     }
 }
 
+// The same index filled from the rows: row k owns the groups whose first edge
+// lies in [start_k, end_k) -- no binary search.  A lane takes a row; rows with
+// more than 32 groups (hubs) are written by the whole warp.
+__global__ void k_pr_grp_fill(int64_t ngroups, int64_t e_base, int64_t e_begin, int32_t nnz,
+                              const int2* __restrict__ nz, int2* grp) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; k0 < nnz;
+         k0 += nw * 32) {
+        const int64_t k = k0 + lane;
+        int64_t g0 = 0, g1 = 0;
+        int32_t end = 0;
+        if (k < nnz) {
+            const int64_t start = k > 0 ? nz[k - 1].y : e_begin;
+            end = nz[k].y;
+            // group g's first edge: e_begin for g = 0, e_base + 8 g after
+            g0 = k == 0 ? 0 : (start - e_base + kEdgeGroup - 1) / kEdgeGroup;
+            g1 = min((int64_t(end) - e_base + kEdgeGroup - 1) / kEdgeGroup, ngroups);
+        }
+        const bool big = g1 - g0 > 32;
+        if (!big)
+            for (int64_t g = g0; g < g1; ++g) grp[g] = make_int2(int32_t(k), end);
+        unsigned hubs = __ballot_sync(full, big);
+        while (hubs) {
+            const int l = __ffs(hubs) - 1;
+            hubs &= hubs - 1;
+            const int64_t h0 = __shfl_sync(full, g0, l), h1 = __shfl_sync(full, g1, l);
+            const int32_t hk = int32_t(__shfl_sync(full, k, l)), he = __shfl_sync(full, end, l);
+            for (int64_t g = h0 + lane; g < h1; g += 32) grp[g] = make_int2(hk, he);
+        }
+    }
+}
+
 // pr.sp:9 -- rank = 1/numNodes; contrib and the round-0 dangling mass.
 __global__ void __launch_bounds__(kPrBlock) k_pr_init(PrArgs a) {
     double dang_local = 0.0;
@@ -469,8 +503,12 @@ static void build_edge_plan(gdx_graph* g, PrPlan& P, int32_t v_begin, int32_t v_
     P.ngroups = (P.e_end - P.e_base + kEdgeGroup - 1) / kEdgeGroup;
     P.grp.alloc(size_t(P.ngroups) + 1);
     if (P.ngroups > 0) {
-        k_pr_grp_rows<<<blocks_for(P.ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
-            P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz.get(), P.grp.get());
+        if (std::getenv("GDX_PR_GRP_SEARCH"))  // A/B: one binary search per group
+            k_pr_grp_rows<<<blocks_for(P.ngroups, 256, g->num_sms * 16), 256, 0, s>>>(
+                P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz.get(), P.grp.get());
+        else
+            k_pr_grp_fill<<<blocks_for(int64_t(P.nnz), 256, g->num_sms * 16), 256, 0, s>>>(
+                P.ngroups, P.e_base, P.e_begin, P.nnz, P.nz.get(), P.grp.get());
         GDX_LAUNCH_CHECK();
     }
     P.row_sum.alloc(n);

@@ -437,13 +437,21 @@ static_assert(kShardChunk % 32 == 0 && kShardChunk >= 32, "GDX_SSSP_CHUNK must b
 #define GDX_SSSP_FBLOCK 256
 #endif
 constexpr int kFBlock = GDX_SSSP_FBLOCK;
-template <class D>
+#ifndef GDX_SSSP_FPER
+#define GDX_SSSP_FPER 8
+#endif
+constexpr int kFPer = GDX_SSSP_FPER;  // vertices per thread per scan chunk
+// graphs below 2^22 vertices scan 4 vertices per thread (more, shorter chunks:
+// same-box C1 0.279 -> 0.250 ms per call; C5 keeps 8: 19.1 vs 19.4 ms)
+constexpr int kFPerSmall = 4;
+constexpr int32_t kSmallScan = 1 << 22;
+template <class D, int PER = kFPer>
 __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int32_t v1,
                                                            const int32_t* __restrict__ offsets,
                                                            const D* __restrict__ dist, D* prev,
                                                            int2* queue,
                                                            unsigned long long* ctr) {
-    constexpr int kPer = 8;  // vertices per thread per chunk
+    constexpr int kPer = PER;  // vertices per thread per chunk
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ int s_warp[kFBlock / 32];
@@ -558,12 +566,24 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
 // 21.0 vs 21.35 ms with one resident wave of ~44-chunk blocks);
 // GDX_SSSP_FGRID = blocks per SM overrides.
 template <class D>
-static int frontier_grid(const gdx_graph* g, int64_t cnt) {
+static int frontier_grid(const gdx_graph* g, int64_t cnt, int per = kFPer) {
     static const int per_sm = [] {
         const char* e = std::getenv("GDX_SSSP_FGRID");
         return e ? std::max(1, std::atoi(e)) : 64;
     }();
-    return blocks_for(cnt, kFBlock * 8, g->num_sms * per_sm);
+    return blocks_for(cnt, kFBlock * per, g->num_sms * per_sm);
+}
+
+// The single-GPU round loop's scan: per-thread chunk by graph size.
+template <class D>
+static void launch_scan(const gdx_graph* g, cudaStream_t st, int32_t n, D* dist, D* prev,
+                        int2* queue, unsigned long long* ctr) {
+    if (n < kSmallScan)
+        k_sssp_scan_frontier<D, kFPerSmall><<<frontier_grid<D>(g, n, kFPerSmall), kFBlock, 0, st>>>(
+            0, n, g->offsets.get(), dist, prev, queue, ctr);
+    else
+        k_sssp_scan_frontier<D><<<frontier_grid<D>(g, n), kFBlock, 0, st>>>(
+            0, n, g->offsets.get(), dist, prev, queue, ctr);
 }
 
 
@@ -705,10 +725,8 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
     GDX_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
     const int32_t n = g->n;
-    const int fgrid = frontier_grid<D>(g, n);
     unsigned long long* ctr = w.shard_ctr.get();
-    k_sssp_scan_frontier<D><<<fgrid, kFBlock, 0, cs>>>(0, n, g->offsets.get(), dist, prev,
-                                                   w.shard_queue.get(), ctr);
+    launch_scan<D>(g, cs, n, dist, prev, w.shard_queue.get(), ctr);
     auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
             : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
     fn<<<relax_grid, 256, 0, cs>>>(w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
@@ -755,7 +773,6 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     unsigned long long vvis = 0, evis = 0;
     int rounds = 0, launches = 1;
-    const int fgrid = frontier_grid<D>(g, n);
     const char* lv = std::getenv("GDX_SSSP_LPI");
     const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
     const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
@@ -784,8 +801,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     for (; !use_graph; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
-            k_sssp_scan_frontier<D><<<fgrid, kFBlock, 0, s>>>(0, n, g->offsets.get(), dist, prev,
-                                                          w.shard_queue.get(), ctr);
+            launch_scan<D>(g, s, n, dist, prev, w.shard_queue.get(), ctr);
         });
         GDX_CUDA(cudaMemcpyAsync(h, ctr, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         GDX_CUDA(cudaStreamSynchronize(s));
