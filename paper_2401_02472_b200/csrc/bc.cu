@@ -418,7 +418,7 @@ struct BcCtaArgs {
     bool any_heavy;    // some vertex has more than kHeavy out- (or in-) edges
     int32_t* log;      // [grid][n] int4 (v, out-begin, out-end, 0): discovery order, levels contiguous
     int32_t* loff;     // [grid][n+2] level boundaries in log
-    int4* kids;        // [grid][n] children of each log entry (low-degree graphs) or nullptr
+    bool kids;         // record each item's children in its own log entry (low-degree graphs)
     double* bcs;       // [grid][n] the slot's partial scores (its sources in order), 0 between calls
     double* bc;
     unsigned long long* ctr;
@@ -510,7 +510,7 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
 #endif
 constexpr bool kBcPipe = GDX_BC_PIPE != 0;
 struct __align__(16) BcPf {
-    int4 log, kids, own, ch[kNb];
+    int4 log, own, ch[3];
 };
 __device__ inline void cp16(void* sdst, const void* gsrc) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
@@ -518,15 +518,16 @@ __device__ inline void cp16(void* sdst, const void* gsrc) {
 }
 __device__ inline void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ inline void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-// stage 2: the item's own record and its recorded children's (slot's log/kids ready)
+// stage 2: the item's own record and its recorded children's (slot's log entry ready)
 __device__ inline void bc_pf_records(BcPf* pf, const BcRec* rec) {
-    const int4 it = pf->log, kc = pf->kids;
-    cp16(&pf->own, rec + it.x);
-    if (kc.x != -2) {
-        const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
-#pragma unroll
-        for (int k = 0; k < kNb; ++k)
-            if (w[k] >= 0) cp16(&pf->ch[k], rec + w[k]);
+    const int4 it = pf->log;
+    if (it.x < 0) {  // (~v, children): see the forward pass
+        cp16(&pf->own, rec + ~it.x);
+        if (it.y >= 0) cp16(&pf->ch[0], rec + it.y);
+        if (it.z >= 0) cp16(&pf->ch[1], rec + it.z);
+        if (it.w >= 0) cp16(&pf->ch[2], rec + it.w);
+    } else {
+        cp16(&pf->own, rec + it.x);
     }
     cp_commit();
 }
@@ -636,7 +637,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     BcRec* rec = a.rec + slot * a.n;
     int4* log = reinterpret_cast<int4*>(a.log) + slot * a.n;  // (v, out-begin, out-end, 0)
     int32_t* loff = a.loff + slot * (int64_t(a.n) + 2);
-    int4* kids = a.kids ? a.kids + slot * a.n : nullptr;
+    // children recorded in the log entries: after the forward pass processed
+    // item i (vertex v), log[i] = (~v, c0, c1, c2) -- v's children (neighbours
+    // claimed at the next level, by v or not) in ascending order, -1 padded --
+    // when v has at most 3; otherwise it stays (v, out-begin, out-end) and the
+    // backward pass scans the adjacency.  (A vertex below the source has a
+    // parent, so on graphs of maximum degree 4 only the source can have 4.)
+    const bool kids = !HEAVY && a.kids;
     double* bcs = a.bcs + slot * bcs_stride(a.n);
     // per-source 32-bit counters (registers are the kernel's limit), flushed
     // to the 64-bit totals after every source
@@ -662,7 +669,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // claims (CAS) of undiscovered neighbours, the children list, the claims'
         // log positions (one DSMEM atomic per converged lane group) and entries.
         // mid1 / mid2 run while the CAS / the claim atomic are in flight.
-        auto fwd_chunk = [&](int i, int L, int end, int deg, const int32_t (&w)[kNb],
+        auto fwd_chunk = [&](int i, int32_t v, int L, int end, int deg, const int32_t (&w)[kNb],
                              const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc,
                              auto&& mid1, auto&& mid2) {
             bool par[kNb], got[kNb];
@@ -677,15 +684,21 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 got[k] = cand && lnew[k] == lw[k];
             }
             mid1();  // pipelined path: the next item's dests while the CAS are in flight
-            if (!HEAVY && a.kids && deg <= kNb) {
+            if (kids && deg <= kNb) {
                 // the children of v: neighbours claimed at this level, by v or
                 // not (a failed CAS returns the claimer's level) -- the
                 // backward pass reads them here instead of the adjacency
-                int32_t c[kNb];
+                int32_t c0 = -1, c1 = -1, c2 = -1;
+                int nc = 0;
 #pragma unroll
                 for (int k = 0; k < kNb; ++k)
-                    c[k] = w[k] >= 0 && (got[k] || lnew[k] == base + L + 1) ? w[k] : -1;
-                kids[i] = make_int4(c[0], c[1], c[2], c[3]);
+                    if (w[k] >= 0 && (got[k] || lnew[k] == base + L + 1)) {
+                        if (nc == 0) c0 = w[k];
+                        else if (nc == 1) c1 = w[k];
+                        else if (nc == 2) c2 = w[k];
+                        ++nc;
+                    }
+                if (nc <= 3) log[i] = make_int4(~v, c0, c1, c2);
             }
             // log positions: one DSMEM atomic per group of converged lanes
             // (scan of the claim counts) instead of one per claim
@@ -746,7 +759,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
-                    fwd_chunk(i, L, end, oe - ob, w, lw, sg, acc, [] {}, [] {});
+                    fwd_chunk(i, v, L, end, oe - ob, w, lw, sg, acc, [] {}, [] {});
                 }
                 if (!a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
@@ -770,8 +783,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             }
                     }
                 }
-                if (!HEAVY && a.kids && (oe - ob > kNb || oe == ob))  // scan fallback / none
-                    kids[i] = oe == ob ? make_int4(-1, -1, -1, -1) : make_int4(-2, -2, -2, -2);
+                if (kids && oe == ob) log[i] = make_int4(~v, -1, -1, -1);  // no children
                 rec_store_sigma(rec + v, base + L, acc);
             }
             // heavy items of this CTA: one warp each, lanes stride over the adjacency
@@ -807,39 +819,34 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 int i = b0 + tid;
                 if (i < b1) {  // the first item: both stages now
                     cp16(&pf->log, log + i);
-                    cp16(&pf->kids, kids + i);
                     cp_commit();
                     cp_wait();
                     bc_pf_records(pf, rec);
                 }
                 for (; i < b1; i += kStride) {
                     cp_wait();
-                    const int4 it = pf->log, kc = pf->kids, ow = pf->own;
-                    const int32_t v = it.x, ob = it.y, oe = it.z;
+                    const int4 it = pf->log, ow = pf->own;
+                    const bool kf = it.x < 0;  // (~v, children) or (v, out-begin, out-end)
+                    const int32_t v = kf ? ~it.x : it.x, ob = it.y, oe = it.z;
                     const int32_t lv = ow.x;
                     const XF sv{__hiloint2double(ow.w, ow.z), ow.y};
                     XF sum{0.0, 0};
-                    if (kc.x != -2) {  // the recorded children, ascending
-                        const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
-                        int4 r[kNb];
+                    const int in = i + kStride;
+                    if (kf) {  // the recorded children, ascending
+                        const int32_t w[3] = {it.y, it.z, it.w};
+                        int4 r[3];
 #pragma unroll
-                        for (int k = 0; k < kNb; ++k) r[k] = w[k] >= 0 ? pf->ch[k] : make_int4(0, 0, 0, 0);
-                        const int in = i + kStride;
+                        for (int k = 0; k < 3; ++k) r[k] = w[k] >= 0 ? pf->ch[k] : make_int4(0, 0, 0, 0);
                         if (in < b1) {  // stage 1 of the next item
                             cp16(&pf->log, log + in);
-                            cp16(&pf->kids, kids + in);
                             cp_commit();
                         }
 #pragma unroll
-                        for (int k = 0; k < kNb; ++k)
-                            if (w[k] >= 0) {
-                                sum = xf_add(sum, XF{__hiloint2double(r[k].w, r[k].z), r[k].y});
-                            }
+                        for (int k = 0; k < 3; ++k)
+                            if (w[k] >= 0) sum = xf_add(sum, XF{__hiloint2double(r[k].w, r[k].z), r[k].y});
                     } else {
-                        const int in = i + kStride;
                         if (in < b1) {
                             cp16(&pf->log, log + in);
-                            cp16(&pf->kids, kids + in);
                             cp_commit();
                         }
                         for (int32_t e = ob; e < oe; e += kNb) {
@@ -855,12 +862,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                             }
 #pragma unroll
                             for (int k = 0; k < kNb; ++k)
-                                if (w[k] >= 0 && lw[k] == base + Lb + 1) {
-                                    sum = xf_add(sum, qw[k]);
-                                }
+                                if (w[k] >= 0 && lw[k] == base + Lb + 1) sum = xf_add(sum, qw[k]);
                         }
                     }
-                    if (i + kStride < b1) {  // stage 2 of the next item
+                    if (in < b1) {  // stage 2 of the next item
                         cp_wait();
                         bc_pf_records(pf, rec);
                     }
@@ -877,7 +882,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             int deferred = 0;
             for (int i = b0 + tid; i < b1; i += kStride) {
                 const int4 it = log[i];
-                const int32_t v = it.x, ob = it.y, oe = it.z;
+                const bool kf = kids && it.x < 0;  // (~v, children) or (v, out-begin, out-end)
+                const int32_t v = kf ? ~it.x : it.x, ob = it.y, oe = it.z;
                 if (HEAVY && oe - ob > kHeavy) {
                     const int hp = atomicAdd(&s_hn, 1);
                     if (hp < kBcCta) {
@@ -891,21 +897,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 rec_level_sigma(rec + v, lv, sv);
                 // S = sum of the children's q(w) = (1 + delta(w)) / sigma(w), ascending
                 XF sum{0.0, 0};
-                const int4 kc = !HEAVY && kids ? kids[i] : make_int4(-2, 0, 0, 0);
-                if (!HEAVY && kc.x != -2) {  // the recorded children, ascending
-                    const int32_t w[kNb] = {kc.x, kc.y, kc.z, kc.w};
-                    int32_t lw[kNb];
-                    XF qw[kNb];
+                if (kf) {  // the recorded children, ascending
+                    const int32_t w[3] = {it.y, it.z, it.w};
+                    int32_t lw[3];
+                    XF qw[3];
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k) {
+                    for (int k = 0; k < 3; ++k) {
                         qw[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], qw[k]);
                     }
 #pragma unroll
-                    for (int k = 0; k < kNb; ++k)
-                        if (w[k] >= 0) {
-                            sum = xf_add(sum, qw[k]);
-                        }
+                    for (int k = 0; k < 3; ++k)
+                        if (w[k] >= 0) sum = xf_add(sum, qw[k]);
                 } else {
                     for (int32_t e = ob; e < oe; e += kNb) {
                         int32_t w[kNb], lw[kNb];
@@ -998,17 +1001,17 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     const bool any_heavy = graph_max_degree(g) > kHeavy;
     const char* kv = std::getenv("GDX_BC_KIDS");
     const bool a_kids = !any_heavy && !(kv && std::string(kv) == "0");
-    // a slot holds 44 B per vertex (record, log entry, level bound, partial score; + 16 B of
-    // children): fewer
+    // a slot holds 44 B per vertex (record, log entry -- later the children --,
+    // level bound, partial score): fewer
     // slots (each then runs several sources) when they would not fit (queried
     // only when the slots have to grow)
     if (W.cta_grid < slots) {
         size_t free_b = 0, tot_b = 0;
         GDX_CUDA(cudaMemGetInfo(&free_b, &tot_b));
-        const size_t per_slot = size_t(n) * (a_kids ? 60 : 44) + 8;
+        const size_t per_slot = size_t(n) * 44 + 8;
         const size_t held = W.cta_rec.bytes() + W.cta_log.bytes() + W.cta_loff.bytes() +
                             W.cta_bcs.bytes() +
-                            W.cta_kids.bytes() + pool_cached();
+                            pool_cached();
         const int64_t fit = int64_t(double(free_b + held) * 0.85 / double(per_slot));
         if (fit < 1)
             fail(GDX_ERR_OUT_OF_MEMORY, "OutOfMemory: BC needs " + std::to_string(per_slot) +
@@ -1023,7 +1026,6 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         W.log.release();
         W.cta_log.release();
         W.cta_loff.release();
-        W.cta_kids.release();
         W.batch = 0;
         W.cta_rec.alloc(size_t(slots) * n * 2);  // 16 B BcRec per (slot, vertex)
         W.cta_log.alloc(size_t(slots) * n * 4);  // int4 entries
@@ -1042,7 +1044,6 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
                                  cudaMemcpyHostToDevice, s));
         GDX_CUDA(cudaStreamSynchronize(s));  // `ones` is pageable and local
     }
-    if (a_kids) W.cta_kids.ensure(size_t(W.cta_grid) * n * 4);  // int4 per (slot, vertex)
     W.sources.ensure(size_t(nsrc));
     GDX_CUDA(cudaMemcpyAsync(W.sources.get(), hsrc.data(), size_t(nsrc) * 4,
                              cudaMemcpyHostToDevice, s));
@@ -1059,7 +1060,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     a.rec = reinterpret_cast<BcRec*>(W.cta_rec.get());
     a.base = W.cta_base.get();
     a.any_heavy = any_heavy;
-    a.kids = a_kids ? reinterpret_cast<int4*>(W.cta_kids.get()) : nullptr;
+    a.kids = a_kids;
     used_kids = a_kids;
     a.log = W.cta_log.get();
     a.loff = W.cta_loff.get();
@@ -1178,8 +1179,7 @@ extern "C" int gdx_bc(gdx_graph* g, const int32_t* sources, int32_t nsrc, double
                 W.cta_bcs.release();
                 W.cta_log.release();
                 W.cta_loff.release();
-                W.cta_kids.release();
-                W.cta_grid = 0;
+                        W.cta_grid = 0;
                 W.batch = 0;
             }
             // batch size: 36 bytes per (source, vertex) of state + log

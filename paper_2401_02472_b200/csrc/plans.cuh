@@ -152,7 +152,6 @@ struct BcWork {
     DevBuf<double> cta_bcs;     // [cta_grid][n] per-slot partial scores (summed in slot order)
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
-    DevBuf<int32_t> cta_kids;   // [cta_grid][n] int4: children of each log entry (or -2)
 };
 
 }  // namespace gdx
