@@ -76,6 +76,7 @@ struct SsspWork {
     int32_t shard_v0 = 0, shard_v1 = 0;
     int64_t shard_edges = 0;
     DevBuf<int2> shard_queue;
+    DevBuf<int2> small_queue;  // single-GPU rounds: vertices of <= 8 out-edges (one item each)
     DevBuf<unsigned long long> shard_ctr;  // [items, improved sinks, overflow, vertices, edges, changed]
     DevBuf<int32_t> shard_mark;  // delta mode: round in which a vertex was last listed as changed
     int32_t shard_round = 0;

@@ -445,17 +445,28 @@ constexpr int kFPer = GDX_SSSP_FPER;  // vertices per thread per scan chunk
 // same-box C1 0.279 -> 0.250 ms per call; C5 keeps 8: 19.1 vs 19.4 ms)
 constexpr int kFPerSmall = 4;
 constexpr int32_t kSmallScan = 1 << 22;
-template <class D, int PER = kFPer>
+// SPLIT (the single-GPU round loop): vertices with at most kSmallDeg out-edges
+// go to a second queue of one-item vertices, relaxed 2 lanes per item (lane
+// utilisation: a 3-edge vertex no longer occupies a 16-lane group); their
+// count is ctr[kSmallCtr].
+#ifndef GDX_SSSP_SMALLDEG
+#define GDX_SSSP_SMALLDEG 8
+#endif
+constexpr int kSmallDeg = GDX_SSSP_SMALLDEG;
+constexpr int kSmallLpi = kSmallDeg / 4;  // 4 edges per lane
+constexpr int kSmallCtr = 7;
+template <class D, int PER = kFPer, bool SPLIT = false>
 __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int32_t v1,
                                                            const int32_t* __restrict__ offsets,
                                                            const D* __restrict__ dist, D* prev,
                                                            int2* queue,
-                                                           unsigned long long* ctr) {
+                                                           unsigned long long* ctr,
+                                                           int2* squeue = nullptr) {
     constexpr int kPer = PER;  // vertices per thread per chunk
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ int s_warp[kFBlock / 32];
-    __shared__ unsigned long long s_base;
+    __shared__ unsigned long long s_warp[kFBlock / 32];  // (small << 32) | large item counts
+    __shared__ unsigned long long s_base, s_sbase;
     // statistics (improved sinks, frontier vertices, their edges) accumulate in
     // registers across the block's chunks and reach the counters with one
     // atomic per block at the end: per-warp atomics on three single addresses
@@ -481,50 +492,59 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
             first[k] = f ? offsets[v] : 0;
             last[k] = f ? offsets[v + 1] : -1;
         }
-        int mine = 0, sinks = 0;
+        unsigned long long mine = 0;  // (small items << 32) | large items
+        int sinks = 0;
         unsigned long long vis = 0, edg = 0;
+        bool small[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             items[k] = 0;
+            small[k] = false;
             if (last[k] >= 0) {
                 st_scan(prev + v, dk[k]);
                 const int32_t deg = last[k] - first[k];
-                items[k] = (deg + kShardChunk - 1) / kShardChunk;
+                small[k] = SPLIT && deg > 0 && deg <= kSmallDeg;
+                items[k] = small[k] ? 0 : (deg + kShardChunk - 1) / kShardChunk;
                 sinks += deg == 0;
                 ++vis;
                 edg += deg;
             }
-            mine += items[k];
+            mine += (unsigned long long)items[k] + (small[k] ? (1ull << 32) : 0ull);
         }
         t_sinks += sinks;
         t_vis += vis;
         t_edg += edg;
-        int incl = mine;
+        unsigned long long incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(full, incl, o);
+            const unsigned long long t = __shfl_up_sync(full, incl, o);
             if (lane >= o) incl += t;
         }
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
         if (threadIdx.x == 0) {
-            int tot = 0;
+            unsigned long long tot = 0;
             for (int w = 0; w < kFBlock / 32; ++w) {
-                const int x = s_warp[w];
+                const unsigned long long x = s_warp[w];
                 s_warp[w] = tot;
                 tot += x;
             }
-            s_base = tot ? atomicAdd(&ctr[0], (unsigned long long)tot) : 0;
+            const unsigned long long tl = tot & 0xffffffffull, ts = tot >> 32;
+            s_base = tl ? atomicAdd(&ctr[0], tl) : 0;
+            if (SPLIT) s_sbase = ts ? atomicAdd(&ctr[kSmallCtr], ts) : 0;
         }
         __syncthreads();
-        unsigned long long pos = s_base + s_warp[warp] + incl - mine;
+        const unsigned long long ex = s_warp[warp] + incl - mine;
+        unsigned long long pos = s_base + (ex & 0xffffffffull);
+        unsigned long long spos = SPLIT ? s_sbase + (ex >> 32) : 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int32_t v = int32_t(c0 + int64_t(k) * kFBlock + threadIdx.x);
             // a hub's items (a degree-10^6 vertex has ~10^4) are written by the
             // whole warp, not serially by its own lane
             const bool big = items[k] > kSplitItems;
+            if (SPLIT && small[k]) squeue[spos++] = make_int2(v, first[k]);
             if (!big)
                 for (int t = 0; t < items[k]; ++t) queue[pos + t] = make_int2(v, first[k] + t * kShardChunk);
             unsigned hubs = __ballot_sync(full, big);
@@ -577,13 +597,22 @@ static int frontier_grid(const gdx_graph* g, int64_t cnt, int per = kFPer) {
 // The single-GPU round loop's scan: per-thread chunk by graph size.
 template <class D>
 static void launch_scan(const gdx_graph* g, cudaStream_t st, int32_t n, D* dist, D* prev,
-                        int2* queue, unsigned long long* ctr) {
-    if (n < kSmallScan)
+                        int2* queue, unsigned long long* ctr, int2* squeue) {
+    if (squeue) {
+        if (n < kSmallScan)
+            k_sssp_scan_frontier<D, kFPerSmall, true>
+                <<<frontier_grid<D>(g, n, kFPerSmall), kFBlock, 0, st>>>(
+                    0, n, g->offsets.get(), dist, prev, queue, ctr, squeue);
+        else
+            k_sssp_scan_frontier<D, kFPer, true><<<frontier_grid<D>(g, n), kFBlock, 0, st>>>(
+                0, n, g->offsets.get(), dist, prev, queue, ctr, squeue);
+    } else if (n < kSmallScan) {
         k_sssp_scan_frontier<D, kFPerSmall><<<frontier_grid<D>(g, n, kFPerSmall), kFBlock, 0, st>>>(
             0, n, g->offsets.get(), dist, prev, queue, ctr);
-    else
+    } else {
         k_sssp_scan_frontier<D><<<frontier_grid<D>(g, n), kFBlock, 0, st>>>(
             0, n, g->offsets.get(), dist, prev, queue, ctr);
+    }
 }
 
 
@@ -599,7 +628,7 @@ struct SsspDelta {
     int32_t round;
 };
 
-template <class D, int LPI, bool DELTA = false>
+template <class D, int LPI, bool DELTA = false, int CH = kShardChunk>
 __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict__ queue,
                                                         const unsigned long long* __restrict__ ctr,
                                                         const int32_t* __restrict__ offsets,
@@ -611,14 +640,15 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
     // LPI lanes per item: lane groups of LPI take one item each
     const int sub = threadIdx.x & (LPI - 1);
     unsigned int issued = 0;  // relaxations that issued an atomicMin
-    constexpr int kU = kShardChunk / LPI;  // edges per lane per item, all loads issued together
+    constexpr int kU = CH / LPI;  // edges per lane per item, all loads issued together
+    static_assert(CH % LPI == 0, "an item's edges split evenly over its lanes");
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
         const int2 it = ld_stream(queue + i);
         const D dv = dist[it.x];
-        // int64: it.y + kShardChunk passes INT32_MAX on the last items of m ~ 2^31 graphs
-        const int32_t e1 = int32_t(min(int64_t(it.y) + kShardChunk, int64_t(offsets[it.x + 1])));
+        // int64: it.y + CH passes INT32_MAX on the last items of m ~ 2^31 graphs
+        const int32_t e1 = int32_t(min(int64_t(it.y) + CH, int64_t(offsets[it.x + 1])));
         int32_t u[kU];
         D c[kU], du[kU];
 #pragma unroll
@@ -649,6 +679,23 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
             }
     }
     if (upd) warp_count(issued, upd);
+}
+
+// The round's relaxations: the <= 64-edge items (LPI lanes each) and, with the
+// split queue, the small vertices' one items (2 lanes, <= kSmallDeg edges).
+template <class D>
+static void launch_relax(const gdx_graph* g, cudaStream_t st, int lpi, int grid, const int2* queue,
+                         const unsigned long long* ctr, const int2* squeue, D* dist,
+                         unsigned long long* ovf, unsigned long long* upd) {
+    const int32_t* w = g->weighted ? g->weights.get() : nullptr;
+    auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
+            : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
+    fn<<<grid, 256, 0, st>>>(queue, ctr, g->offsets.get(), g->dests.get(), w, dist, ovf,
+                             SsspDelta{}, upd);
+    if (squeue)
+        k_sssp_scan_relax<D, kSmallLpi, false, kSmallDeg><<<grid, 256, 0, st>>>(
+            squeue, ctr + kSmallCtr, g->offsets.get(), g->dests.get(), w, dist, ovf, SsspDelta{},
+            upd);
 }
 
 // (id, value) pairs of the vertices listed by a delta relaxation.
@@ -695,18 +742,19 @@ __global__ void k_sssp_scan_init(int32_t n, int32_t src, D inf, D* dist, D* prev
 // round trip per round.
 __global__ void k_sssp_graph_finish(unsigned long long* ctr, unsigned long long* acc,
                                     cudaGraphConditionalHandle h) {
-    const unsigned long long items = ctr[0];
+    const unsigned long long items = ctr[0] + ctr[kSmallCtr];
     if (items) acc[0] += 1;
     acc[1] += ctr[3];
     acc[2] += ctr[4];
     for (int i = 0; i < 5; ++i) ctr[i] = 0;
+    ctr[kSmallCtr] = 0;
     // a narrow-width overflow ends the loop at once (the call reruns wider)
     cudaGraphSetConditional(h, items && !acc[3] ? 1u : 0u);
 }
 
 template <class D>
 static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned long long* ovf,
-                                        int lpi, int relax_grid) {
+                                        int lpi, int relax_grid, int2* squeue) {
     auto& w = *g->sssp;
     cudaGraph_t graph;
     GDX_CUDA(cudaGraphCreate(&graph, 0));
@@ -726,12 +774,9 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
                                            cudaStreamCaptureModeRelaxed));
     const int32_t n = g->n;
     unsigned long long* ctr = w.shard_ctr.get();
-    launch_scan<D>(g, cs, n, dist, prev, w.shard_queue.get(), ctr);
-    auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
-            : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
-    fn<<<relax_grid, 256, 0, cs>>>(w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
-                                   g->weighted ? g->weights.get() : nullptr, dist, ovf, SsspDelta{},
-                                   w.upd_slots.get());
+    launch_scan<D>(g, cs, n, dist, prev, w.shard_queue.get(), ctr, squeue);
+    launch_relax<D>(g, cs, lpi, relax_grid, w.shard_queue.get(), ctr, squeue, dist, ovf,
+                    w.upd_slots.get());
     k_sssp_graph_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), h);
     cudaGraph_t captured;
     GDX_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -757,9 +802,16 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const D inf = sizeof(D) < 8 ? std::numeric_limits<D>::max() : D(INT64_MAX / 2);
     const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
     w.shard_queue.ensure(items_cap);
-    w.shard_ctr.ensure(kUpdSlot + 1);
+    w.shard_ctr.ensure(kSmallCtr + 1);
     w.upd_slots.ensure(kUpdSlots);
     unsigned long long* ctr = w.shard_ctr.get();
+    // large graphs: small vertices in their own queue (one more launch per
+    // round: same-box C5 19.18 -> 18.65 ms, C1 0.226 -> 0.246 ms, so graphs
+    // below 2^22 vertices keep one queue; GDX_SSSP_SPLIT=0/1 overrides)
+    const char* spl = std::getenv("GDX_SSSP_SPLIT");
+    const bool split = spl ? std::atoi(spl) != 0 : n >= kSmallScan;
+    if (split) w.small_queue.ensure(size_t(n));
+    int2* squeue = split ? w.small_queue.get() : nullptr;
     // graph path: round counters, [rounds, vertices, edges, overflow] in
     // graph_acc; host loop: its own overflow flag
     w.graph_acc.ensure(4);
@@ -767,7 +819,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     unsigned long long* ovf_flag = use_graph ? w.graph_acc.get() + 3 : ovf.get();
     timed_launch(g, "sssp_init", [&] {
         k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-            n, src, inf, dist, prev, ctr, kUpdSlot + 1, use_graph ? w.graph_acc.get() : ovf.get(),
+            n, src, inf, dist, prev, ctr, kSmallCtr + 1, use_graph ? w.graph_acc.get() : ovf.get(),
             use_graph ? 4 : 1, w.upd_slots.get());
     });
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
@@ -787,37 +839,36 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         void* key[SsspWork::kKey] = {dist, prev, w.shard_queue.get(), ctr, w.graph_acc.get(),
                                      g->offsets.get(), g->dests.get(),
                                      g->weighted ? g->weights.get() : nullptr,
-                                     reinterpret_cast<void*>(intptr_t(lpi * 65536 + relax_grid)),
+                                     reinterpret_cast<void*>(intptr_t(lpi * 65536 + relax_grid) |
+                                                             (intptr_t(split) << 40)),
                                      w.upd_slots.get()};
         bool same = w.gexec[di] != nullptr;
         for (int i = 0; i < SsspWork::kKey; ++i) same = same && w.gkey[di][i] == key[i];
         if (!same) {
             if (w.gexec[di]) cudaGraphExecDestroy(w.gexec[di]);
-            w.gexec[di] = build_sssp_graph<D>(g, dist, prev, ovf_flag, lpi, relax_grid);
+            w.gexec[di] = build_sssp_graph<D>(g, dist, prev, ovf_flag, lpi, relax_grid, squeue);
             for (int i = 0; i < SsspWork::kKey; ++i) w.gkey[di][i] = key[i];
         }
         timed_launch(g, "sssp_graph", [&] { GDX_CUDA(cudaGraphLaunch(w.gexec[di], s)); });
     }
     for (; !use_graph; ++rounds) {
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
+        GDX_CUDA(cudaMemsetAsync(ctr + kSmallCtr, 0, sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
-            launch_scan<D>(g, s, n, dist, prev, w.shard_queue.get(), ctr);
+            launch_scan<D>(g, s, n, dist, prev, w.shard_queue.get(), ctr, squeue);
         });
-        GDX_CUDA(cudaMemcpyAsync(h, ctr, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaMemcpyAsync(h, ctr, (kSmallCtr + 1) * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
         GDX_CUDA(cudaStreamSynchronize(s));
         ++launches;
         vvis += h[3];
         evis += h[4];
-        if (h[0] == 0) break;
+        if (h[0] + h[kSmallCtr] == 0) break;
         timed_launch(g, "sssp_relax", [&] {
-            auto fn = lpi == 8 ? k_sssp_scan_relax<D, 8>
-                    : lpi == 16 ? k_sssp_scan_relax<D, 16> : k_sssp_scan_relax<D, 32>;
-            fn<<<relax_grid, 256, 0, s>>>(w.shard_queue.get(), ctr, g->offsets.get(),
-                                               g->dests.get(),
-                                               g->weighted ? g->weights.get() : nullptr, dist,
-                                               ovf.get(), SsspDelta{}, w.upd_slots.get());
+            launch_relax<D>(g, s, lpi, relax_grid, w.shard_queue.get(), ctr, squeue, dist,
+                            ovf.get(), w.upd_slots.get());
         });
-        ++launches;
+        launches += split ? 2 : 1;
     }
     cudaPointerAttributes pa;
     bool dev_out = cudaPointerGetAttributes(&pa, dist_out) == cudaSuccess &&
@@ -843,7 +894,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         rounds = int(h[0]);
         vvis = h[1];
         evis = h[2];
-        launches += 3 * (rounds + 1);
+        launches += (split ? 4 : 3) * (rounds + 1);
     }
     if (stats) {
         stats->rounds = rounds;

@@ -172,11 +172,13 @@ def test_sssp_c1_bit_exact(gdx, port):
             assert st["rounds"] >= 2 and st["edges_visited"] >= g.m * 0.5
 
 
-@pytest.mark.parametrize("mode", ["persistent", "scan", "graph"])
+@pytest.mark.parametrize("mode", ["persistent", "scan", "graph", "scan_split", "graph_split"])
 def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
     """Both SSSP executions (persistent cooperative kernel for small graphs,
-    frontier-scan rounds for large ones) are bit-exact on config 1."""
-    monkeypatch.setenv("GDX_SSSP_MODE", mode)
+    frontier-scan rounds for large ones) are bit-exact on config 1; *_split:
+    the large-graph form with small vertices (<= 8 edges) in their own queue."""
+    monkeypatch.setenv("GDX_SSSP_MODE", mode.split("_")[0])
+    monkeypatch.setenv("GDX_SSSP_SPLIT", "1" if mode.endswith("split") else "0")
     u, v = port.gen_rmat_edges(1 << 18, 1 << 22, 1)
     g = port.with_random_weights(port.build_from_edges(1 << 18, u, v, None, False), 1, 100, 1)
     dg = gdx.DeviceGraph.from_csr(g)
