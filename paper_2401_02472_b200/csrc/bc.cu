@@ -1079,6 +1079,10 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
     }
     if (g->directed && (!a.in_offsets || !a.in_srcs))
         fail(GDX_ERR_UNSUPPORTED, "Unsupported: directed BC needs the reverse CSR");
+    // the slot partials are cleared by the sum kernel; a call that stopped
+    // between the two (an error) leaves them dirty: clear them before reuse
+    if (W.cta_dirty) GDX_CUDA(cudaMemsetAsync(W.cta_bcs.get(), 0, W.cta_bcs.bytes(), s));
+    W.cta_dirty = true;
     timed_launch(g, "bc_cta", [&] {
         if (a.any_heavy) {
             if (CS == 4)
@@ -1111,6 +1115,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
         k_bc_slot_sum<<<blocks_for((n + 1) / 2, 256, g->num_sms * 8), 256, 0, s>>>(
             int32_t(n), bcs_stride(n), slots, a.bcs, a.bc);
     });
+    W.cta_dirty = false;
     launches += 2;
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     GDX_CUDA(cudaMemcpyAsync(h, W.ctrs.get(), kBcCtrs * 8, cudaMemcpyDeviceToHost, s));

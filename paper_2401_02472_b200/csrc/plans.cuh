@@ -151,6 +151,7 @@ struct BcWork {
     DevBuf<double> cta_rec;     // [cta_grid][n] x 16 B (level tag, exponent, mantissa)
     DevBuf<int32_t> cta_base;   // [cta_grid] level tag base of each slot's next source
     DevBuf<double> cta_bcs;     // [cta_grid][n] per-slot partial scores (summed in slot order)
+    bool cta_dirty = false;     // partials written but not yet summed (and cleared)
     DevBuf<int32_t> cta_log;    // [cta_grid][n] int4
     DevBuf<int32_t> cta_loff;   // [cta_grid][n+2]
 };
