@@ -681,9 +681,18 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
     v.offsets, v.rev_offsets, v.rev_srcs = pin["offsets"], pin["rev_offsets"], pin["rev_srcs"]
     v.dests = v.weights = v.rev_eid = None
 
+    rank_host = torch.empty(n, dtype=torch.float64).pin_memory()
+
     def e2e_step():
+        # the same exchange as the timed rounds; the full rank vector lands in
+        # pinned host memory
         g2 = gdx.DeviceGraph.from_csr(v, device=dist.local)
-        _, r = D.sharded_pr(D.DeviceExecutor(g2), 0.85, 1e-6, 100, to_host=True)
+        ex2 = D.DeviceExecutor(g2)
+        if exchange["kind"] == "p2p":
+            out, r = D.sharded_pr_p2p(ex2, 0.85, 1e-6, 100, to_host=False)
+        else:
+            out, r = D.sharded_pr(ex2, 0.85, 1e-6, 100, to_host=False)
+        rank_host.copy_(out)
         g2.close()
         return r
 
@@ -697,7 +706,8 @@ def bench_pr_sharded(torch, gdx, dist, args, pk) -> dict:
     res["e2e"] = {"value": float(m) * sum(rr) / e2e_s / 1e9, "unit": "GTEPS",
                   "h2d_bytes_per_step": int(sum(t.numel() * 4 for t in pin.values())),
                   "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3 / args.steps,
-                  "path": "per rank: gdx_graph_create(host CSR) + sharded_pr (NCCL) + host rank"}
+                  "path": f"per rank: gdx_graph_create(host CSR) + sharded PR ({exchange['kind']}) "
+                          "+ rank gather to pinned host memory"}
     return res
 
 
@@ -916,6 +926,10 @@ def spawn_ranks(args) -> int:
 
 
 def main() -> None:
+    # NCCL's log (banner, INFO lines when NCCL_DEBUG is set) goes to a file, not
+    # to stdout: rank 0's stdout carries exactly the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(tempfile.gettempdir(),
+                                                          "gdx_nccl.%h.%p.log"))
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
