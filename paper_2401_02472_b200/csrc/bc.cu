@@ -652,6 +652,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
     int32_t base = a.base[slot];  // tag of the next source's level 0
     for (int32_t si = int32_t(slot); si < a.nsrc; si += nslots) {
         const int32_t src = a.sources[si];
+        const bool first_src = si == int32_t(slot);
         if (int64_t(base) + a.n + 2 > INT32_MAX) {  // tags exhausted: clear the slot
             for (int i = tid; i < a.n; i += kStride) rec[i].level = 0;
             base = 1;
@@ -871,7 +872,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     }
                     const double d = xf_mul_double(sv, sum);  // delta(v)
                     rec_store_sigma(rec + v, lv, xf_q(d, sv));
-                    if (v != src && d != 0.0) bcs[v] += d;
+                    if (v != src && d != 0.0) bcs[v] = first_src ? d : bcs[v] + d;
                 }
                 cluster.sync();
                 bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
@@ -930,7 +931,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 const double d = xf_mul_double(sv, sum);  // delta(v)
                 rec_store_sigma(rec + v, lv, xf_q(d, sv));
-                if (v != src && d != 0.0) bcs[v] += d;  // leaves add nothing (one thread per v)
+                // leaves add nothing (one thread per v); the slot's first source of
+                // the call stores (its partials were cleared by the last sum)
+                if (v != src && d != 0.0) bcs[v] = first_src ? d : bcs[v] + d;
             }
             if (HEAVY && __syncthreads_count(deferred) > 0) {
                 bc_cta_heavy_backward(a, rec, log, s_h, min(s_hn, kBcCta), Lb, src, base, bcs);
