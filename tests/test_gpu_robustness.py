@@ -80,6 +80,24 @@ def test_sssp_after_set_hash_weights(gdx, port):
     assert not np.array_equal(d_w, d_unit)
 
 
+def test_sssp_reweighted_in_place(gdx, port, monkeypatch):
+    """Reweighting a handle in place (same weight buffer) with a larger maximum
+    weight must not replay a round loop whose overflow test assumed the old
+    maximum: the cached loop is keyed on it (16-bit distances forced, so the
+    second weighting overflows them and the call reruns wider)."""
+    monkeypatch.setenv("GDX_SSSP_NARROW", "1")
+    monkeypatch.setenv("GDX_SSSP_MODE", "graph")
+    gu, gv = port.gen_grid_ctr(100, 2.0, 1)
+    g = port.build_from_edges(100 * 100, gu, gv, None, False)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for lo, hi in ((1, 10), (300, 600), (1, 10)):
+        dg.set_random_weights(lo, hi, 3)
+        h = dg.download()
+        hw = G(h.n, h.m, False, h.offsets, h.dests, h.weights)
+        exp = port.sssp(hw, 0)
+        assert np.array_equal(dg.sssp(0), exp), (lo, hi)
+
+
 def test_undirected_view_must_be_symmetric(gdx):
     """An undirected view with a missing mirror edge is rejected (the handle
     reads the forward arrays as the reverse CSR and TC sizes from them)."""
