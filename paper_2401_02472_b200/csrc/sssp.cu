@@ -389,12 +389,6 @@ constexpr int kSplitItems = 8;   // vertices with more items are emitted warp-co
 #endif
 constexpr int kUpdSlot = 6;  // shard_ctr slot counting issued relaxations (U)
 constexpr int kShardChunk = GDX_SSSP_CHUNK;
-// L2 policy of the streamed arrays (A/B knob): 1 = the relaxation's items,
-// dests and weights are loaded evict-first (ld.global.cs), 2 = also the
-// scan's prev array, so the hot dist lines of the gathers stay in L2
-#ifndef GDX_SSSP_HINT
-#define GDX_SSSP_HINT 0
-#endif
 // atomicMin over any distance width: 16-bit distances (the narrow first
 // attempt of large graphs) take a CAS loop on their aligned 32-bit word.
 __device__ __forceinline__ unsigned short dist_atomic_min(unsigned short* p, unsigned short v) {
@@ -412,21 +406,7 @@ __device__ __forceinline__ unsigned short dist_atomic_min(unsigned short* p, uns
 template <class D>
 __device__ __forceinline__ D dist_atomic_min(D* p, D v) { return atomicMin(p, v); }
 
-template <class T>
-__device__ __forceinline__ T ld_stream(const T* p) {
-    if constexpr (GDX_SSSP_HINT >= 1) return __ldcs(p);
-    else return *p;
-}
-template <class T>
-__device__ __forceinline__ T ld_scan(const T* p) {
-    if constexpr (GDX_SSSP_HINT >= 2) return __ldcs(p);
-    else return *p;
-}
-template <class T>
-__device__ __forceinline__ void st_scan(T* p, T v) {
-    if constexpr (GDX_SSSP_HINT >= 2) __stcs(p, v);
-    else *p = v;
-}  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
+  // edges per relaxation item (same-box C5: 21.0 ms vs 22.2 at 32, 24.4 at 128)
 // every relaxation kernel splits an item over LPI in {8, 16, 32} lanes
 static_assert(kShardChunk % 32 == 0 && kShardChunk >= 32, "GDX_SSSP_CHUNK must be a multiple of 32");
 
@@ -482,7 +462,7 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
         for (int k = 0; k < kPer; ++k) {
             const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
             dk[k] = v < v1 ? dist[v] : D(0);
-            pk[k] = v < v1 ? ld_scan(prev + v) : D(0);
+            pk[k] = v < v1 ? prev[v] : D(0);
         }
         int items[kPer], first[kPer], last[kPer];
 #pragma unroll
@@ -502,7 +482,7 @@ __global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int3
             items[k] = 0;
             small[k] = false;
             if (last[k] >= 0) {
-                st_scan(prev + v, dk[k]);
+                prev[v] = dk[k];
                 const int32_t deg = last[k] - first[k];
                 small[k] = SPLIT && deg > 0 && deg <= kSmallDeg;
                 items[k] = small[k] ? 0 : (deg + kShardChunk - 1) / kShardChunk;
@@ -645,7 +625,7 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
-        const int2 it = ld_stream(queue + i);
+        const int2 it = queue[i];
         const D dv = dist[it.x];
         // int64: it.y + CH passes INT32_MAX on the last items of m ~ 2^31 graphs
         const int32_t e1 = int32_t(min(int64_t(it.y) + CH, int64_t(offsets[it.x + 1])));
@@ -654,8 +634,8 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
             const int32_t e = it.y + sub + k * LPI;
-            u[k] = e < e1 ? ld_stream(dests + e) : -1;
-            const D w = e < e1 ? (weights ? D(ld_stream(weights + e)) : D(1)) : D(0);
+            u[k] = e < e1 ? dests[e] : -1;
+            const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
             c[k] = dv + w;
             if (sizeof(D) < 8 && u[k] >= 0 &&
                 uint64_t(dv) + uint64_t(w) >= uint64_t(std::numeric_limits<D>::max())) {
