@@ -127,6 +127,7 @@ struct TcPlan {
     DevBuf<long long> heavy_pre;       // their pair prefix
     DevBuf<int32_t> off_plus;  // oriented CSR (undirected graphs): N+(v) = N(v) ∩ (v, inf)
     DevBuf<int32_t> adj_plus;
+    DevBuf<unsigned long long> sigp;  // per adj+ entry: signature of that vertex's N+ (pair filter)
     DevBuf<uint8_t> scan_tmp;
     bool oriented = false;     // off+/adj+ built (once per handle: the graph is immutable)
     double survey_pairs = 0;   // sum over oriented edges of d+(u) + d+(v)

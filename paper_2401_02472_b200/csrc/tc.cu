@@ -218,6 +218,38 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
     }
 }
 
+// Pair filter (GDX_TC_SIG): every vertex x has a 64-bit signature -- one bit
+// per element w of N+(x), bit = hash(w) -- and sigp[i] = signature of adj+[i]
+// sits beside each entry of adj+, so the v side of a pair streams it in order.
+// A pair (v, u) whose short tail of N+(v) after u shares no signature bit with
+// N+(u) has no common element: it is skipped without touching N+(u) or its
+// off+ range -- the random DRAM access that bounds the kernel.  Exact: a
+// common element would set the same bit on both sides.
+#ifndef GDX_TC_SIG
+#define GDX_TC_SIG 1
+#endif
+constexpr bool kTcSig = GDX_TC_SIG != 0;
+constexpr int kSigTail = 16;  // longer tails are not filtered (hashing them costs more)
+__device__ __forceinline__ unsigned long long sig_bit(int32_t x) {
+    return 1ull << ((uint32_t(x) * 0x9E3779B1u) >> 26);
+}
+__global__ void k_tc_sig(int32_t n, const int32_t* __restrict__ off_plus,
+                         const int32_t* __restrict__ adj, unsigned long long* __restrict__ sig) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long b = 0;
+        for (int32_t i = off_plus[v], e = off_plus[v + 1]; i < e; ++i) b |= sig_bit(adj[i]);
+        sig[v] = b;
+    }
+}
+__global__ void k_tc_sigp(int64_t cnt, const int32_t* __restrict__ adj,
+                          const unsigned long long* __restrict__ sig,
+                          unsigned long long* __restrict__ sigp) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        sigp[i] = sig[adj[i]];
+}
+
 #ifndef GDX_TC_STAGE
 #define GDX_TC_STAGE 512
 #endif
@@ -226,11 +258,15 @@ constexpr int kTcStage = GDX_TC_STAGE;  // ints of staged N+ lists per warp
 __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
                                                           const int32_t* __restrict__ off_plus,
                                                           const int32_t* __restrict__ adj,
-                                                          unsigned long long* acc) {
+                                                          unsigned long long* acc,
+                                                          const unsigned long long* __restrict__ sigp =
+                                                              nullptr) {
     const unsigned full = 0xffffffffu;
     __shared__ int32_t stage[kTcBlock / 32][kTcStage];
+    __shared__ uint16_t s_list[kTcBlock / 32][kTcStage];  // the warp's pairs that pass the filter
     const int lane = threadIdx.x & 31;
     int32_t* sA = stage[threadIdx.x >> 5];
+    uint16_t* sL = s_list[threadIdx.x >> 5];
     const int64_t gwarp = (blockIdx.x * (int64_t)kTcBlock + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * (kTcBlock / 32);
     const int4* adj4 = reinterpret_cast<const int4*>(adj);
@@ -251,6 +287,36 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
             for (int32_t i = lane; i < rlen; i += 32) sA[i] = adj[r0 + i];
         __syncwarp();
         const int32_t* A = staged ? sA - r0 : adj;  // A[x] for x in [r0, last_end)
+        // The pair filter, computed here for every staged entry (its pair is
+        // (owner vertex, entry)) in one coalesced pass: the pairs that pass are
+        // listed in shared memory and only they are spread over the lanes --
+        // a filtered pair costs neither its random N+(u) fetch nor a lane slot.
+        const bool filt = kTcSig && sigp && staged;
+        int ntp = 0;  // pairs that pass
+        if (filt) {
+            for (int32_t i0 = 0; i0 < rlen; i0 += 32) {
+                const int32_t q = r0 + i0 + lane;
+                int k = 0;  // the warp's vertex lane whose list holds entry q
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int c = k + step;
+                    const int32_t st = __shfl_sync(full, valid ? ob : INT32_MAX, c & 31);
+                    if (c < 32 && st <= q) k = c;
+                }
+                const int32_t kend = __shfl_sync(full, oe, k);
+                const int32_t kbeg = __shfl_sync(full, ob, k);
+                bool pass = i0 + lane < rlen && q < kend - 1 && kend - kbeg <= kTcHeavy;
+                if (pass && kend - q - 1 <= kSigTail) {
+                    unsigned long long ts = 0;
+                    for (int32_t x = q + 1; x < kend; ++x) ts |= sig_bit(A[x]);
+                    pass = (ts & sigp[q]) != 0;
+                }
+                const unsigned m = __ballot_sync(full, pass);
+                if (pass) sL[ntp + __popc(m & ((1u << lane) - 1))] = uint16_t(q - r0);
+                ntp += __popc(m);
+            }
+            __syncwarp();
+        }
         // pairs (v, i): u = N+(v)[i] for i < len-1 (the last u has no tail)
         // heavy vertices (|N+(v)| > kTcHeavy) are left to k_tc_heavy, which
         // spreads their pairs over the whole grid instead of one warp
@@ -278,18 +344,31 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
             koe = __shfl_sync(full, oe, k);
             pu = kob + (j - __shfl_sync(full, excl, k));
         };
+        // filtered warps walk their listed pairs: entry -> owner list's end
+        auto locate_f = [&](int j, int32_t& pu_, int32_t& koe_) {
+            pu_ = r0 + (j < ntp ? int32_t(sL[j]) : 0);
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int c = k + step;
+                const int32_t st = __shfl_sync(full, valid ? ob : INT32_MAX, c & 31);
+                if (c < 32 && st <= pu_) k = c;
+            }
+            koe_ = __shfl_sync(full, oe, k);
+        };
+        const int npairs = filt ? ntp : total;
         int32_t pu = 0, koe = 0, bb = 0, be = 0;
-        locate(lane, pu, koe);
-        if (lane < total) {
+        if (filt) locate_f(lane, pu, koe); else locate(lane, pu, koe);
+        if (lane < npairs) {
             const int32_t u = A[pu];
             bb = off_plus[u];
             be = off_plus[u + 1];
         }
-        for (int j0 = 0; j0 < total; j0 += 32) {
-            const bool have = j0 + lane < total;
+        for (int j0 = 0; j0 < npairs; j0 += 32) {
+            const bool have = j0 + lane < npairs;
             const int32_t cpu = pu, ckoe = koe, cbb = bb, cbe = be;
-            locate(j0 + 32 + lane, pu, koe);
-            if (j0 + 32 + lane < total) {
+            if (filt) locate_f(j0 + 32 + lane, pu, koe); else locate(j0 + 32 + lane, pu, koe);
+            if (j0 + 32 + lane < npairs) {
                 const int32_t u = A[pu];
                 bb = off_plus[u];
                 be = off_plus[u + 1];
@@ -588,7 +667,8 @@ static void build_oriented(gdx_graph* g, TcPlan& P) {
     int32_t* h = reinterpret_cast<int32_t*>(g->pinned);
     GDX_CUDA(cudaMemcpyAsync(h, P.off_plus.get() + n, 4, cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
-    P.adj_plus.ensure(size_t(h[0]) + 8);
+    const int64_t total = h[0];  // oriented entries
+    P.adj_plus.ensure(size_t(total) + 8);
     timed_launch(g, "tc_orient_fill", [&] {
         k_tc_orient_fill<<<grid_v, 256, 0, s>>>(n, g->dests.get(), P.hi_start.get(),
                                                 P.off_plus.get(), P.adj_plus.get());
@@ -602,6 +682,15 @@ static void build_oriented(gdx_graph* g, TcPlan& P) {
     GDX_CUDA(cudaMemcpyAsync(h64, sp.get(), 8, cudaMemcpyDeviceToHost, s));
     GDX_CUDA(cudaStreamSynchronize(s));
     P.survey_pairs = double(h64[0]);
+    if (kTcSig && total > 0) {  // the pair filter's signatures: sig per vertex, sigp per entry
+        DevBuf<unsigned long long> sig{size_t(n)};
+        P.sigp.ensure(size_t(total));
+        timed_launch(g, "tc_sig", [&] {
+            k_tc_sig<<<grid_v, 256, 0, s>>>(n, P.off_plus.get(), P.adj_plus.get(), sig.get());
+            k_tc_sigp<<<blocks_for(total, 256, g->num_sms * 16), 256, 0, s>>>(
+                total, P.adj_plus.get(), sig.get(), P.sigp.get());
+        });
+    }
     P.oriented = true;
 }
 
@@ -617,7 +706,8 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
                                     (cap ? std::max(1, std::atoi(cap)) : 512) * g->num_sms);
         timed_launch(g, "tc", [&] {
             k_tc_oriented<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, P.off_plus.get(),
-                                                    P.adj_plus.get(), P.acc.get());
+                                                    P.adj_plus.get(), P.acc.get(),
+                                                    kTcSig ? P.sigp.get() : nullptr);
         });
     }
     // degree binning: the heavy vertices' pairs over the whole grid
