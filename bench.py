@@ -515,8 +515,10 @@ def bench_tc(torch, gdx, dist, args, pk, cpu_legs: bool) -> dict:
            "plan": {"first_call_ms": round(plan_ms, 2),
                     "orientation_kernels_ms": round(sum(plan_prof.get(k, (0, 0))[0] for k in
                                                         ("tc_orient", "tc_orient_fill")), 3),
-                    "note": "the oriented CSR (off+, adj+) is built by the first call on a "
-                            "handle and cached with it, like the PageRank plan"},
+                    "signature_kernels_ms": round(plan_prof.get("tc_sig", (0, 0))[0], 3),
+                    "note": "the oriented CSR (off+, adj+) and the pair-filter signatures "
+                            "are built by the first call on a handle and cached with it, "
+                            "like the PageRank plan"},
            "gpu_launches": int(sum(v[1] for v in prof.values())),
            "kernels": {k: {"ms": round(v[0], 3), "launches": v[1]} for k, v in prof.items()}}
     res["roofline"]["bytes_formula"] = ("4(n+1) + 4m + 4 * sum over oriented edges u->v of "

@@ -229,22 +229,43 @@ __global__ void k_tc_orient_fill(int32_t n, const int32_t* __restrict__ dests,
 #define GDX_TC_SIG 1
 #endif
 constexpr bool kTcSig = GDX_TC_SIG != 0;
-constexpr int kSigTail = 16;  // longer tails are not filtered (hashing them costs more)
-__device__ __forceinline__ unsigned long long sig_bit(int32_t x) {
-    return 1ull << ((uint32_t(x) * 0x9E3779B1u) >> 26);
+#ifndef GDX_TC_SIGTAIL
+#define GDX_TC_SIGTAIL 16
+#endif
+constexpr int kSigTail = GDX_TC_SIGTAIL;  // longer tails are not filtered (hashing them costs more)
+#ifndef GDX_TC_SIGW
+#define GDX_TC_SIGW 2  // signature words of 64 bits (same-box C3: 3.37 ms at 2, 3.46 at 1)
+#endif
+constexpr int kSigW = GDX_TC_SIGW;
+struct Sig {
+    unsigned long long w[kSigW];
+};
+__device__ __forceinline__ void sig_add(Sig& s, int32_t x) {
+    const uint32_t h = uint32_t(x) * 0x9E3779B1u;
+    if (kSigW == 1) {
+        s.w[0] |= 1ull << (h >> 26);
+    } else {
+#pragma unroll
+        for (int q = 0; q < kSigW; ++q) s.w[q] |= (h >> 31) == uint32_t(q & 1) ? 1ull << ((h >> 25) & 63) : 0ull;
+    }
+}
+__device__ __forceinline__ bool sig_meet(const Sig& a, const Sig& b) {
+    unsigned long long x = 0;
+#pragma unroll
+    for (int q = 0; q < kSigW; ++q) x |= a.w[q] & b.w[q];
+    return x != 0;
 }
 __global__ void k_tc_sig(int32_t n, const int32_t* __restrict__ off_plus,
-                         const int32_t* __restrict__ adj, unsigned long long* __restrict__ sig) {
+                         const int32_t* __restrict__ adj, Sig* __restrict__ sig) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long b = 0;
-        for (int32_t i = off_plus[v], e = off_plus[v + 1]; i < e; ++i) b |= sig_bit(adj[i]);
+        Sig b{};
+        for (int32_t i = off_plus[v], e = off_plus[v + 1]; i < e; ++i) sig_add(b, adj[i]);
         sig[v] = b;
     }
 }
 __global__ void k_tc_sigp(int64_t cnt, const int32_t* __restrict__ adj,
-                          const unsigned long long* __restrict__ sig,
-                          unsigned long long* __restrict__ sigp) {
+                          const Sig* __restrict__ sig, Sig* __restrict__ sigp) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x)
         sigp[i] = sig[adj[i]];
@@ -259,8 +280,7 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
                                                           const int32_t* __restrict__ off_plus,
                                                           const int32_t* __restrict__ adj,
                                                           unsigned long long* acc,
-                                                          const unsigned long long* __restrict__ sigp =
-                                                              nullptr) {
+                                                          const Sig* __restrict__ sigp = nullptr) {
     const unsigned full = 0xffffffffu;
     __shared__ int32_t stage[kTcBlock / 32][kTcStage];
     __shared__ uint16_t s_list[kTcBlock / 32][kTcStage];  // the warp's pairs that pass the filter
@@ -307,9 +327,9 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
                 const int32_t kbeg = __shfl_sync(full, ob, k);
                 bool pass = i0 + lane < rlen && q < kend - 1 && kend - kbeg <= kTcHeavy;
                 if (pass && kend - q - 1 <= kSigTail) {
-                    unsigned long long ts = 0;
-                    for (int32_t x = q + 1; x < kend; ++x) ts |= sig_bit(A[x]);
-                    pass = (ts & sigp[q]) != 0;
+                    Sig ts{};
+                    for (int32_t x = q + 1; x < kend; ++x) sig_add(ts, A[x]);
+                    pass = sig_meet(ts, sigp[q]);
                 }
                 const unsigned m = __ballot_sync(full, pass);
                 if (pass) sL[ntp + __popc(m & ((1u << lane) - 1))] = uint16_t(q - r0);
@@ -683,12 +703,14 @@ static void build_oriented(gdx_graph* g, TcPlan& P) {
     GDX_CUDA(cudaStreamSynchronize(s));
     P.survey_pairs = double(h64[0]);
     if (kTcSig && total > 0) {  // the pair filter's signatures: sig per vertex, sigp per entry
-        DevBuf<unsigned long long> sig{size_t(n)};
-        P.sigp.ensure(size_t(total));
+        DevBuf<unsigned long long> sig{size_t(n) * kSigW};
+        P.sigp.ensure(size_t(total) * kSigW);
         timed_launch(g, "tc_sig", [&] {
-            k_tc_sig<<<grid_v, 256, 0, s>>>(n, P.off_plus.get(), P.adj_plus.get(), sig.get());
+            k_tc_sig<<<grid_v, 256, 0, s>>>(n, P.off_plus.get(), P.adj_plus.get(),
+                                            reinterpret_cast<Sig*>(sig.get()));
             k_tc_sigp<<<blocks_for(total, 256, g->num_sms * 16), 256, 0, s>>>(
-                total, P.adj_plus.get(), sig.get(), P.sigp.get());
+                total, P.adj_plus.get(), reinterpret_cast<const Sig*>(sig.get()),
+                reinterpret_cast<Sig*>(P.sigp.get()));
         });
     }
     P.oriented = true;
@@ -707,7 +729,8 @@ static void run_tc_oriented(gdx_graph* g, int32_t v_begin, int32_t v_end, gdx_st
         timed_launch(g, "tc", [&] {
             k_tc_oriented<<<grid, kTcBlock, 0, s>>>(v_begin, v_end, P.off_plus.get(),
                                                     P.adj_plus.get(), P.acc.get(),
-                                                    kTcSig ? P.sigp.get() : nullptr);
+                                                    kTcSig ? reinterpret_cast<const Sig*>(P.sigp.get())
+                                                           : nullptr);
         });
     }
     // degree binning: the heavy vertices' pairs over the whole grid
