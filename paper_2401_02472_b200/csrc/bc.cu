@@ -521,7 +521,8 @@ __device__ inline void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory
 // stage 2: the item's own record and its recorded children's (slot's log entry ready)
 __device__ inline void bc_pf_records(BcPf* pf, const BcRec* rec) {
     const int4 it = pf->log;
-    if (it.x < 0) {  // (~v, children): see the forward pass
+    if (it.x < 0 && it.y < 0) {  // a leaf: nothing to load (its q is final)
+    } else if (it.x < 0) {  // (~v, children): see the forward pass
         cp16(&pf->own, rec + ~it.x);
         if (it.y >= 0) cp16(&pf->ch[0], rec + it.y);
         if (it.z >= 0) cp16(&pf->ch[1], rec + it.z);
@@ -666,6 +667,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         }
         if (ltid == 0) s_next_local[0] = s_next_local[1] = s_next_local[2] = 0;
         cluster.sync();
+        bool leaf = false;  // the current forward item has no children (recorded lists)
         // one chunk of <= kNb neighbours of item i (level L): parents' sigma,
         // claims (CAS) of undiscovered neighbours, the children list, the claims'
         // log positions (one DSMEM atomic per converged lane group) and entries.
@@ -700,6 +702,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         ++nc;
                     }
                 if (nc <= 3) log[i] = make_int4(~v, c0, c1, c2);
+                leaf = nc == 0;
             }
             // log positions: one DSMEM atomic per group of converged lanes
             // (scan of the claim counts) instead of one per claim
@@ -749,6 +752,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 }
                 XF acc{L == 0 ? 1.0 : 0.0, 0};
                 fscan += oe - ob;
+                leaf = kids && oe == ob;  // fwd_chunk sets it from the children it records
                 for (int32_t e = ob; e < oe; e += kNb) {
                     int32_t w[kNb], lw[kNb];
                     XF sg[kNb];
@@ -785,7 +789,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     }
                 }
                 if (kids && oe == ob) log[i] = make_int4(~v, -1, -1, -1);  // no children
-                rec_store_sigma(rec + v, base + L, acc);
+                // a leaf's sigma has no reader in the forward pass (a reader would
+                // be a child), so its record gets its final q = 1 / sigma now and
+                // the backward pass skips it
+                rec_store_sigma(rec + v, base + L, leaf ? xf_q(0.0, acc) : acc);
             }
             // heavy items of this CTA: one warp each, lanes stride over the adjacency
             // (graphs without a vertex above kHeavy skip the extra barrier)
@@ -828,6 +835,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                     cp_wait();
                     const int4 it = pf->log, ow = pf->own;
                     const bool kf = it.x < 0;  // (~v, children) or (v, out-begin, out-end)
+                    const bool lf = kf && it.y < 0;  // a leaf: final q stored by the forward pass
                     const int32_t v = kf ? ~it.x : it.x, ob = it.y, oe = it.z;
                     const int32_t lv = ow.x;
                     const XF sv{__hiloint2double(ow.w, ow.z), ow.y};
@@ -870,9 +878,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         cp_wait();
                         bc_pf_records(pf, rec);
                     }
-                    const double d = xf_mul_double(sv, sum);  // delta(v)
-                    rec_store_sigma(rec + v, lv, xf_q(d, sv));
-                    if (v != src && d != 0.0) bcs[v] = first_src ? d : bcs[v] + d;
+                    if (!lf) {
+                        const double d = xf_mul_double(sv, sum);  // delta(v)
+                        rec_store_sigma(rec + v, lv, xf_q(d, sv));
+                        if (v != src && d != 0.0) bcs[v] = first_src ? d : bcs[v] + d;
+                    }
                 }
                 cluster.sync();
                 bc_trace(a, slot, tid, tk, b0 - b1);  // negative: backward
@@ -884,6 +894,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
             for (int i = b0 + tid; i < b1; i += kStride) {
                 const int4 it = log[i];
                 const bool kf = kids && it.x < 0;  // (~v, children) or (v, out-begin, out-end)
+                if (kf && it.y < 0) continue;      // a leaf: its q is final (forward pass)
                 const int32_t v = kf ? ~it.x : it.x, ob = it.y, oe = it.z;
                 if (HEAVY && oe - ob > kHeavy) {
                     const int hp = atomicAdd(&s_hn, 1);
