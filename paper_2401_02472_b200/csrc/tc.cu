@@ -249,6 +249,15 @@ __device__ __forceinline__ void sig_add(Sig& s, int32_t x) {
         for (int q = 0; q < kSigW; ++q) s.w[q] |= (h >> 31) == uint32_t(q & 1) ? 1ull << ((h >> 25) & 63) : 0ull;
     }
 }
+// the same bit from its precomputed 7-bit index (h >> 25)
+__device__ __forceinline__ void sig_add_bit(Sig& s, unsigned b) {
+    if (kSigW == 1) {
+        s.w[0] |= 1ull << (b >> 1);
+    } else {
+#pragma unroll
+        for (int q = 0; q < kSigW; ++q) s.w[q] |= (b >> 6) == unsigned(q & 1) ? 1ull << (b & 63) : 0ull;
+    }
+}
 __device__ __forceinline__ bool sig_meet(const Sig& a, const Sig& b) {
     unsigned long long x = 0;
 #pragma unroll
@@ -284,6 +293,7 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
     const unsigned full = 0xffffffffu;
     __shared__ int32_t stage[kTcBlock / 32][kTcStage];
     __shared__ uint16_t s_list[kTcBlock / 32][kTcStage];  // the warp's pairs that pass the filter
+    __shared__ uint8_t s_bit[kTcBlock / 32][kTcStage];    // signature bit of each staged element
     const int lane = threadIdx.x & 31;
     int32_t* sA = stage[threadIdx.x >> 5];
     uint16_t* sL = s_list[threadIdx.x >> 5];
@@ -304,7 +314,11 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
         // stage the warp's lists (one contiguous range of adj+) when they fit
         const bool staged = rlen <= kTcStage;
         if (staged)
-            for (int32_t i = lane; i < rlen; i += 32) sA[i] = adj[r0 + i];
+            for (int32_t i = lane; i < rlen; i += 32) {
+                const int32_t x = adj[r0 + i];
+                sA[i] = x;
+                if (kTcSig && sigp) s_bit[threadIdx.x >> 5][i] = uint8_t((uint32_t(x) * 0x9E3779B1u) >> 25);
+            }
         __syncwarp();
         const int32_t* A = staged ? sA - r0 : adj;  // A[x] for x in [r0, last_end)
         // The pair filter, computed here for every staged entry (its pair is
@@ -328,7 +342,8 @@ __global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32
                 bool pass = i0 + lane < rlen && q < kend - 1 && kend - kbeg <= kTcHeavy;
                 if (pass && kend - q - 1 <= kSigTail) {
                     Sig ts{};
-                    for (int32_t x = q + 1; x < kend; ++x) sig_add(ts, A[x]);
+                    const uint8_t* sb = s_bit[threadIdx.x >> 5] - r0;
+                    for (int32_t x = q + 1; x < kend; ++x) sig_add_bit(ts, sb[x]);
                     pass = sig_meet(ts, sigp[q]);
                 }
                 const unsigned m = __ballot_sync(full, pass);
