@@ -808,10 +808,11 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const char* lv = std::getenv("GDX_SSSP_LPI");
     const int lpi = lv ? std::atoi(lv) : 16;  // lanes per relaxation item
     const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
-    // 16 blocks/SM for small graphs (fewer idle blocks per short round: C1 0.33
-    // vs 0.35 ms), 128 for large ones (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32)
+    // 8 blocks/SM for small graphs -- one resident wave of 256-thread blocks
+    // (same-box C1 0.222 vs 0.227 ms at 16, 0.238 at 4) -- 128 for large ones
+    // (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32)
     const int relax_grid =
-        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 16 : 128)) * g->num_sms;
+        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 8 : 128)) * g->num_sms;
     if (use_graph) {
         const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
         // the instantiated graph bakes in these buffers and the CSR arrays
