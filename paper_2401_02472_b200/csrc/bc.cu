@@ -671,10 +671,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // one chunk of <= kNb neighbours of item i (level L): parents' sigma,
         // claims (CAS) of undiscovered neighbours, the children list, the claims'
         // log positions (one DSMEM atomic per converged lane group) and entries.
-        // mid1 / mid2 run while the CAS / the claim atomic are in flight.
         auto fwd_chunk = [&](int i, int32_t v, int L, int end, int deg, const int32_t (&w)[kNb],
-                             const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc,
-                             auto&& mid1, auto&& mid2) {
+                             const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc) {
             bool par[kNb], got[kNb];
             int32_t w0[kNb], w1[kNb], lnew[kNb];
 #pragma unroll
@@ -686,7 +684,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 lnew[k] = cand ? atomicCAS(&rec[w[k]].level, lw[k], base + L + 1) : lw[k];
                 got[k] = cand && lnew[k] == lw[k];
             }
-            mid1();  // pipelined path: the next item's dests while the CAS are in flight
             if (kids && deg <= kNb) {
                 // the children of v: neighbours claimed at this level, by v or
                 // not (a failed CAS returns the claimer's level) -- the
@@ -718,7 +715,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
 #pragma unroll
                     for (int q = 0; q < CS - 1; ++q) atomicAdd(&s_copy[q][L % 3], tot);
                 }
-                mid2();  // pipelined path: the next item's records while the claim atomic is in flight
                 int pos = end + act.shfl(qb, last) + excl;
 #pragma unroll
                 for (int k = 0; k < kNb; ++k) {
@@ -764,7 +760,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
-                    fwd_chunk(i, v, L, end, oe - ob, w, lw, sg, acc, [] {}, [] {});
+                    fwd_chunk(i, v, L, end, oe - ob, w, lw, sg, acc);
                 }
                 if (!a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
