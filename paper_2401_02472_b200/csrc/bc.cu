@@ -512,20 +512,12 @@ __device__ inline void rec_store_sigma(BcRec* r, int32_t level, XF sig) {
 #define GDX_BC_PIPE 1
 #endif
 constexpr bool kBcPipe = GDX_BC_PIPE != 0;
-#ifndef GDX_BC_PIPEF
-#define GDX_BC_PIPEF 0
-#endif
-constexpr int kBcPipeF = GDX_BC_PIPEF;  // forward stages prefetched (0 = none)
 struct __align__(16) BcPf {
     int4 log, own, ch[3];
 };
 __device__ inline void cp16(void* sdst, const void* gsrc) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ inline void cp4(void* sdst, const void* gsrc) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ inline void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ inline void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -682,11 +674,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         // one chunk of <= kNb neighbours of item i (level L): parents' sigma,
         // claims (CAS) of undiscovered neighbours, the children list, the claims'
         // log positions (one DSMEM atomic per converged lane group) and entries.
-        // mid1 / mid2 (the pipelined forward pass) run while the CAS / the claim
-        // atomic are in flight.
         auto fwd_chunk = [&](int i, int32_t v, int L, int end, int deg, const int32_t (&w)[kNb],
-                             const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc,
-                             auto&& mid1, auto&& mid2) {
+                             const int32_t (&lw)[kNb], const XF (&sg)[kNb], XF& acc) {
             bool par[kNb], got[kNb];
             int32_t w0[kNb], w1[kNb], lnew[kNb];
 #pragma unroll
@@ -698,7 +687,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                 lnew[k] = cand ? atomicCAS(&rec[w[k]].level, lw[k], base + L + 1) : lw[k];
                 got[k] = cand && lnew[k] == lw[k];
             }
-            mid1();
             if (kids && deg <= kNb) {
                 // the children of v: neighbours claimed at this level, by v or
                 // not (a failed CAS returns the claimer's level) -- the
@@ -730,7 +718,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
 #pragma unroll
                     for (int q = 0; q < CS - 1; ++q) atomicAdd(&s_copy[q][L % 3], tot);
                 }
-                mid2();
                 int pos = end + act.shfl(qb, last) + excl;
 #pragma unroll
                 for (int k = 0; k < kNb; ++k) {
@@ -746,110 +733,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
         int beg = 0, end = 1, L = 0;
         for (;; ++L) {
             int deferred = 0;
-            if (!HEAVY && kBcPipeF > 0 && a.undirected && kids) {
-                // Pipelined forward (GDX_BC_PIPEF stages): a thread's next item --
-                // its log entry (1), then its <= kNb dests (2), then its
-                // neighbours' records (3) -- is copied into the thread's
-                // shared-memory slot by cp.async while this item's CAS and claim
-                // atomic are in flight.
-                BcPf* pf = s_pf + ltid;
-                int32_t* pdst = reinterpret_cast<int32_t*>(&pf->own);
-                auto dests_of = [&] {  // stage 2 (the slot's log entry is in)
-                    const int4 it = pf->log;
-                    const int32_t dg = it.z - it.y;
-                    if (kBcPipeF >= 2 && dg <= kNb)
-                        for (int k = 0; k < dg; ++k) cp4(pdst + k, a.dests + it.y + k);
-                    cp_commit();
-                };
-                auto records_of = [&] {  // stage 3 (the slot's dests are in)
-                    const int4 it = pf->log;
-                    const int32_t dg = it.z - it.y;
-                    if (kBcPipeF >= 3 && dg <= 3)
-                        for (int k = 0; k < dg; ++k) cp16(&pf->ch[k], rec + pdst[k]);
-                    cp_commit();
-                };
-                int i = beg + tid;
-                if (i < end) {
-                    cp16(&pf->log, log + i);
-                    cp_commit();
-                    cp_wait();
-                    dests_of();
-                    cp_wait();
-                    records_of();
-                }
-                for (; i < end; i += kStride) {
-                    cp_wait();
-                    const int4 it = pf->log;
-                    const int32_t v = it.x, ob = it.y, oe = it.z, deg = oe - ob;
-                    const int in = i + kStride;
-                    const bool more = in < end;
-                    XF acc{L == 0 ? 1.0 : 0.0, 0};
-                    fscan += deg;
-                    leaf = oe == ob;
-                    int32_t w[kNb], lw[kNb];
-                    XF sg[kNb];
-                    if (deg <= kNb) {
-#pragma unroll
-                        for (int k = 0; k < kNb; ++k)
-                            w[k] = k < deg ? (kBcPipeF >= 2 ? pdst[k] : a.dests[ob + k]) : -1;
-#pragma unroll
-                        for (int k = 0; k < kNb; ++k) {
-                            lw[k] = -2;
-                            sg[k] = XF{0.0, 0};
-                            if (k < deg) {
-                                if (kBcPipeF >= 3 && deg <= 3) {
-                                    const int4 r = pf->ch[k];
-                                    lw[k] = r.x;
-                                    sg[k] = XF{__hiloint2double(r.w, r.z), r.y};
-                                } else {
-                                    rec_level_sigma(rec + w[k], lw[k], sg[k]);
-                                }
-                            }
-                        }
-                        if (more) {  // stage 1 of the next item
-                            cp16(&pf->log, log + in);
-                            cp_commit();
-                        }
-                        fwd_chunk(i, v, L, end, deg, w, lw, sg, acc,
-                                  [&] {
-                                      if (more) {
-                                          cp_wait();
-                                          dests_of();
-                                      }
-                                  },
-                                  [&] {
-                                      if (more) {
-                                          cp_wait();
-                                          records_of();
-                                      }
-                                  });
-                    } else {  // longer lists: chunks from global memory
-                        if (more) {
-                            cp16(&pf->log, log + in);
-                            cp_commit();
-                        }
-                        for (int32_t e = ob; e < oe; e += kNb) {
-#pragma unroll
-                            for (int k = 0; k < kNb; ++k) w[k] = e + k < oe ? a.dests[e + k] : -1;
-#pragma unroll
-                            for (int k = 0; k < kNb; ++k) {
-                                lw[k] = -2;
-                                sg[k] = XF{0.0, 0};
-                                if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
-                            }
-                            fwd_chunk(i, v, L, end, deg, w, lw, sg, acc, [] {}, [] {});
-                        }
-                        if (more) {
-                            cp_wait();
-                            dests_of();
-                            cp_wait();
-                            records_of();
-                        }
-                    }
-                    if (oe == ob) log[i] = make_int4(~v, -1, -1, -1);  // no children
-                    rec_store_sigma(rec + v, base + L, leaf ? xf_q(0.0, acc) : acc);
-                }
-            } else
             for (int i = beg + tid; i < end; i += kStride) {
                 // the log entry carries v's out-edge range (one dependent load fewer)
                 const int4 it = log[i];
@@ -880,7 +763,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kBcCta) k_bc_cta(Bc
                         sg[k] = XF{0.0, 0};
                         if (w[k] >= 0) rec_level_sigma(rec + w[k], lw[k], sg[k]);
                     }
-                    fwd_chunk(i, v, L, end, oe - ob, w, lw, sg, acc, [] {}, [] {});
+                    fwd_chunk(i, v, L, end, oe - ob, w, lw, sg, acc);
                 }
                 if (!a.undirected && L > 0) {
                     const int32_t ib = a.in_offsets[v], ie = a.in_offsets[v + 1];
@@ -1222,7 +1105,7 @@ static void run_bc_cta(gdx_graph* g, const std::vector<int32_t>& hsrc,
             else
                 k_bc_cta<1, true><<<grid, kBcCta, 0, s>>>(a);
         } else {
-            const int dyn = kBcPipe || kBcPipeF > 0 ? int(kBcCta * sizeof(BcPf)) : 0;
+            const int dyn = kBcPipe ? int(kBcCta * sizeof(BcPf)) : 0;
             static bool attr_set = false;
             if (dyn && !attr_set) {
                 GDX_CUDA(cudaFuncSetAttribute(k_bc_cta<4, false>,
