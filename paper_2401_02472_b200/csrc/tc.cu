@@ -285,7 +285,10 @@ __global__ void k_tc_sigp(int64_t cnt, const int32_t* __restrict__ adj,
 #endif
 constexpr int kTcStage = GDX_TC_STAGE;  // ints of staged N+ lists per warp
 
-__global__ void __launch_bounds__(kTcBlock, 1536 / kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
+#ifndef GDX_TC_THREADS_SM
+#define GDX_TC_THREADS_SM 1536  // resident threads per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kTcBlock, GDX_TC_THREADS_SM / kTcBlock) k_tc_oriented(int32_t v_begin, int32_t v_end,
                                                           const int32_t* __restrict__ off_plus,
                                                           const int32_t* __restrict__ adj,
                                                           unsigned long long* acc,
