@@ -4,8 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -234,6 +236,28 @@ inline void timed_launch(gdx_graph* g, const char* name, F&& launch) {
 inline void copy_out(gdx_graph* g, void* dst, const void* src, size_t bytes) {
     if (bytes == 0) return;
     GDX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream));
+}
+
+// Shared-memory carveout (percent of the unified L1 / shared capacity) of a
+// gather kernel that uses no shared memory, so the L1 holding its gathered
+// lines is as large as it gets; GDX_CARVEOUT = percent overrides, -1 leaves
+// the driver's choice.  Set once per kernel and device.
+inline void prefer_l1(const void* fn, int dflt) {
+    static const int env = [] {
+        const char* e = std::getenv("GDX_CARVEOUT");
+        return e ? std::atoi(e) : -2;
+    }();
+    const int pct = env == -2 ? dflt : env;
+    if (pct < 0) return;
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    GDX_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& d : done)
+        if (d.first == fn && d.second == dev) return;
+    GDX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    done.emplace_back(fn, dev);
 }
 
 inline int blocks_for(int64_t items, int threads, int cap) {

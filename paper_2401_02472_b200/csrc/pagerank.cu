@@ -36,6 +36,7 @@
 namespace gdx {
 
 constexpr int kPrBlock = 256;
+constexpr int kPrCarveout = -1;  // pass A's shared-memory carveout (prefer_l1; -1: the driver's)
 constexpr int32_t kFlagRing = 256;  // per-round vote slots (a ring; see clear_flags)
 __host__ __device__ inline int32_t flag_slot(int32_t round) { return round & (kFlagRing - 1); }
 
@@ -308,7 +309,12 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
                                       double* __restrict__ contrib_out, double& dang_local,
                                       int& unsettled) {
     const int64_t vb = R ? a.v_begin : 0, ve = R ? a.v_end : a.n;
-    if (!R && v + 1 < ve) {
+    // a pair inside the range takes the vector path; a shard's contrib slice
+    // is 16 B aligned at the pair only when v_begin is even (peer buffers are
+    // whole-graph arrays, always aligned at an even v)
+    const bool vec = R ? v >= vb && v + 1 < ve && (a.npeers > 0 || (a.v_begin & 1) == 0)
+                       : v + 1 < ve;
+    if (vec) {
         const double2 sum = *reinterpret_cast<const double2*>(a.row_sum + v);
         const double2 ri = *reinterpret_cast<const double2*>(rank_in + v);
         const int32_t o0 = a.offsets[v], o1 = a.offsets[v + 1], o2 = a.offsets[v + 2];
@@ -322,8 +328,16 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
         if ((c0 >= a.threshold || c1 >= a.threshold) && round < a.max_iter) unsettled = 1;
         *reinterpret_cast<double2*>(rank_out + v) = make_double2(nr0, nr1);
         const int32_t d0 = o1 - o0, d1 = o2 - o1;
-        *reinterpret_cast<double2*>(contrib_out + v) =
+        const double2 cc =
             make_double2(d0 > 0 ? nr0 / double(d0) : 0.0, d1 > 0 ? nr1 / double(d1) : 0.0);
+        if (R && a.npeers > 0) {
+            // P2P stores over NVLink; a pair without out-edges is never
+            // gathered, so it is not sent
+            if (d0 > 0 || d1 > 0)
+                for (int q = 0; q < a.npeers; ++q) __stcg(reinterpret_cast<double2*>(a.peers[q] + v), cc);
+        } else {
+            *reinterpret_cast<double2*>(contrib_out + v) = cc;
+        }
         if (d0 == 0) dang_local += nr0;
         if (d1 == 0) dang_local += nr1;
     } else {
@@ -675,6 +689,7 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         const int64_t want = max_iter >= 0 ? int64_t(max_iter) + 1 : 1;
         const int64_t limit = std::min(want, cap);
         PrArgs a = make_args(g, P, damping, threshold, max_iter);
+        prefer_l1(reinterpret_cast<const void*>(&k_pr_edges<false>), kPrCarveout);
 
         GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
         int launches = 0;
@@ -1109,6 +1124,7 @@ extern "C" int gdx_pr_p2p_rounds(gdx_graph* g, int32_t first, int32_t count, dou
                                      cudaMemcpyHostToDevice, s));
         }
         clear_flags(P, first, count, s);
+        prefer_l1(reinterpret_cast<const void*>(&k_pr_edges<true>), kPrCarveout);
         for (int32_t round = first; round < last; ++round) {
             const int64_t j = X.publishes;
             PrArgs a = make_args(g, P, damping, threshold, max_iter);

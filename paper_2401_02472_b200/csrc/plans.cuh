@@ -91,8 +91,9 @@ struct SsspWork {
     // instantiated round loop per distance width
     DevBuf<unsigned long long> msync;
     DevBuf<void*> mpeers;
-    cudaGraphExec_t mexec[2] = {nullptr, nullptr};
-    std::vector<void*> mkey[2];
+    cudaGraphExec_t mexec[3] = {nullptr, nullptr, nullptr};  // u32, u64, u16 distances
+    std::vector<void*> mkey[3];
+    bool multi_narrow_overflowed = false;  // a 16-bit multi-GPU attempt overflowed
     ~SsspWork() {
         for (auto& e : gexec)
             if (e) cudaGraphExecDestroy(e);

@@ -575,23 +575,27 @@ static int frontier_grid(const gdx_graph* g, int64_t cnt, int per = kFPer) {
 }
 
 // The single-GPU round loop's scan: per-thread chunk by graph size.
+// (The partitions of the multi-GPU rounds scan their range [v0, v1) with the
+// variant the whole graph's size selects, so every partition runs the same.)
 template <class D>
-static void launch_scan(const gdx_graph* g, cudaStream_t st, int32_t n, D* dist, D* prev,
-                        int2* queue, unsigned long long* ctr, int2* squeue) {
+static void launch_scan(const gdx_graph* g, cudaStream_t st, int32_t v0, int32_t v1, D* dist,
+                        D* prev, int2* queue, unsigned long long* ctr, int2* squeue) {
+    const int64_t cnt = int64_t(v1) - v0;
+    const bool small = g->n < kSmallScan;
     if (squeue) {
-        if (n < kSmallScan)
+        if (small)
             k_sssp_scan_frontier<D, kFPerSmall, true>
-                <<<frontier_grid<D>(g, n, kFPerSmall), kFBlock, 0, st>>>(
-                    0, n, g->offsets.get(), dist, prev, queue, ctr, squeue);
+                <<<frontier_grid<D>(g, cnt, kFPerSmall), kFBlock, 0, st>>>(
+                    v0, v1, g->offsets.get(), dist, prev, queue, ctr, squeue);
         else
-            k_sssp_scan_frontier<D, kFPer, true><<<frontier_grid<D>(g, n), kFBlock, 0, st>>>(
-                0, n, g->offsets.get(), dist, prev, queue, ctr, squeue);
-    } else if (n < kSmallScan) {
-        k_sssp_scan_frontier<D, kFPerSmall><<<frontier_grid<D>(g, n, kFPerSmall), kFBlock, 0, st>>>(
-            0, n, g->offsets.get(), dist, prev, queue, ctr);
+            k_sssp_scan_frontier<D, kFPer, true><<<frontier_grid<D>(g, cnt), kFBlock, 0, st>>>(
+                v0, v1, g->offsets.get(), dist, prev, queue, ctr, squeue);
+    } else if (small) {
+        k_sssp_scan_frontier<D, kFPerSmall><<<frontier_grid<D>(g, cnt, kFPerSmall), kFBlock, 0, st>>>(
+            v0, v1, g->offsets.get(), dist, prev, queue, ctr);
     } else {
-        k_sssp_scan_frontier<D><<<frontier_grid<D>(g, n), kFBlock, 0, st>>>(
-            0, n, g->offsets.get(), dist, prev, queue, ctr);
+        k_sssp_scan_frontier<D><<<frontier_grid<D>(g, cnt), kFBlock, 0, st>>>(
+            v0, v1, g->offsets.get(), dist, prev, queue, ctr);
     }
 }
 
@@ -660,6 +664,8 @@ __global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict_
     }
     if (upd) warp_count(issued, upd);
 }
+
+constexpr int kRelaxCarveout = -1;  // relaxation's shared-memory carveout (prefer_l1)
 
 // The round's relaxations: the <= 64-edge items (LPI lanes each) and, with the
 // split queue, the small vertices' one items (2 lanes, <= kSmallDeg edges).
@@ -754,7 +760,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
                                            cudaStreamCaptureModeRelaxed));
     const int32_t n = g->n;
     unsigned long long* ctr = w.shard_ctr.get();
-    launch_scan<D>(g, cs, n, dist, prev, w.shard_queue.get(), ctr, squeue);
+    launch_scan<D>(g, cs, 0, n, dist, prev, w.shard_queue.get(), ctr, squeue);
     launch_relax<D>(g, cs, lpi, relax_grid, w.shard_queue.get(), ctr, squeue, dist, ovf,
                     w.upd_slots.get());
     k_sssp_graph_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), h);
@@ -813,6 +819,9 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     // (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32)
     const int relax_grid =
         (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 8 : 128)) * g->num_sms;
+    prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, 16>), kRelaxCarveout);
+    prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, kSmallLpi, false, kSmallDeg>),
+              kRelaxCarveout);
     if (use_graph) {
         const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
         // the instantiated graph bakes in these buffers and the CSR arrays
@@ -836,7 +845,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         GDX_CUDA(cudaMemsetAsync(ctr, 0, 5 * sizeof(unsigned long long), s));
         GDX_CUDA(cudaMemsetAsync(ctr + kSmallCtr, 0, sizeof(unsigned long long), s));
         timed_launch(g, "sssp_frontier", [&] {
-            launch_scan<D>(g, s, n, dist, prev, w.shard_queue.get(), ctr, squeue);
+            launch_scan<D>(g, s, 0, n, dist, prev, w.shard_queue.get(), ctr, squeue);
         });
         GDX_CUDA(cudaMemcpyAsync(h, ctr, (kSmallCtr + 1) * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s));
@@ -1143,9 +1152,10 @@ struct SsspOwners {
     int32_t nd, self;
 };
 
-__global__ void k_multi_arrive(const unsigned long long* items, MultiSync* const* peers, int nd) {
-    if (items) {
-        const unsigned long long v = *items;
+__global__ void k_multi_arrive(const unsigned long long* items, MultiSync* const* peers, int nd,
+                               int split = 0) {
+    if (items) {  // the scan's item count (both queues)
+        const unsigned long long v = items[0] + (split ? items[kSmallCtr] : 0ull);
         for (int q = 0; q < nd; ++q) atomicAdd_system(&peers[q]->cum, v);
     }
     __threadfence_system();
@@ -1180,6 +1190,7 @@ __global__ void k_multi_finish(unsigned long long* ctr, unsigned long long* acc,
     acc[1] += ctr[3];
     acc[2] += ctr[4];
     for (int i = 0; i < 5; ++i) ctr[i] = 0;
+    ctr[kSmallCtr] = 0;
     cudaGraphSetConditional(h, total ? 1u : 0u);
 }
 
@@ -1202,7 +1213,7 @@ __global__ void k_multi_init(int32_t n, int32_t src, D inf, D* dist, D* prev,
 // candidate for u goes to the owner's replica (peer atomicMin) and to the
 // local hint.  Hints never drop below the owner's value, so the filter
 // c < dist[u] (local) never drops a candidate the owner needs.
-template <class D, int LPI>
+template <class D, int LPI, int CH = kShardChunk>
 __global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict__ queue,
                                                           const unsigned long long* __restrict__ ctr,
                                                           const int32_t* __restrict__ offsets,
@@ -1211,14 +1222,15 @@ __global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict
                                                           D* dist, unsigned long long* ovf,
                                                           unsigned long long* upd, SsspOwners own) {
     const int sub = threadIdx.x & (LPI - 1);
-    constexpr int kU = kShardChunk / LPI;
+    constexpr int kU = CH / LPI;
+    static_assert(CH % LPI == 0, "an item's edges split evenly over its lanes");
     unsigned int issued = 0;
     const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
         const int2 it = queue[i];
         const D dv = dist[it.x];
-        const int32_t e1 = int32_t(min(int64_t(it.y) + kShardChunk, int64_t(offsets[it.x + 1])));
+        const int32_t e1 = int32_t(min(int64_t(it.y) + CH, int64_t(offsets[it.x + 1])));
         int32_t u[kU];
         D c[kU], du[kU];
 #pragma unroll
@@ -1227,7 +1239,8 @@ __global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict
             u[k] = e < e1 ? dests[e] : -1;
             const D w = e < e1 ? (weights ? D(weights[e]) : D(1)) : D(0);
             c[k] = dv + w;
-            if (sizeof(D) == 4 && u[k] >= 0 && dv > std::numeric_limits<D>::max() - D(1) - w) {
+            if (sizeof(D) < 8 && u[k] >= 0 &&
+                uint64_t(dv) + uint64_t(w) >= uint64_t(std::numeric_limits<D>::max())) {
                 *ovf = 1;
                 u[k] = -1;
             }
@@ -1240,8 +1253,8 @@ __global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict
                 ++issued;
                 int q = 0;
                 while (q + 1 < own.nd && u[k] >= own.bound[q + 1]) ++q;
-                if (q != own.self) atomicMin(static_cast<D*>(own.dist[q]) + u[k], c[k]);
-                atomicMin(&dist[u[k]], c[k]);
+                if (q != own.self) dist_atomic_min(static_cast<D*>(own.dist[q]) + u[k], c[k]);
+                dist_atomic_min(&dist[u[k]], c[k]);
             }
     }
     warp_count(issued, upd);
@@ -1250,7 +1263,7 @@ __global__ void __launch_bounds__(256) k_sssp_multi_relax(const int2* __restrict
 template <class D>
 static cudaGraphExec_t build_multi_graph(gdx_graph* g, D* dist, D* prev, int32_t v0, int32_t v1,
                                          MultiSync* me, MultiSync* const* peers, int nd,
-                                         const SsspOwners& own, int relax_grid) {
+                                         const SsspOwners& own, int relax_grid, int2* squeue) {
     auto& w = *g->sssp;
     cudaGraph_t graph;
     GDX_CUDA(cudaGraphCreate(&graph, 0));
@@ -1269,13 +1282,17 @@ static cudaGraphExec_t build_multi_graph(gdx_graph* g, D* dist, D* prev, int32_t
     GDX_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
     unsigned long long* ctr = w.shard_ctr.get();
-    k_sssp_scan_frontier<D><<<frontier_grid<D>(g, int64_t(v1) - v0), kFBlock, 0, cs>>>(
-        v0, v1, g->offsets.get(), dist, prev, w.shard_queue.get(), ctr);
-    k_multi_arrive<<<1, 1, 0, cs>>>(ctr, peers, nd);
+    launch_scan<D>(g, cs, v0, v1, dist, prev, w.shard_queue.get(), ctr, squeue);
+    k_multi_arrive<<<1, 1, 0, cs>>>(ctr, peers, nd, squeue ? 1 : 0);
     k_multi_wait<<<1, 1, 0, cs>>>(me, nd, 1);
+    const int32_t* wts = g->weighted ? g->weights.get() : nullptr;
     k_sssp_multi_relax<D, 16><<<relax_grid, 256, 0, cs>>>(
-        w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(),
-        g->weighted ? g->weights.get() : nullptr, dist, w.graph_acc.get() + 3, w.upd_slots.get(), own);
+        w.shard_queue.get(), ctr, g->offsets.get(), g->dests.get(), wts, dist,
+        w.graph_acc.get() + 3, w.upd_slots.get(), own);
+    if (squeue)  // the small vertices' one items, 2 lanes each (as launch_relax)
+        k_sssp_multi_relax<D, kSmallLpi, kSmallDeg><<<relax_grid, 256, 0, cs>>>(
+            squeue, ctr + kSmallCtr, g->offsets.get(), g->dests.get(), wts, dist,
+            w.graph_acc.get() + 3, w.upd_slots.get(), own);
     k_multi_arrive<<<1, 1, 0, cs>>>(nullptr, peers, nd);
     k_multi_wait<<<1, 1, 0, cs>>>(me, nd, 0);
     k_multi_finish<<<1, 1, 0, cs>>>(ctr, w.graph_acc.get(), me, h);
@@ -1314,6 +1331,20 @@ __global__ void k_multi_gather(int32_t n, SsspOwners own, D inf, int64_t* __rest
     }
 }
 
+// The partitions' round loop follows gdx_sssp's choices from the whole
+// graph's size, so every partition (and every rank) decides alike: the small
+// vertices' queue on graphs of >= 2^22 vertices (GDX_SSSP_SPLIT overrides),
+// and 16-bit distances first there (GDX_SSSP_NARROW overrides) unless a 16-bit
+// multi-GPU attempt on the handle already overflowed.
+static bool multi_split(const gdx_graph* g) {
+    const char* e = std::getenv("GDX_SSSP_SPLIT");
+    return e ? std::atoi(e) != 0 : g->n >= kSmallScan;
+}
+static bool multi_narrow(const gdx_graph* g) {
+    const char* e = std::getenv("GDX_SSSP_NARROW");
+    return e ? std::atoi(e) > 0 : g->n >= (1 << 22) && !g->sssp->multi_narrow_overflowed;
+}
+
 // With lazy module loading (the CUDA 12 default) a kernel's first launch
 // loads its module, which waits for the work running on the device: a
 // partition whose first launch comes while another partition of the same GPU
@@ -1325,7 +1356,11 @@ static void preload_multi_kernels() {
     const void* fns[] = {
         reinterpret_cast<const void*>(&k_multi_init<D>),
         reinterpret_cast<const void*>(&k_sssp_scan_frontier<D>),
+        reinterpret_cast<const void*>(&k_sssp_scan_frontier<D, kFPerSmall>),
+        reinterpret_cast<const void*>(&k_sssp_scan_frontier<D, kFPer, true>),
+        reinterpret_cast<const void*>(&k_sssp_scan_frontier<D, kFPerSmall, true>),
         reinterpret_cast<const void*>(&k_sssp_multi_relax<D, 16>),
+        reinterpret_cast<const void*>(&k_sssp_multi_relax<D, kSmallLpi, kSmallDeg>),
         reinterpret_cast<const void*>(&k_sssp_widen<D>),
         reinterpret_cast<const void*>(&k_multi_gather<D>),
         reinterpret_cast<const void*>(&k_multi_arrive),
@@ -1356,8 +1391,9 @@ static void multi_prepare(MultiPart& p, SsspOwners own, int nd, int self) {
     GraphScope sc(g);
     preload_multi_kernels<D>();
     auto& w = *g->sssp;
-    const int di = sizeof(D) == 4 ? 0 : 1;
+    const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
     own.self = self;
+    int2* squeue = multi_split(g) ? w.small_queue.get() : nullptr;
     D* dist = static_cast<D*>(p.dist);
     D* prev = reinterpret_cast<D*>(w.prev.get());
     const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
@@ -1368,12 +1404,12 @@ static void multi_prepare(MultiPart& p, SsspOwners own, int nd, int self) {
                               g->offsets.get(), g->dests.get(),
                               g->weighted ? g->weights.get() : nullptr,
                               reinterpret_cast<void*>(intptr_t(p.v0)),
-                              reinterpret_cast<void*>(intptr_t(p.v1))};
+                              reinterpret_cast<void*>(intptr_t(p.v1)), squeue};
     for (int q = 0; q < nd; ++q) key.push_back(own.dist[q]);
     if (!w.mexec[di] || w.mkey[di] != key) {
         if (w.mexec[di]) cudaGraphExecDestroy(w.mexec[di]);
         w.mexec[di] = build_multi_graph<D>(g, dist, prev, p.v0, p.v1, p.me, p.peers, nd, own,
-                                           relax_grid);
+                                           relax_grid, squeue);
         w.mkey[di] = key;
     }
 }
@@ -1390,15 +1426,15 @@ static void multi_enqueue(MultiPart& p, SsspOwners own, int nd, int32_t src, boo
     GraphScope sc(g);
     auto& w = *g->sssp;
     cudaStream_t s = g->stream;
-    const int di = sizeof(D) == 4 ? 0 : 1;
-    const D inf = sizeof(D) == 4 ? D(0xFFFFFFFFu) : D(INT64_MAX / 2);
+    const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
+    const D inf = sizeof(D) < 8 ? std::numeric_limits<D>::max() : D(INT64_MAX / 2);
     const int32_t n = g->n;
     D* dist = static_cast<D*>(p.dist);
     D* prev = reinterpret_cast<D*>(w.prev.get());
     k_multi_reset<<<1, 1, 0, s>>>(p.me);
     timed_launch(g, "sssp_multi_init", [&] {
         k_multi_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-            n, src, inf, dist, prev, w.shard_ctr.get(), kUpdSlot + 1, w.graph_acc.get(), 4,
+            n, src, inf, dist, prev, w.shard_ctr.get(), kSmallCtr + 1, w.graph_acc.get(), 4,
             w.upd_slots.get());
     });
     k_multi_arrive<<<1, 1, 0, s>>>(nullptr, p.peers, nd);
@@ -1452,10 +1488,10 @@ static void multi_collect(MultiPart& p, MultiResult& r) {
     r.upd += h[4];
 }
 
-static void multi_stats(const MultiResult& r, int nd, gdx_stats* stats) {
+static void multi_stats(const MultiResult& r, int nd, gdx_stats* stats, bool split) {
     if (!stats) return;
     stats->rounds = int32_t(r.rounds);
-    stats->launches = int32_t(nd * (8 + 6 * (r.rounds + 1)));
+    stats->launches = int32_t(nd * (8 + (split ? 7 : 6) * (r.rounds + 1)));
     stats->vertices_visited = int64_t(r.vvis);
     stats->edges_visited = int64_t(r.evis);
     stats->updates = int64_t(r.upd);
@@ -1474,7 +1510,8 @@ static void multi_workspace(gdx_graph* g, int32_t v0, int32_t v1) {
         GDX_CUDA(cudaMemcpy(&off[1], g->offsets.get() + v1, 4, cudaMemcpyDeviceToHost));
     }
     w.shard_queue.ensure(size_t(v1 - v0) + size_t(int64_t(off[1]) - off[0]) / kShardChunk + 1);
-    w.shard_ctr.ensure(kUpdSlot + 1);
+    if (multi_split(g)) w.small_queue.ensure(size_t(std::max(v1 - v0, 1)));
+    w.shard_ctr.ensure(kSmallCtr + 1);
     w.upd_slots.ensure(kUpdSlots);
     w.graph_acc.ensure(4);
     w.queue[1].ensure(size_t(std::max(v1 - v0, 1)));
@@ -1521,10 +1558,18 @@ void sssp_multi(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& b
                              reinterpret_cast<int64_t*>(gs[d]->sssp->queue[1].get()));
         MultiResult r;
         for (int d = 0; d < nd; ++d) multi_collect(parts[d], r);
-        if (!r.overflow) multi_stats(r, nd, stats);
+        if (!r.overflow) multi_stats(r, nd, stats, multi_split(gs[0]));
         return r.overflow;
     };
-    if (width((unsigned int)0) && width((unsigned long long)0))
+    // widths as gdx_sssp: 16-bit first on large graphs, then 32, then 64 (every
+    // partition takes the same decision: the overflow vote is global)
+    bool ovf = true;
+    if (multi_narrow(gs[0])) {
+        ovf = width((unsigned short)0);
+        if (ovf)
+            for (auto* g : gs) g->sssp->multi_narrow_overflowed = true;
+    }
+    if (ovf && width((unsigned int)0) && width((unsigned long long)0))
         fail(GDX_ERR_RUNTIME, "RuntimeError: distances overflow 64 bits");
     for (int d = 0; d < nd; ++d) {
         gdx_graph* g = gs[d];
@@ -1632,10 +1677,15 @@ extern "C" int gdx_sssp_p2p_run(gdx_graph* g, int32_t src, int64_t* dist_out, gd
             multi_enqueue<D>(part, own, nd, src, true, target);
             MultiResult r;
             multi_collect(part, r);
-            if (!r.overflow) multi_stats(r, 1, stats);
+            if (!r.overflow) multi_stats(r, 1, stats, multi_split(g));
             return r.overflow;
         };
-        if (width((unsigned int)0) && width((unsigned long long)0))
+        bool ovf = true;
+        if (multi_narrow(g)) {  // every rank takes the same decision (global overflow vote)
+            ovf = width((unsigned short)0);
+            if (ovf) w.multi_narrow_overflowed = true;
+        }
+        if (ovf && width((unsigned int)0) && width((unsigned long long)0))
             fail(GDX_ERR_RUNTIME, "RuntimeError: distances overflow 64 bits");
         if (!dev_out) copy_out(g, dist_out, target, size_t(g->n) * sizeof(int64_t));
         GDX_CUDA(cudaStreamSynchronize(g->stream));

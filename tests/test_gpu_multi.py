@@ -89,3 +89,31 @@ def test_multi_errors(gdx, port, graphs):
     assert e.value.kind == "NonTermination"
     _, it = two.pagerank(0.85, -1.0, 50)
     assert it == 51
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0, 0]])
+def test_multi_sssp_narrow_split(gdx, port, graphs, devices, monkeypatch):
+    """The partitioned rounds with gdx_sssp's large-graph choices forced on a
+    small graph: 16-bit distances first and the small vertices' second queue
+    (GDX_SSSP_NARROW=1, GDX_SSSP_SPLIT=1).  A path whose far end lies beyond
+    2^16 overflows the 16-bit attempt and reruns at 32 bits on every
+    partition."""
+    monkeypatch.setenv("GDX_SSSP_NARROW", "1")
+    monkeypatch.setenv("GDX_SSSP_SPLIT", "1")
+    und, _ = graphs
+    ctx = gdx.Context(devices)
+    mu = gdx.MultiGraph(ctx, und)
+    for src in (0, 17, und.n - 1):
+        assert np.array_equal(mu.sssp(src), port.sssp(und, src)), src
+    n = 3000
+    u = np.arange(n - 1, dtype=np.int32)
+    w = np.full(n - 1, 100, np.int32)  # far end 299,900 away
+    g = port.build_from_edges(n, u, u + 1, w, False)
+    mg = gdx.MultiGraph(ctx, g)
+    ref = port.sssp(g, 0)
+    assert ref.max() > 1 << 16
+    assert np.array_equal(mg.sssp(0), ref)
+    assert np.array_equal(mg.sssp(0), ref)  # the handle remembers the overflow
+    mu.close()
+    mg.close()
+    ctx.close()
