@@ -15,6 +15,7 @@ thread_local std::string g_last_error;
 
 gdx_graph::~gdx_graph() {
     // Plans hold device buffers; release them before the stream goes away.
+    relabel.reset();
     pr_p2p.reset();
     sssp_p2p.reset();
     pr.reset();
@@ -334,6 +335,7 @@ static void check_symmetric(gdx_graph* g) {
 // Computes max_weight (SSSP chooses 32- or 64-bit distances from it) and
 // rejects negative weights (csr.cpp:36-39 NegativeWeight).
 void finalize_graph(gdx_graph* g) {
+    g->relabel.reset();  // the renumbered copy holds the old weights
     g->max_weight = 1;
     if (g->weighted && g->m > 0) {
         DevBuf<int32_t> tmp(2);

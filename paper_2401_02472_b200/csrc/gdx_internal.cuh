@@ -164,6 +164,7 @@ struct SsspWork;
 struct SsspP2P;
 struct TcPlan;
 struct BcWork;
+struct Relabel;
 
 }  // namespace gdx
 
@@ -199,6 +200,7 @@ struct gdx_graph {
     std::unique_ptr<gdx::SsspP2P> sssp_p2p;  // gdx_sssp_p2p_* (peer-memory partitions)
     std::unique_ptr<gdx::TcPlan> tc;
     std::unique_ptr<gdx::BcWork> bc;
+    std::unique_ptr<gdx::Relabel> relabel;  // degree-ordered renumbering (relabel.cu)
 
     // scratch for small device->host reads
     int64_t* pinned = nullptr;  // 4 KB pinned host scratch
@@ -269,6 +271,13 @@ inline int blocks_for(int64_t items, int threads, int cap) {
 // Max out-degree (and in-degree for directed graphs), computed once per handle
 // (api.cu); the kernels pick hub-aware or latency-oriented variants from it.
 int32_t graph_max_degree(gdx_graph* g);
+
+// relabel.cu: the degree-ordered renumbering cached on a handle
+bool relabel_wanted(gdx_graph* g);
+Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev);
+void relabel_leave(gdx_graph* g);  // the hidden graph's profile records to g
+void relabel_unpermute_f64(gdx_graph* g, const double* in, double* out);
+int32_t relabel_vertex(gdx_graph* g, int32_t v);  // newid[v] (host read)
 
 // Builds the reverse CSR (csr.cpp:77-94 semantics) on the device.
 void build_reverse_device(gdx_graph* g);

@@ -668,6 +668,80 @@ __global__ void k_pr_shard_partials(const double* dangling, const int32_t* flags
 
 using namespace gdx;
 
+// The fixedPoint rounds on g; returns the device rank vector of the last
+// round (the plan's buffer) and the round count.
+static const double* pagerank_run(gdx_graph* g, double damping, double threshold,
+                                  int32_t max_iter, int32_t* rounds_out, gdx_stats* stats) {
+    cudaStream_t s = g->stream;
+    if (!g->pr) {
+        g->pr = std::make_unique<PrPlan>();
+        build_plan(g);
+    }
+    auto& P = *g->pr;
+    // fixedPoint rounds: at most max_iter+1 (pr.sp:25) and at most the
+    // interpreter's cap 10n+100 (interpreter.cpp:977-986).
+    const int64_t cap = 10 * int64_t(g->n) + 100;
+    const int64_t want = max_iter >= 0 ? int64_t(max_iter) + 1 : 1;
+    const int64_t limit = std::min(want, cap);
+    PrArgs a = make_args(g, P, damping, threshold, max_iter);
+    prefer_l1(reinterpret_cast<const void*>(&k_pr_edges<false>), kPrCarveout);
+
+    GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
+    int launches = 0;
+    timed_launch(g, "pr_init", [&] {
+        k_pr_init<<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0, s>>>(a);
+    });
+    ++launches;
+    int32_t* hflags = reinterpret_cast<int32_t*>(g->pinned);
+    int64_t r = 0, rounds = -1, batch = 4;
+    while (rounds < 0) {
+        const int64_t lim = std::min(r + batch, limit);
+        clear_flags(P, r, lim - r, s);
+        for (int64_t rr = r; rr < lim; ++rr) {
+            if (P.ngroups > 0)
+                timed_launch(g, "pr_edges", [&] {
+                    k_pr_edges<false><<<P.grid, P.block, 0, s>>>(a, int(rr));
+                });
+            launches += launch_cross(g, P, a, int(rr));
+            timed_launch(g, "pr_vertices", [&] {
+                k_pr_vertices<false><<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock,
+                                       0, s>>>(a, int(rr));
+            });
+            launches += 1 + (P.ngroups > 0);
+        }
+        const int64_t cnt = lim - r;
+        GDX_CUDA(cudaMemcpyAsync(hflags, P.flags.get(), kFlagRing * 4, cudaMemcpyDeviceToHost, s));
+        GDX_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < cnt; ++i)
+            if (hflags[flag_slot(int32_t(r + i))] == 0) {
+                rounds = r + i + 1;
+                break;
+            }
+        if (rounds < 0 && lim >= limit) {
+            if (limit < want)
+                fail(GDX_ERR_NON_TERMINATION, "NonTermination: fixedPoint exceeded " +
+                                                  std::to_string(cap) +
+                                                  " iterations without converging");
+            rounds = limit;  // unreachable: round max_iter never votes
+        }
+        r = lim;
+        batch = std::min<int64_t>(batch * 2, 32);
+    }
+    if (rounds_out) *rounds_out = int32_t(rounds);
+    if (stats) {
+        stats->rounds = int32_t(rounds);
+        stats->launches = launches;
+        stats->vertices_visited = int64_t(g->n) * rounds;
+        stats->edges_visited = int64_t(g->m) * rounds;
+        stats->updates = 0;
+        // SURVEY.md 8(d), per round 12 m + 24 n: rev_srcs 4m + contrib
+        // gather 8m; rev_offsets 4n + rank read 8n + new rank / contrib
+        // write 8n + out-degree 4n.
+        stats->algorithmic_bytes = double(rounds) * (12.0 * g->m + 24.0 * g->n);
+    }
+    return P.rank[rounds & 1].get();
+}
+
 extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int32_t max_iter,
                             double* rank_out, int32_t* rounds_out, gdx_stats* stats) {
     return guard_impl([&] {
@@ -677,75 +751,27 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
         if (!g->in_offsets() || !g->in_srcs())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
         GraphScope dg(g);
-        cudaStream_t s = g->stream;
-        if (!g->pr) {
-            g->pr = std::make_unique<PrPlan>();
-            build_plan(g);
+        const size_t bytes = size_t(g->n) * sizeof(double);
+        if (relabel_wanted(g)) {
+            // the rounds on the degree-ordered renumbering (relabel.cu), the
+            // ranks mapped back: rank_out[v] = rank'[newid[v]]
+            Relabel& R = relabel_ensure(g, false, true);
+            const double* r = pagerank_run(R.h, damping, threshold, max_iter, rounds_out, stats);
+            relabel_leave(g);
+            cudaPointerAttributes pa;
+            const bool dev_out = cudaPointerGetAttributes(&pa, rank_out) == cudaSuccess &&
+                                 pa.type == cudaMemoryTypeDevice;
+            cudaGetLastError();
+            if (!dev_out) R.staging.ensure(size_t(g->n));
+            double* tgt = dev_out ? rank_out : R.staging.get();
+            timed_launch(g, "pr_unpermute", [&] { relabel_unpermute_f64(g, r, tgt); });
+            if (!dev_out) copy_out(g, rank_out, tgt, bytes);
+            if (stats) stats->launches += 1;
+        } else {
+            copy_out(g, rank_out, pagerank_run(g, damping, threshold, max_iter, rounds_out, stats),
+                     bytes);
         }
-        auto& P = *g->pr;
-        // fixedPoint rounds: at most max_iter+1 (pr.sp:25) and at most the
-        // interpreter's cap 10n+100 (interpreter.cpp:977-986).
-        const int64_t cap = 10 * int64_t(g->n) + 100;
-        const int64_t want = max_iter >= 0 ? int64_t(max_iter) + 1 : 1;
-        const int64_t limit = std::min(want, cap);
-        PrArgs a = make_args(g, P, damping, threshold, max_iter);
-        prefer_l1(reinterpret_cast<const void*>(&k_pr_edges<false>), kPrCarveout);
-
-        GDX_CUDA(cudaMemsetAsync(P.dangling.get(), 0, 3 * sizeof(double), s));
-        int launches = 0;
-        timed_launch(g, "pr_init", [&] {
-            k_pr_init<<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock, 0, s>>>(a);
-        });
-        ++launches;
-        int32_t* hflags = reinterpret_cast<int32_t*>(g->pinned);
-        int64_t r = 0, rounds = -1, batch = 4;
-        while (rounds < 0) {
-            const int64_t lim = std::min(r + batch, limit);
-            clear_flags(P, r, lim - r, s);
-            for (int64_t rr = r; rr < lim; ++rr) {
-                if (P.ngroups > 0)
-                    timed_launch(g, "pr_edges", [&] {
-                        k_pr_edges<false><<<P.grid, P.block, 0, s>>>(a, int(rr));
-                    });
-                launches += launch_cross(g, P, a, int(rr));
-                timed_launch(g, "pr_vertices", [&] {
-                    k_pr_vertices<false><<<blocks_for(g->n, kPrBlock, g->num_sms * 8), kPrBlock,
-                                           0, s>>>(a, int(rr));
-                });
-                launches += 1 + (P.ngroups > 0);
-            }
-            const int64_t cnt = lim - r;
-            GDX_CUDA(cudaMemcpyAsync(hflags, P.flags.get(), kFlagRing * 4, cudaMemcpyDeviceToHost, s));
-            GDX_CUDA(cudaStreamSynchronize(s));
-            for (int64_t i = 0; i < cnt; ++i)
-                if (hflags[flag_slot(int32_t(r + i))] == 0) {
-                    rounds = r + i + 1;
-                    break;
-                }
-            if (rounds < 0 && lim >= limit) {
-                if (limit < want)
-                    fail(GDX_ERR_NON_TERMINATION, "NonTermination: fixedPoint exceeded " +
-                                                      std::to_string(cap) +
-                                                      " iterations without converging");
-                rounds = limit;  // unreachable: round max_iter never votes
-            }
-            r = lim;
-            batch = std::min<int64_t>(batch * 2, 32);
-        }
-        copy_out(g, rank_out, P.rank[rounds & 1].get(), size_t(g->n) * sizeof(double));
-        GDX_CUDA(cudaStreamSynchronize(s));
-        if (rounds_out) *rounds_out = int32_t(rounds);
-        if (stats) {
-            stats->rounds = int32_t(rounds);
-            stats->launches = launches;
-            stats->vertices_visited = int64_t(g->n) * rounds;
-            stats->edges_visited = int64_t(g->m) * rounds;
-            stats->updates = 0;
-            // SURVEY.md 8(d), per round 12 m + 24 n: rev_srcs 4m + contrib
-            // gather 8m; rev_offsets 4n + rank read 8n + new rank / contrib
-            // write 8n + out-degree 4n.
-            stats->algorithmic_bytes = double(rounds) * (12.0 * g->m + 24.0 * g->n);
-        }
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
     });
 }
 

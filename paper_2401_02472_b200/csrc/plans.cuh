@@ -35,6 +35,20 @@ struct PrPlan {
     int block = 256;
 };
 
+// Degree-ordered renumbering of a graph (relabel.cu): the renumbered graph as
+// a hidden handle on the owner's stream, and the permutation both ways.
+struct Relabel {
+    gdx_graph* h = nullptr;    // owned
+    DevBuf<int32_t> newid;     // old id -> new id
+    DevBuf<int32_t> order;     // new id -> old id
+    bool fwd_off = false, fwd_adj = false, rev = false;  // arrays of h built so far
+    DevBuf<double> staging;    // a call's output in the old numbering (host outputs)
+    Relabel() = default;
+    Relabel(const Relabel&) = delete;
+    Relabel& operator=(const Relabel&) = delete;
+    ~Relabel();
+};
+
 // Peer-memory exchange state of the sharded PageRank (pagerank.cu gdx_pr_p2p_*).
 struct PrP2P {
     int32_t world = 0, rank = 0;
@@ -85,6 +99,7 @@ struct SsspWork {
     cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};  // u32, u64, u16 distances
     void* gkey[3][kKey] = {};
     bool narrow_overflowed = false;  // a 16-bit attempt on this handle overflowed
+    const int32_t* out_perm = nullptr;  // renumbered graph (relabel.cu): out[v] = dist[out_perm[v]]
     DevBuf<unsigned long long> graph_acc;  // [rounds, vertices, edges, overflow]
     DevBuf<unsigned long long> upd_slots;  // U counter slots (sssp.cu block_count)
     // in-process multi-GPU rounds (gdx_sssp_multi): barrier state and the

@@ -287,11 +287,13 @@ __device__ inline void sum_slots(const unsigned long long* slots, unsigned long 
 template <class D>
 __global__ void k_sssp_widen(int32_t n, const D* __restrict__ dist, D inf, int64_t* __restrict__ out,
                              const unsigned long long* slots = nullptr,
-                             unsigned long long* slots_sum = nullptr) {
+                             unsigned long long* slots_sum = nullptr,
+                             const int32_t* __restrict__ perm = nullptr) {
     if (slots && blockIdx.x == 0 && threadIdx.x < 32) sum_slots(slots, slots_sum);
+    // perm: the distances of a renumbered graph, written in the caller's ids
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        D d = dist[i];
+        D d = dist[perm ? perm[i] : i];
         out[i] = d == inf ? (INT64_MAX / 2) : int64_t(d);
     }
 }
@@ -868,7 +870,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     int64_t* target = dev_out ? dist_out : reinterpret_cast<int64_t*>(w.queue[1].get());
     timed_launch(g, "sssp_widen", [&] {
         k_sssp_widen<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-            n, dist, inf, target, w.upd_slots.get(), ctr + kUpdSlot);
+            n, dist, inf, target, w.upd_slots.get(), ctr + kUpdSlot, w.out_perm);
     });
     if (!dev_out) copy_out(g, dist_out, target, size_t(n) * sizeof(int64_t));
     // one host read per call: the graph path's counters and the overflow flag
@@ -1052,6 +1054,62 @@ extern "C" int gdx_sssp_shard_apply32(gdx_graph* g, int32_t* dist, const int32_t
     });
 }
 
+// The call on g (validated; the caller's GraphScope is active).
+static void sssp_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
+    if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
+    auto& w = *g->sssp;
+    // every vertex enters a round's queue at most once: <= n + m/kChunk
+    // items; warp overflow chunks at most double that, plus the padding of
+    // the last chunk of every warp
+    const size_t qcap = 2 * (size_t(g->n) + size_t(g->m) / kChunk + 1) +
+                        size_t(kWarpChunk) * 64 * size_t(g->num_sms);
+    w.dist.ensure(size_t(g->n));
+    // 32-bit distances unless a relaxation overflows them (then 64-bit):
+    // the result is exact either way.  Large graphs use frontier-scan
+    // rounds (bandwidth-bound), small ones the persistent kernel
+    // (latency-bound); GDX_SSSP_MODE=scan|persistent overrides.
+    // Default: frontier-scan rounds driven on the device by a CUDA graph
+    // with a conditional WHILE node (C1: 0.36 ms vs 0.44 ms for the
+    // persistent kernel and 0.56 ms with a host round trip per round).
+    // GDX_SSSP_MODE=persistent|scan|graph selects one for A/B runs.
+    // Low-degree graphs (max degree <= 64: road-like, high diameter, thousands
+    // of small rounds) take the persistent kernel instead: its queue touches
+    // only the frontier while a scan reads all n per round (2000^2 grid:
+    // 27 ms vs 76 ms).
+    const char* mode = std::getenv("GDX_SSSP_MODE");
+    const std::string md = mode ? mode : graph_max_degree(g) <= 64 ? "persistent" : "graph";
+    const bool graph = md == "graph";
+    const bool scan = md == "scan" || graph;
+    if (scan) {
+        w.prev.ensure(size_t(g->n));
+        // widths: 16-bit first on large graphs (half the footprint of the
+        // gathered distance array in L2; GDX_SSSP_NARROW=0/1 overrides),
+        // unless a 16-bit attempt on this handle already overflowed; then
+        // 32-bit, then 64-bit -- each rerun exact
+        const char* ne = std::getenv("GDX_SSSP_NARROW");
+        const int narrow_env = ne ? std::atoi(ne) : -1;
+        const bool narrow = narrow_env >= 0 ? narrow_env > 0
+                                            : (g->n >= (1 << 22) && !w.narrow_overflowed);
+        bool ovf = true;
+        if (narrow) {
+            ovf = run_sssp_scan<unsigned short>(g, src, dist_out, stats, graph);
+            if (ovf) w.narrow_overflowed = true;
+        }
+        if (ovf && run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
+            run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph);
+    } else {
+        // the persistent kernel's queues exist only in this mode (C5 in the
+        // default graph mode would otherwise hold 2 x ~2 GB of unused items);
+        // queue[1] doubles as the int64 staging buffer for host outputs
+        w.stamp.ensure(size_t(g->n));
+        w.queue[0].ensure(qcap);
+        w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
+        w.ctrs.ensure(kCtrs);
+        const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
+        if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
+    }
+}
+
 extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats) {
     return guard_impl([&] {
         if (!g || !dist_out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
@@ -1062,57 +1120,20 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
         if (!g->dests.get() && g->m > 0)
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
         GraphScope dg(g);
-        if (!g->sssp) g->sssp = std::make_unique<SsspWork>();
-        auto& w = *g->sssp;
-        // every vertex enters a round's queue at most once: <= n + m/kChunk
-        // items; warp overflow chunks at most double that, plus the padding of
-        // the last chunk of every warp
-        const size_t qcap = 2 * (size_t(g->n) + size_t(g->m) / kChunk + 1) +
-                            size_t(kWarpChunk) * 64 * size_t(g->num_sms);
-        w.dist.ensure(size_t(g->n));
-        // 32-bit distances unless a relaxation overflows them (then 64-bit):
-        // the result is exact either way.  Large graphs use frontier-scan
-        // rounds (bandwidth-bound), small ones the persistent kernel
-        // (latency-bound); GDX_SSSP_MODE=scan|persistent overrides.
-        // Default: frontier-scan rounds driven on the device by a CUDA graph
-        // with a conditional WHILE node (C1: 0.36 ms vs 0.44 ms for the
-        // persistent kernel and 0.56 ms with a host round trip per round).
-        // GDX_SSSP_MODE=persistent|scan|graph selects one for A/B runs.
-        // Low-degree graphs (max degree <= 64: road-like, high diameter, thousands
-        // of small rounds) take the persistent kernel instead: its queue touches
-        // only the frontier while a scan reads all n per round (2000^2 grid:
-        // 27 ms vs 76 ms).
         const char* mode = std::getenv("GDX_SSSP_MODE");
-        const std::string md = mode ? mode : graph_max_degree(g) <= 64 ? "persistent" : "graph";
-        const bool graph = md == "graph";
-        const bool scan = md == "scan" || graph;
-        if (scan) {
-            w.prev.ensure(size_t(g->n));
-            // widths: 16-bit first on large graphs (half the footprint of the
-            // gathered distance array in L2; GDX_SSSP_NARROW=0/1 overrides),
-            // unless a 16-bit attempt on this handle already overflowed; then
-            // 32-bit, then 64-bit -- each rerun exact
-            const char* ne = std::getenv("GDX_SSSP_NARROW");
-            const int narrow_env = ne ? std::atoi(ne) : -1;
-            const bool narrow = narrow_env >= 0 ? narrow_env > 0
-                                                : (g->n >= (1 << 22) && !w.narrow_overflowed);
-            bool ovf = true;
-            if (narrow) {
-                ovf = run_sssp_scan<unsigned short>(g, src, dist_out, stats, graph);
-                if (ovf) w.narrow_overflowed = true;
-            }
-            if (ovf && run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
-                run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph);
+        if (relabel_wanted(g) && graph_max_degree(g) > 64 &&
+            !(mode && std::string(mode) == "persistent")) {
+            // frontier-scan rounds on the degree-ordered renumbering
+            // (relabel.cu); the widening writes the distances in the caller's ids
+            Relabel& R = relabel_ensure(g, true, false);
+            gdx_graph* h = R.h;
+            if (!h->sssp) h->sssp = std::make_unique<SsspWork>();
+            h->sssp->out_perm = R.newid.get();
+            sssp_run(h, relabel_vertex(g, src), dist_out, stats);
+            h->sssp->out_perm = nullptr;
+            relabel_leave(g);
         } else {
-            // the persistent kernel's queues exist only in this mode (C5 in the
-            // default graph mode would otherwise hold 2 x ~2 GB of unused items);
-            // queue[1] doubles as the int64 staging buffer for host outputs
-            w.stamp.ensure(size_t(g->n));
-            w.queue[0].ensure(qcap);
-            w.queue[1].ensure(qcap > size_t(g->n) ? qcap : size_t(g->n));
-            w.ctrs.ensure(kCtrs);
-            const bool overflow = run_sssp<unsigned int>(g, src, dist_out, stats);
-            if (overflow) run_sssp<unsigned long long>(g, src, dist_out, stats);
+            sssp_run(g, src, dist_out, stats);
         }
     });
 }

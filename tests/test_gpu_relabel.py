@@ -1,0 +1,104 @@
+"""The degree-ordered renumbering cached on a handle (csrc/relabel.cu) against
+the oracle: PageRank and SSSP run on the renumbered graph and map their
+results back.  It is on by default only for skewed graphs of >= 2^22 vertices
+(the C2 / C5 bench graphs, whose parity bench.py checks every run); here
+GDX_RELABEL=1 forces it on graphs the oracle finishes in seconds.
+
+Bars as in test_gpu_parity.py: SSSP bit-exact, PageRank the same round count
+and within 1e-9 relative (only the summation order differs)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _rmat(port, scale, seed, directed, weights=None):
+    n = 1 << scale
+    u, v = port.gen_rmat_edges(n, 16 * n, seed)
+    g = port.build_from_edges(n, u, v, None, directed)
+    if weights:
+        g = port.with_random_weights(g, weights[0], weights[1], seed)
+    return g
+
+
+@pytest.fixture
+def relabel_on(monkeypatch):
+    monkeypatch.setenv("GDX_RELABEL", "1")
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_pagerank_relabelled(gdx, port, relabel_on, directed):
+    import torch
+    g = _rmat(port, 14, 3, directed)
+    dg = gdx.DeviceGraph.from_csr(g)
+    st = {}
+    r, it = dg.pagerank(0.85, 1e-9, 110, stats=st)
+    re, ie = port.pr(g, 0.85, 1e-9, 110)
+    assert it == ie and rel_err(r, re) < 1e-9
+    # repeated calls reuse the renumbered graph and its plan: identical results
+    r2, it2 = dg.pagerank(0.85, 1e-9, 110)
+    assert it2 == it and np.array_equal(r, r2)
+    # device output
+    out = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    dg.pagerank(0.85, 1e-9, 110, out=out)
+    assert np.array_equal(out.cpu().numpy(), r)
+    dg.close()
+
+
+def test_pagerank_relabel_profiled(gdx, port, relabel_on):
+    """The renumbered graph's kernels appear in the owner's profile."""
+    g = _rmat(port, 12, 4, True)
+    dg = gdx.DeviceGraph.from_csr(g)
+    dg.profile(True)
+    dg.pagerank(0.85, 1e-9, 110)
+    prof = dg.profile_read()
+    assert "relabel" in prof and "pr_edges" in prof and "pr_unpermute" in prof
+    dg.profile_reset()
+    dg.pagerank(0.85, 1e-9, 110)
+    prof = dg.profile_read()
+    assert "relabel" not in prof and prof["pr_edges"][1] > 0
+    dg.close()
+
+
+@pytest.mark.parametrize("narrow", ["0", "1"])
+def test_sssp_relabelled(gdx, port, relabel_on, monkeypatch, narrow):
+    import torch
+    monkeypatch.setenv("GDX_SSSP_NARROW", narrow)
+    monkeypatch.setenv("GDX_SSSP_SPLIT", narrow)
+    g = _rmat(port, 14, 5, False, (1, 100))
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 17, g.n - 1):
+        assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
+    out = torch.empty(g.n, dtype=torch.int64, device="cuda")
+    dg.sssp(5, out=out)
+    assert np.array_equal(out.cpu().numpy(), port.sssp(g, 5))
+    # new weights invalidate the renumbered copy (it holds the old ones)
+    dg.set_random_weights(1, 1000, 9)
+    g2 = port.with_random_weights(g, 1, 1000, 9)
+    assert np.array_equal(dg.sssp(0), port.sssp(g2, 0))
+    dg.close()
+
+
+def test_sssp_relabelled_directed_unweighted(gdx, port, relabel_on):
+    g = _rmat(port, 13, 6, True)
+    dg = gdx.DeviceGraph.from_csr(g)
+    for src in (0, 1, 100):
+        assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
+    dg.close()
+
+
+def test_relabel_off_matches(gdx, port, monkeypatch):
+    """GDX_RELABEL=0 and =1 give the same distances and round counts."""
+    g = _rmat(port, 13, 7, False, (1, 50))
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("GDX_RELABEL", flag)
+        dg = gdx.DeviceGraph.from_csr(g)
+        res[flag] = (dg.sssp(3), dg.pagerank(0.85, 1e-9, 110))
+        dg.close()
+    assert np.array_equal(res["0"][0], res["1"][0])
+    assert res["0"][1][1] == res["1"][1][1] and rel_err(res["0"][1][0], res["1"][1][0]) < 1e-12
