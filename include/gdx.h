@@ -342,6 +342,17 @@ int gdx_sssp_p2p_open(gdx_graph* g, const void* handles /* world * 64 bytes */);
 int gdx_sssp_p2p_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats);
 int gdx_sssp_p2p_close(gdx_graph* g);
 
+/* The degree-ordered renumbering gdx_pagerank / gdx_sssp run skewed graphs of
+ * >= 2^22 vertices on (csrc/relabel.cu; GDX_RELABEL=0/1 overrides): new id i
+ * is the i-th vertex by descending out-degree.  No reference counterpart --
+ * it lets the partitioned paths above (distributed.py) run on the same
+ * renumbered graph as the single-GPU calls.  algo: 0 PageRank (reverse CSR),
+ * 1 SSSP (forward CSR).  *h_out = the renumbered graph, owned by g (valid
+ * until g is destroyed or its weights change; never destroy it), or NULL when
+ * g is not renumbered for that algorithm; newid_out (n int32, host or device,
+ * may be NULL) receives newid[v] for every vertex v of g. */
+int gdx_graph_renumbered(gdx_graph* g, int32_t algo, gdx_graph** h_out, int32_t* newid_out);
+
 /* ---- measurement ------------------------------------------------------------
  * When enabled, the library brackets every kernel launch of this handle with
  * CUDA events on the launching stream.  gdx_profile_read reports, per kernel

@@ -132,6 +132,7 @@ SIGNATURES = {
     "gdx_sssp_p2p_run": ([C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(GdxStats)], C.c_int),
     "gdx_sssp_p2p_close": ([C.c_void_p], C.c_int),
     "gdx_profile_enable": ([C.c_void_p, C.c_int], C.c_int),
+    "gdx_graph_renumbered": ([C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.c_void_p], C.c_int),
     "gdx_profile_reset": ([C.c_void_p], C.c_int),
     "gdx_profile_read": ([C.c_void_p, C.c_char_p, f64p, i64p, C.c_int32, i32p], C.c_int),
 }

@@ -490,6 +490,7 @@ int gdx_profile_enable(gdx_graph* g, int enable) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
         g->prof.enabled = enable != 0;
+        if (g->relabel) g->relabel->h->prof.enabled = enable != 0;
     });
 }
 
@@ -497,6 +498,7 @@ int gdx_profile_reset(gdx_graph* g) {
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
         GraphScope dg(g);
+        relabel_leave(g);  // the renumbered graph's launches count as g's
         g->prof.drain();
         g->prof.totals.clear();
     });
@@ -507,6 +509,7 @@ int gdx_profile_read(gdx_graph* g, char* names, double* ms, int64_t* launches, i
     return guard_impl([&] {
         if (!g) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null graph");
         GraphScope dg(g);
+        relabel_leave(g);
         g->prof.drain();
         int32_t i = 0;
         for (auto& kv : g->prof.totals) {
@@ -525,3 +528,25 @@ int gdx_profile_read(gdx_graph* g, char* names, double* ms, int64_t* launches, i
 }
 
 }  // extern "C"
+
+// The degree-ordered renumbering kept on g (relabel.cu), for callers that run
+// the multi-GPU partitions on it (distributed.py): the renumbered graph, owned
+// by g, or NULL when g is not renumbered for this algorithm.
+extern "C" int gdx_graph_renumbered(gdx_graph* g, int32_t algo, gdx_graph** h_out, int32_t* newid_out) {
+    return guard_impl([&] {
+        if (!g || !h_out) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: null argument");
+        if (algo != 0 && algo != 1) fail(GDX_ERR_INVALID_ARGUMENT, "InvalidArgument: algo is 0 (PR) or 1 (SSSP)");
+        *h_out = nullptr;
+        GraphScope dg(g);
+        const bool want = algo == 0 ? g->in_offsets() && g->in_srcs() && relabel_wanted(g)
+                                    : g->dests.get() && graph_max_degree(g) > 64 &&
+                                          relabel_wanted(g);
+        if (!want) return;
+        Relabel& R = relabel_ensure(g, algo == 1, algo == 0);
+        if (newid_out)
+            copy_out(g, newid_out, R.newid.get(), size_t(g->n) * sizeof(int32_t));
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        *h_out = R.h;
+    });
+}
+

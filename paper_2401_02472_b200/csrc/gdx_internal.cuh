@@ -201,6 +201,7 @@ struct gdx_graph {
     std::unique_ptr<gdx::TcPlan> tc;
     std::unique_ptr<gdx::BcWork> bc;
     std::unique_ptr<gdx::Relabel> relabel;  // degree-ordered renumbering (relabel.cu)
+    int32_t relabel_calls = 0;              // PR / SSSP calls that could have used it
 
     // scratch for small device->host reads
     int64_t* pinned = nullptr;  // 4 KB pinned host scratch

@@ -1121,8 +1121,8 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
         GraphScope dg(g);
         const char* mode = std::getenv("GDX_SSSP_MODE");
-        if (relabel_wanted(g) && graph_max_degree(g) > 64 &&
-            !(mode && std::string(mode) == "persistent")) {
+        if (graph_max_degree(g) > 64 && !(mode && std::string(mode) == "persistent") &&
+            relabel_wanted(g)) {
             // frontier-scan rounds on the degree-ordered renumbering
             // (relabel.cu); the widening writes the distances in the caller's ids
             Relabel& R = relabel_ensure(g, true, false);

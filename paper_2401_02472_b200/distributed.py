@@ -367,6 +367,29 @@ def sharded_pr(ex: Executor, damping: float, threshold: float, max_iter: int, gr
     return (out.cpu().numpy() if to_host else out), rounds
 
 
+def _renumbered(ex: "DeviceExecutor", algo: str):
+    """(executor over the degree-ordered renumbering gdx_pagerank / gdx_sssp
+    run this graph on, newid) or None (csrc/relabel.cu).  Every rank renumbers
+    its replica with the same deterministic sort, so the ranks agree on the
+    ids.  The renumbered graph's handle is re-queried on every call (it is
+    rebuilt when the weights change); its executor is kept while it stays the
+    same handle."""
+    from .graph import _BorrowedGraph
+    if isinstance(ex.g, _BorrowedGraph):
+        return None
+    r = ex.g.renumbered(algo)
+    if r is None:
+        return None
+    h, newid = r
+    cache = ex.__dict__.setdefault("_ren", {})
+    old = cache.get(algo)
+    if old is None or old[0].g._h.value != h._h.value:
+        cache[algo] = (DeviceExecutor(h), newid)
+    else:
+        h.close()
+    return cache[algo][0], newid
+
+
 def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_iter: int,
                    group=None, to_host: bool = True):
     """ComputePR across ranks with the exchange fused into the kernels over
@@ -382,6 +405,12 @@ def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_i
     n = ex.num_nodes()
     if n == 0:
         raise GraphdslError("RuntimeError", "RuntimeError: division by zero")
+    ren = _renumbered(ex, "pr")
+    if ren is not None:  # the partitions of the graph gdx_pagerank runs on
+        rex, newid = ren
+        out, rounds = sharded_pr_p2p(rex, damping, threshold, max_iter, group, to_host=False)
+        out = torch.index_select(out, 0, newid.to(out.device))
+        return (out.cpu().numpy() if to_host else out), rounds
     ranges = _cached_ranges(ex, "pr", world, lambda: _partition(ex, "pr", world))
     v0, v1 = ranges[rank]
     g = ex.g
@@ -480,6 +509,12 @@ def sharded_sssp_p2p(ex: "DeviceExecutor", src: int, group=None, to_host: bool =
     n = ex.num_nodes()
     if not 0 <= src < n:
         raise GraphdslError("RuntimeError", f"RuntimeError: node id {src} out of range [0, {n})")
+    ren = _renumbered(ex, "sssp")
+    if ren is not None:  # the partitions of the graph gdx_sssp runs on
+        rex, newid = ren
+        out = sharded_sssp_p2p(rex, int(newid[src].item()), group, to_host=False, stats=stats)
+        out = torch.index_select(out, 0, newid.to(out.device))
+        return out.cpu().numpy() if to_host else out
     ranges = _cached_ranges(ex, "sssp", world, lambda: _partition(ex, "sssp", world))
     g = ex.g
     if getattr(ex, "_sssp_p2p", None) != (world, rank, tuple(ranges)):

@@ -185,8 +185,20 @@ class DeviceGraph:
         except Exception:
             pass
 
-    def __enter__(self):
-        return self
+    def renumbered(self, algo: str):
+        """The degree-ordered renumbering the library runs PageRank ("pr") /
+        SSSP ("sssp") on for this graph (gdx_graph_renumbered): (the renumbered
+        graph, owned by this one -- valid until this graph is closed or its
+        weights change --, newid as an int32 device tensor), or None when the
+        graph is not renumbered."""
+        import torch
+        h = C.c_void_p()
+        newid = torch.empty(max(self.n, 1), dtype=torch.int32, device=f"cuda:{self.device}")
+        check(_lib.load().gdx_graph_renumbered(self._h, 0 if algo == "pr" else 1, C.byref(h),
+                                               _ptr(newid)))
+        if not h.value:
+            return None
+        return _BorrowedGraph(h, self.device, self), newid[: self.n]
 
     def __exit__(self, *exc):
         self.close()
@@ -432,6 +444,19 @@ def _prefer_torch_nccl() -> None:
                 return
     except Exception:
         pass
+
+
+
+class _BorrowedGraph(DeviceGraph):
+    """A graph handle owned by another DeviceGraph (its renumbering): never
+    destroyed from here."""
+
+    def __init__(self, handle: C.c_void_p, device: int, owner: DeviceGraph):
+        super().__init__(handle, device)
+        self._owner = owner
+
+    def close(self) -> None:
+        self._h = None
 
 
 class Context:

@@ -102,3 +102,60 @@ def test_relabel_off_matches(gdx, port, monkeypatch):
         dg.close()
     assert np.array_equal(res["0"][0], res["1"][0])
     assert res["0"][1][1] == res["1"][1][1] and rel_err(res["0"][1][0], res["1"][1][0]) < 1e-12
+
+
+def _relabel_shard_worker(rank, world, port, q):
+    import os
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0", GDX_RELABEL="1")
+    import torch.distributed as tdist
+    import paper_2401_02472_b200 as G
+    from paper_2401_02472_b200 import distributed as D
+    from oracle import Port
+    D.init_from_env("gloo")  # the ranks share cuda:0 (see test_gpu_parity.py)
+    p = Port()
+    n = 1 << 12
+    u, v = p.gen_rmat_edges(n, 16 * n, 31)
+    gd = p.build_from_edges(n, u, v, None, True)
+    gu = p.with_random_weights(p.build_from_edges(n, u, v, None, False), 1, 100, 31)
+    exd = D.DeviceExecutor(G.DeviceGraph.from_csr(gd))
+    r, rounds = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
+    r2, rounds2 = D.sharded_pr_p2p(exd, 0.85, 1e-9, 110)
+    single, srounds = exd.g.pagerank(0.85, 1e-9, 110)
+    exu = D.DeviceExecutor(G.DeviceGraph.from_csr(gu))
+    d = D.sharded_sssp_p2p(exu, 7)
+    d2 = D.sharded_sssp_p2p(exu, 9)
+    if rank == 0:
+        er, erounds = p.pr(gd, 0.85, 1e-9, 110)
+        q.put((r, rounds, r2, rounds2, single, srounds, er, erounds, d, p.sssp(gu, 7), d2,
+               p.sssp(gu, 9)))
+    tdist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_on_renumbered_graph(gdx, world):
+    """The peer-memory PR / SSSP partitions run on the renumbered graph the
+    single-GPU calls use (distributed._renumbered) and map results back."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_relabel_shard_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    r, rounds, r2, rounds2, single, srounds, er, erounds, d, ed, d2, ed2 = q.get(timeout=250)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert rounds == rounds2 == srounds == erounds
+    assert rel_err(r, er) < 1e-9 and rel_err(single, er) < 1e-9 and np.array_equal(r, r2)
+    assert np.array_equal(d, ed) and np.array_equal(d2, ed2)
