@@ -174,6 +174,8 @@ def timed_steps(torch, dist, step, steps: int, warmup: int, flush, keep_all: boo
     t0 = time.perf_counter()
     for a, b in evs:
         flush.zero_()
+        if not keep_all:
+            results = []  # the previous step's output freed before this step allocates its own
         a.record()
         r = step()
         results = results + [r] if keep_all else [r]
