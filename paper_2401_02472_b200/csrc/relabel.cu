@@ -133,7 +133,7 @@ static void scan_offsets(gdx_graph* g, const int32_t* deg, int32_t* off, int32_t
 // One side (forward or reverse) of the renumbered CSR.
 static void relabel_side(gdx_graph* g, Relabel& R, const int32_t* old_off, const int32_t* old_adj,
                          const int32_t* old_w, DevBuf<int32_t>& off, DevBuf<int32_t>& adj,
-                         DevBuf<int32_t>* w) {
+                         DevBuf<int32_t>* w, bool sort_rows) {
     cudaStream_t s = g->stream;
     const int32_t n = g->n;
     DevBuf<int32_t> deg(size_t(n) + 1);
@@ -163,6 +163,30 @@ static void relabel_side(gdx_graph* g, Relabel& R, const int32_t* old_off, const
         m, rowid.get(), R.order.get(), off.get(), old_off, old_adj, w ? old_w : nullptr,
         R.newid.get(), adj.get(), w ? w->get() : nullptr);
     GDX_LAUNCH_CHECK();
+    rowid.release();
+    if (!sort_rows) return;
+    // rows sorted by the new ids (hubs first in every row), weights alongside
+    DevBuf<int32_t> adj2(static_cast<size_t>(m));
+    DevBuf<int32_t> w2;
+    if (w) w2.alloc(size_t(m));
+    size_t sb = 0;
+    if (w)
+        GDX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, adj.get(), adj2.get(), w->get(),
+                                                     w2.get(), int(m), n, off.get(),
+                                                     off.get() + 1, s));
+    else
+        GDX_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, adj.get(), adj2.get(), int(m), n,
+                                                    off.get(), off.get() + 1, s));
+    DevBuf<uint8_t> tmp(sb);
+    if (w)
+        GDX_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.get(), sb, adj.get(), adj2.get(), w->get(),
+                                                     w2.get(), int(m), n, off.get(),
+                                                     off.get() + 1, s));
+    else
+        GDX_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.get(), sb, adj.get(), adj2.get(), int(m), n,
+                                                    off.get(), off.get() + 1, s));
+    adj = std::move(adj2);
+    if (w) *w = std::move(w2);
 }
 
 Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev) {
@@ -208,9 +232,11 @@ Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev) {
     if (!R.fwd_off || (fwd_adj && !R.fwd_adj)) {
         timed_launch(g, "relabel", [&] {
             if (fwd_adj) {
+                // GDX_RELABEL_SORT=1: rows sorted by the new ids (A/B knob)
+                const char* se = std::getenv("GDX_RELABEL_SORT");
                 relabel_side(g, R, g->offsets.get(), g->dests.get(),
                              g->weighted ? g->weights.get() : nullptr, h->offsets, h->dests,
-                             g->weighted ? &h->weights : nullptr);
+                             g->weighted ? &h->weights : nullptr, se && std::atoi(se) != 0);
             } else {
                 DevBuf<int32_t> deg(size_t(n) + 1);
                 k_rl_row_degrees<<<blocks_for(int64_t(n) + 1, 256, g->num_sms * 8), 256, 0, s>>>(
@@ -226,7 +252,7 @@ Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev) {
     if (need_rev && g->directed && !R.rev) {
         timed_launch(g, "relabel", [&] {
             relabel_side(g, R, g->in_offsets(), g->in_srcs(), nullptr, h->rev_offsets,
-                         h->rev_srcs, nullptr);
+                         h->rev_srcs, nullptr, false);
         });
         R.rev = true;
     }
