@@ -840,7 +840,7 @@ def run_ours(args) -> None:
         elif a == "bc":
             per["bc"] = bench_bc(torch, gdx, dist, args, pk, cpu)
     per["pr"] = {k: head[k] for k in ("workload", "gteps", "ms_per_step", "rounds", "roofline",
-                                      "cpu_baseline", "parity") if k in head}
+                                      "cpu_baseline", "parity", "renumbering") if k in head}
     parity = {k: v["parity"]["ok"] for k, v in per.items() if "parity" in v}
     for k, v in per.items():
         if "certificate_ok" in v:
@@ -864,6 +864,8 @@ def run_ours(args) -> None:
     }
     if "cpu_baseline" in head:
         line["cpu_baseline"] = head["cpu_baseline"]
+    if "renumbering" in head:
+        line["renumbering"] = head["renumbering"]
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
