@@ -57,7 +57,9 @@ struct PrArgs {
     int32_t m, nnz;
     const int2* __restrict__ nz;          // k-th row with in-edges: (vertex, rev_offsets[vertex + 1])
     const int2* __restrict__ grp;         // per 8-edge group: (nz index of its first row, that row's end)
-    double* row_sum;                      // per vertex, zero between rounds
+    double* row_sum;                      // per vertex: every non-empty row's sum is stored
+                                          // once per round (plain stores, no accumulation),
+                                          // empty rows stay 0 from the plan's memset
     // rows crossing a warp chunk (256 in-edges) are summed in pass B from the
     // chunks' partials, in chunk order (deterministic: no atomics)
     double* head_part;                    // per chunk: the row that began in an earlier chunk
@@ -134,7 +136,8 @@ __device__ inline void block_flush(const PrArgs& a, int round, double dang_local
 // warp (segmented shuffle scan), or across warps (per-chunk partials summed
 // in chunk order by pass B).
 // Pass B (k_pr_vertices) applies pr.sp:17-30 to every vertex with coalesced
-// loads, and clears row_sum for the next round.
+// loads (row_sum needs no clearing: pass A / k_pr_cross store every
+// non-empty row's sum exactly once per round).
 // ---------------------------------------------------------------------------
 
 constexpr int kEdgeGroup = 8;
@@ -281,8 +284,7 @@ __device__ inline void pr_vertex_one(const PrArgs& a, int round, int64_t v, doub
                                      double* __restrict__ rank_out,
                                      double* __restrict__ contrib_out, double& dang_local,
                                      int& unsettled) {
-    const double sum = a.row_sum[v];
-    if (sum != 0.0) a.row_sum[v] = 0.0;
+    const double sum = a.row_sum[v];  // stored this round (or 0: no in-edges)
     const double nr = a.base + a.damping * (dang_term + sum);
     double c = nr - rank_in[v];
     if (c < 0.0) c = 0.0 - c;
@@ -318,8 +320,6 @@ __device__ inline void pr_vertex_pair(const PrArgs& a, int round, int64_t v, dou
         const double2 sum = *reinterpret_cast<const double2*>(a.row_sum + v);
         const double2 ri = *reinterpret_cast<const double2*>(rank_in + v);
         const int32_t o0 = a.offsets[v], o1 = a.offsets[v + 1], o2 = a.offsets[v + 2];
-        if (sum.x != 0.0 || sum.y != 0.0)
-            *reinterpret_cast<double2*>(a.row_sum + v) = make_double2(0.0, 0.0);
         const double nr0 = a.base + a.damping * (dang_term + sum.x);
         const double nr1 = a.base + a.damping * (dang_term + sum.y);
         double c0 = nr0 - ri.x, c1 = nr1 - ri.y;
