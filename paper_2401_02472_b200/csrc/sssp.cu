@@ -818,9 +818,10 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const char* rc = std::getenv("GDX_SSSP_RELAX_CAP");  // blocks per SM (A/B)
     // 8 blocks/SM for small graphs -- one resident wave of 256-thread blocks
     // (same-box C1 0.222 vs 0.227 ms at 16, 0.238 at 4) -- 128 for large ones
-    // (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32)
+    // (same-box C5: 21.3 vs 21.9 ms at 64, 22.9 at 32; on the renumbered graph
+    // 256: 16.61-16.66 vs 16.86 ms at 128, 16.78-16.85 at 512)
     const int relax_grid =
-        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 8 : 128)) * g->num_sms;
+        (rc ? std::max(1, std::atoi(rc)) : (g->m < (int64_t(1) << 26) ? 8 : 256)) * g->num_sms;
     prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, 16>), kRelaxCarveout);
     prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, kSmallLpi, false, kSmallDeg>),
               kRelaxCarveout);
@@ -1417,7 +1418,7 @@ static void multi_prepare(MultiPart& p, SsspOwners own, int nd, int self) {
     int2* squeue = multi_split(g) ? w.small_queue.get() : nullptr;
     D* dist = static_cast<D*>(p.dist);
     D* prev = reinterpret_cast<D*>(w.prev.get());
-    const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 128) * g->num_sms;
+    const int relax_grid = (g->m < (int64_t(1) << 26) ? 16 : 256) * g->num_sms;  // as gdx_sssp
     // the instantiated loop bakes in this partition's buffers, its range and
     // every partition's replica
     std::vector<void*> key = {dist, prev, w.shard_queue.get(), w.shard_ctr.get(), w.graph_acc.get(),
