@@ -443,9 +443,11 @@ def sharded_pr_p2p(ex: "DeviceExecutor", damping: float, threshold: float, max_i
                                 "iterations without converging")
     dev = _device_for_collectives()
     chunk = max(max(b - a for a, b in ranges), 1)
-    rank_slice = torch.zeros(chunk, dtype=torch.float64, device=dev)
+    # no zero fills: the slice's padding is never unpacked, and the ranges
+    # cover [0, n), so every entry of `out` is written
+    rank_slice = torch.empty(chunk, dtype=torch.float64, device=dev)
     ex.pr_rank(rounds, rank_slice)
-    out = torch.zeros(n, dtype=torch.float64, device=dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
     _all_gather_slices(rank_slice, ranges, out, group)
     return (out.cpu().numpy() if to_host else out), rounds
 
