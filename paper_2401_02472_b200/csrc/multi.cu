@@ -43,6 +43,7 @@ void sssp_multi(const std::vector<gdx_graph*>& gs, const std::vector<int32_t>& b
 void pr_p2p_local_setup(gdx_graph* g, int32_t world, int32_t rank);
 double* pr_p2p_block(gdx_graph* g);
 void pr_p2p_local_open(gdx_graph* g, const std::vector<double*>& blocks);
+void relabel_unpermute_i64(gdx_graph* g, const int64_t* in, int64_t* out);
 
 namespace {
 
@@ -174,6 +175,10 @@ struct gdx_multi_graph {
     std::vector<int32_t> offsets, in_offsets;  // host copies, for the partitions
     std::vector<int32_t> pr_bound;             // ranges of the prepared PR exchange
     std::vector<gdx::DevBuf<double>> bc_buf;   // per-device BC accumulators
+    // the replicas' degree-ordered renumbering (relabel.cu), once they have one:
+    // its host offsets per side for the partitions, and the PR exchange over it
+    gdx_graph* ren_h0 = nullptr;               // device 0's renumbered handle they belong to
+    std::vector<int32_t> ren_offsets, ren_in_offsets, ren_pr_bound;
     ~gdx_multi_graph() {
         for (size_t d = 0; d < bc_buf.size() && d < gs.size(); ++d) {  // on its own device
             gdx::GraphScope sc(gs[d]);
@@ -196,6 +201,56 @@ std::vector<double> degree_weights(const std::vector<int32_t>& off, bool squared
         w[v] = squared ? d * d / 2.0 + d + 1.0 : d + 1.0;
     }
     return w;
+}
+
+// The replicas' renumbered handles for this call (algo 0 PR, 1 SSSP), or an
+// empty vector: every replica takes gdx_pagerank / gdx_sssp's decision
+// (relabel_wanted counts the calls per handle, so they agree), and the host
+// offsets of the renumbered graph are cached for the partitions.
+std::vector<gdx_graph*> multi_renumbered(gdx_multi_graph* mg, int algo) {
+    std::vector<gdx_graph*> hs;
+    const int nd = int(mg->gs.size());
+    for (int d = 0; d < nd; ++d) {
+        gdx_graph* g = mg->gs[d];
+        GraphScope sc(g);
+        const bool want = algo == 0 ? relabel_wanted(g)
+                                    : graph_max_degree(g) > 64 && relabel_wanted(g);
+        if (!want) {
+            if (d > 0) fail(GDX_ERR_RUNTIME, "RuntimeError: replicas disagree on the renumbering");
+            return {};
+        }
+        hs.push_back(relabel_ensure(g, algo == 1, algo == 0).h);
+    }
+    if (mg->ren_h0 != hs[0]) {  // a new renumbering (first use, or the weights changed)
+        mg->ren_h0 = hs[0];
+        mg->ren_offsets.clear();
+        mg->ren_in_offsets.clear();
+        mg->ren_pr_bound.clear();
+    }
+    gdx_graph* h = hs[0];
+    GraphScope sc(mg->gs[0]);
+    if (mg->ren_offsets.empty()) {
+        mg->ren_offsets.resize(size_t(mg->n) + 1);
+        GDX_CUDA(cudaMemcpyAsync(mg->ren_offsets.data(), h->offsets.get(), mg->ren_offsets.size() * 4,
+                                 cudaMemcpyDeviceToHost, h->stream));
+    }
+    if (algo == 0 && mg->ren_in_offsets.empty()) {
+        mg->ren_in_offsets.resize(size_t(mg->n) + 1);
+        GDX_CUDA(cudaMemcpyAsync(mg->ren_in_offsets.data(), h->in_offsets(),
+                                 mg->ren_in_offsets.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+    }
+    GDX_CUDA(cudaStreamSynchronize(h->stream));
+    return hs;
+}
+
+// out[v] = in[newid[v]] on device 0, into dst (host or device).
+void multi_unpermute(gdx_multi_graph* mg, const int64_t* in, int64_t* dst) {
+    gdx_graph* g = mg->gs[0];
+    GraphScope sc(g);
+    DevBuf<int64_t> tmp(size_t(std::max(mg->n, 1)));
+    relabel_unpermute_i64(g, in, tmp.get());
+    copy_out(g, dst, tmp.get(), size_t(mg->n) * sizeof(int64_t));
+    GDX_CUDA(cudaStreamSynchronize(g->stream));
 }
 
 void merge_stats(gdx_stats* into, const gdx_stats& s) {
@@ -308,8 +363,26 @@ int gdx_sssp_multi(gdx_multi_graph* mg, int32_t src, int64_t* dist_out, gdx_stat
                                            " out of range [0, " + std::to_string(mg->n) + ")");
         const int nd = int(mg->gs.size());
         gdx_stats st{};
-        sssp_multi(mg->gs, balanced_bounds(degree_weights(mg->offsets, false), nd), src, dist_out,
-                   &st);
+        const auto hs = multi_renumbered(mg, 1);
+        if (!hs.empty()) {
+            // the partitions of the renumbered graph gdx_sssp runs on, the
+            // distances mapped back (device 0 gathers them)
+            gdx_graph* g0 = mg->gs[0];
+            const int32_t s = relabel_vertex(g0, src);
+            DevBuf<int64_t> tmp;
+            {
+                GraphScope sc(g0);
+                tmp.alloc(size_t(std::max(mg->n, 1)));
+            }
+            sssp_multi(hs, balanced_bounds(degree_weights(mg->ren_offsets, false), nd), s,
+                       tmp.get(), &st);
+            multi_unpermute(mg, tmp.get(), dist_out);
+            GraphScope sc(g0);
+            tmp.release();
+        } else {
+            sssp_multi(mg->gs, balanced_bounds(degree_weights(mg->offsets, false), nd), src,
+                       dist_out, &st);
+        }
         if (stats) *stats = st;
     });
 }
@@ -322,18 +395,30 @@ int gdx_pagerank_multi(gdx_multi_graph* mg, double damping, double threshold, in
         if (mg->in_offsets.empty())
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
         const int nd = int(mg->gs.size());
-        if (mg->pr_bound.empty()) {  // shard plans and the peer-memory exchange, once
-            const auto b = balanced_bounds(degree_weights(mg->in_offsets, false), nd);
+        // the replicas, or their renumbering (the graph gdx_pagerank runs on)
+        const auto hs = multi_renumbered(mg, 0);
+        const bool ren = !hs.empty();
+        const std::vector<gdx_graph*>& gs = ren ? hs : mg->gs;
+        std::vector<int32_t>& bound = ren ? mg->ren_pr_bound : mg->pr_bound;
+        if (bound.empty()) {  // shard plans and the peer-memory exchange, once
+            const auto b = balanced_bounds(
+                degree_weights(ren ? mg->ren_in_offsets : mg->in_offsets, false), nd);
             std::vector<double*> blocks(nd);
             for (int d = 0; d < nd; ++d) {
-                call(gdx_pr_shard_setup(mg->gs[d], b[d], b[d + 1]));
-                pr_p2p_local_setup(mg->gs[d], nd, d);
-                blocks[d] = pr_p2p_block(mg->gs[d]);
+                call(gdx_pr_shard_setup(gs[d], b[d], b[d + 1]));
+                pr_p2p_local_setup(gs[d], nd, d);
+                blocks[d] = pr_p2p_block(gs[d]);
             }
-            for (int d = 0; d < nd; ++d) pr_p2p_local_open(mg->gs[d], blocks);
-            mg->pr_bound = b;
+            for (int d = 0; d < nd; ++d) pr_p2p_local_open(gs[d], blocks);
+            bound = b;
         }
-        const auto& b = mg->pr_bound;
+        const auto& b = bound;
+        DevBuf<int64_t> tmp;  // renumbered: the ranks in the new ids, on device 0
+        if (ren) {
+            GraphScope sc(mg->gs[0]);
+            tmp.alloc(size_t(mg->n));
+        }
+        double* out = ren ? reinterpret_cast<double*>(tmp.get()) : rank_out;
         // fixedPoint rounds: at most max_iter+1 (pr.sp:25) and the
         // interpreter's cap 10n+100 (interpreter.cpp:977-986)
         const int64_t cap = 10 * int64_t(mg->n) + 100;
@@ -342,7 +427,7 @@ int gdx_pagerank_multi(gdx_multi_graph* mg, double damping, double threshold, in
         std::vector<int64_t> rounds(nd, -1);
         std::vector<char> settled_seen(nd, 0);
         on_devices(nd, [&](int d) {
-            gdx_graph* g = mg->gs[d];
+            gdx_graph* g = gs[d];
             double part[2];
             call(gdx_pr_p2p_init(g, part));
             const double dangling = part[0];
@@ -361,8 +446,13 @@ int gdx_pagerank_multi(gdx_multi_graph* mg, double damping, double threshold, in
                 batch = std::min<int64_t>(2 * batch, 64);
             }
             rounds[d] = done;
-            call(gdx_pr_shard_rank(g, int32_t(done), rank_out + b[d]));
+            call(gdx_pr_shard_rank(g, int32_t(done), out + b[d]));
         });
+        if (ren) {  // the f64 bit patterns move like int64
+            multi_unpermute(mg, tmp.get(), reinterpret_cast<int64_t*>(rank_out));
+            GraphScope sc(mg->gs[0]);
+            tmp.release();
+        }
         const int64_t done = rounds[0];
         if (!settled_seen[0] && limit < want) {
             // every round voted "unsettled" up to the cap

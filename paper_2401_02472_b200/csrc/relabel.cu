@@ -283,6 +283,12 @@ void relabel_unpermute_f64(gdx_graph* g, const double* in, double* out) {
     GDX_LAUNCH_CHECK();
 }
 
+void relabel_unpermute_i64(gdx_graph* g, const int64_t* in, int64_t* out) {
+    k_rl_unpermute<int64_t><<<blocks_for(g->n, 256, g->num_sms * 8), 256, 0, g->stream>>>(
+        g->n, g->relabel->newid.get(), in, out);
+    GDX_LAUNCH_CHECK();
+}
+
 int32_t relabel_vertex(gdx_graph* g, int32_t v) {
     int32_t r = 0;
     GDX_CUDA(cudaMemcpyAsync(&r, g->relabel->newid.get() + v, 4, cudaMemcpyDeviceToHost, g->stream));

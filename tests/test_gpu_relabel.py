@@ -159,3 +159,24 @@ def test_sharded_on_renumbered_graph(gdx, world):
     assert rounds == rounds2 == srounds == erounds
     assert rel_err(r, er) < 1e-9 and rel_err(single, er) < 1e-9 and np.array_equal(r, r2)
     assert np.array_equal(d, ed) and np.array_equal(d2, ed2)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0]])
+def test_multi_on_renumbered_graph(gdx, port, relabel_on, devices):
+    """The in-process gdx_sssp_multi / gdx_pagerank_multi partition the
+    replicas' renumbering and map the results back."""
+    und = _rmat(port, 13, 8, False, (1, 100))
+    dr = _rmat(port, 13, 9, True)
+    ctx = gdx.Context(devices)
+    mu = gdx.MultiGraph(ctx, und)
+    md = gdx.MultiGraph(ctx, dr)
+    for src in (0, 17, und.n - 1):
+        assert np.array_equal(mu.sssp(src), port.sssp(und, src)), src
+    r, it = md.pagerank(0.85, 1e-9, 110)
+    re, ie = port.pr(dr, 0.85, 1e-9, 110)
+    assert it == ie and rel_err(r, re) < 1e-9
+    r2, it2 = md.pagerank(0.85, 1e-9, 110)
+    assert it2 == it and np.array_equal(r, r2)
+    mu.close()
+    md.close()
+    ctx.close()
