@@ -36,5 +36,7 @@ cap pr_edges pr k_pr_edges 2 GDX_RELABEL=1
 cap pr_vertices pr k_pr_vertices 2 GDX_RELABEL=1
 cap tc tc k_tc_oriented 0
 cap sssp_relax_c1 sssp k_sssp_scan_relax 3
-cap sssp_relax sssp26 k_sssp_scan_relax 3 GDX_RELABEL=1
+# the third round's main relaxation (the largest of a C5 call; main and small-vertex
+# launches alternate)
+cap sssp_relax sssp26 k_sssp_scan_relax 4 GDX_RELABEL=1
 cap bc_cta bc k_bc_cta 0
