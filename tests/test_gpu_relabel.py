@@ -180,3 +180,29 @@ def test_multi_on_renumbered_graph(gdx, port, relabel_on, devices):
     mu.close()
     md.close()
     ctx.close()
+
+
+def test_auto_policy_at_size(gdx, monkeypatch):
+    """Default policy on a skewed graph of 2^22 vertices: the first call runs
+    on the caller's numbering, the second builds the renumbering and runs on
+    it (the profile shows the build), later calls reuse it.  SSSP distances
+    identical across all calls, PageRank within 1e-12 with the same rounds
+    (bit-identical from the second call on)."""
+    import torch
+    monkeypatch.delenv("GDX_RELABEL", raising=False)
+    n = 1 << 22
+    du = gdx.DeviceGraph.generate("rmat", n, 16 * n, seed=3, directed=False, weights=(1, 100))
+    out = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(3)]
+    du.profile(True)
+    du.sssp(0, out=out[0])
+    assert "relabel" not in du.profile_read()
+    du.sssp(0, out=out[1])
+    assert "relabel" in du.profile_read()
+    du.sssp(0, out=out[2])
+    assert torch.equal(out[0], out[1]) and torch.equal(out[1], out[2])
+    du.close()
+    dd = gdx.DeviceGraph.generate("rmat", n, 16 * n, seed=4, directed=True)
+    r = [dd.pagerank(0.85, 1e-6, 100) for _ in range(3)]
+    assert r[0][1] == r[1][1] == r[2][1]
+    assert rel_err(r[0][0], r[1][0]) < 1e-12 and np.array_equal(r[1][0], r[2][0])
+    dd.close()
