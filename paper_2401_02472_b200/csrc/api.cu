@@ -541,8 +541,9 @@ extern "C" int gdx_graph_renumbered(gdx_graph* g, int32_t algo, gdx_graph** h_ou
         const bool want = algo == 0 ? g->in_offsets() && g->in_srcs() && relabel_wanted(g)
                                     : g->dests.get() && graph_max_degree(g) > 64 &&
                                           relabel_wanted(g);
-        if (!want) return;
-        Relabel& R = relabel_ensure(g, algo == 1, algo == 0);
+        Relabel* RP = want ? relabel_try(g, algo == 1, algo == 0) : nullptr;
+        if (!RP) return;
+        Relabel& R = *RP;
         if (newid_out)
             copy_out(g, newid_out, R.newid.get(), size_t(g->n) * sizeof(int32_t));
         GDX_CUDA(cudaStreamSynchronize(g->stream));

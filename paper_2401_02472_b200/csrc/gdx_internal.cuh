@@ -202,6 +202,7 @@ struct gdx_graph {
     std::unique_ptr<gdx::BcWork> bc;
     std::unique_ptr<gdx::Relabel> relabel;  // degree-ordered renumbering (relabel.cu)
     int32_t relabel_calls = 0;              // PR / SSSP calls that could have used it
+    bool relabel_failed = false;            // its build ran out of device memory: never again
 
     // scratch for small device->host reads
     int64_t* pinned = nullptr;  // 4 KB pinned host scratch
@@ -276,6 +277,9 @@ int32_t graph_max_degree(gdx_graph* g);
 // relabel.cu: the degree-ordered renumbering cached on a handle
 bool relabel_wanted(gdx_graph* g);
 Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev);
+// relabel_ensure, or nullptr when its build runs out of device memory (the
+// call then runs on the caller's numbering, and the handle stops trying)
+Relabel* relabel_try(gdx_graph* g, bool need_fwd, bool need_rev);
 void relabel_leave(gdx_graph* g);  // the hidden graph's profile records to g
 void relabel_unpermute_f64(gdx_graph* g, const double* in, double* out);
 int32_t relabel_vertex(gdx_graph* g, int32_t v);  // newid[v] (host read)

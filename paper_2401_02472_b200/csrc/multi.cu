@@ -219,7 +219,17 @@ std::vector<gdx_graph*> multi_renumbered(gdx_multi_graph* mg, int algo) {
             if (d > 0) fail(GDX_ERR_RUNTIME, "RuntimeError: replicas disagree on the renumbering");
             return {};
         }
-        hs.push_back(relabel_ensure(g, algo == 1, algo == 0).h);
+        Relabel* R = relabel_try(g, algo == 1, algo == 0);
+        if (!R) {  // out of memory on one replica: every replica keeps its numbering
+            for (auto* r : mg->gs) {
+                GraphScope s2(r);
+                r->relabel.reset();
+                r->relabel_failed = true;
+            }
+            mg->ren_h0 = nullptr;
+            return {};
+        }
+        hs.push_back(R->h);
     }
     if (mg->ren_h0 != hs[0]) {  // a new renumbering (first use, or the weights changed)
         mg->ren_h0 = hs[0];

@@ -752,10 +752,11 @@ extern "C" int gdx_pagerank(gdx_graph* g, double damping, double threshold, int3
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no reverse adjacency");
         GraphScope dg(g);
         const size_t bytes = size_t(g->n) * sizeof(double);
-        if (relabel_wanted(g)) {
+        Relabel* RP = relabel_wanted(g) ? relabel_try(g, false, true) : nullptr;
+        if (RP) {
             // the rounds on the degree-ordered renumbering (relabel.cu), the
             // ranks mapped back: rank_out[v] = rank'[newid[v]]
-            Relabel& R = relabel_ensure(g, false, true);
+            Relabel& R = *RP;
             const double* r = pagerank_run(R.h, damping, threshold, max_iter, rounds_out, stats);
             relabel_leave(g);
             cudaPointerAttributes pa;

@@ -112,6 +112,7 @@ Relabel::~Relabel() { delete h; }
 // pattern, never pays for it) and stays renumbered.  GDX_RELABEL=0/1 forces
 // it off / on from the first call.
 bool relabel_wanted(gdx_graph* g) {
+    if (g->relabel_failed) return false;
     const char* e = std::getenv("GDX_RELABEL");
     if (e) return std::atoi(e) != 0 && g->n > 0;
     if (g->relabel) return true;
@@ -205,6 +206,8 @@ Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev) {
     cudaStream_t s = g->stream;
     const int32_t n = g->n;
     if (!g->relabel) {
+        if (std::getenv("GDX_RELABEL_TEST_OOM"))  // tests: the out-of-memory fallback
+            fail(GDX_ERR_OUT_OF_MEMORY, "OutOfMemory: renumbering (GDX_RELABEL_TEST_OOM)");
         auto R = std::make_unique<Relabel>();
         timed_launch(g, "relabel", [&] {
             DevBuf<int32_t> deg(n), iota(n), sorted(n);
@@ -268,6 +271,19 @@ Relabel& relabel_ensure(gdx_graph* g, bool need_fwd, bool need_rev) {
     }
     h->prof.enabled = g->prof.enabled;
     return R;
+}
+
+Relabel* relabel_try(gdx_graph* g, bool need_fwd, bool need_rev) {
+    try {
+        return &relabel_ensure(g, need_fwd, need_rev);
+    } catch (const Error& e) {
+        if (e.code != GDX_ERR_OUT_OF_MEMORY) throw;
+        GDX_CUDA(cudaStreamSynchronize(g->stream));
+        g->relabel.reset();
+        g->relabel_failed = true;
+        cudaGetLastError();
+        return nullptr;
+    }
 }
 
 void relabel_leave(gdx_graph* g) {

@@ -1122,11 +1122,14 @@ extern "C" int gdx_sssp(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats*
             fail(GDX_ERR_UNSUPPORTED, "Unsupported: graph has no forward adjacency");
         GraphScope dg(g);
         const char* mode = std::getenv("GDX_SSSP_MODE");
-        if (graph_max_degree(g) > 64 && !(mode && std::string(mode) == "persistent") &&
-            relabel_wanted(g)) {
+        Relabel* RP = graph_max_degree(g) > 64 && !(mode && std::string(mode) == "persistent") &&
+                              relabel_wanted(g)
+                          ? relabel_try(g, true, false)
+                          : nullptr;
+        if (RP) {
             // frontier-scan rounds on the degree-ordered renumbering
             // (relabel.cu); the widening writes the distances in the caller's ids
-            Relabel& R = relabel_ensure(g, true, false);
+            Relabel& R = *RP;
             gdx_graph* h = R.h;
             if (!h->sssp) h->sssp = std::make_unique<SsspWork>();
             h->sssp->out_perm = R.newid.get();

@@ -206,3 +206,18 @@ def test_auto_policy_at_size(gdx, monkeypatch):
     assert r[0][1] == r[1][1] == r[2][1]
     assert rel_err(r[0][0], r[1][0]) < 1e-12 and np.array_equal(r[1][0], r[2][0])
     dd.close()
+
+
+def test_renumbering_out_of_memory_falls_back(gdx, port, relabel_on, monkeypatch):
+    """A renumbering build that runs out of device memory leaves the call on
+    the caller's numbering (same results) and the handle stops trying."""
+    monkeypatch.setenv("GDX_RELABEL_TEST_OOM", "1")
+    g = _rmat(port, 12, 10, False, (1, 100))
+    dg = gdx.DeviceGraph.from_csr(g)
+    dg.profile(True)
+    assert np.array_equal(dg.sssp(0), port.sssp(g, 0))
+    r, it = dg.pagerank(0.85, 1e-9, 110)
+    re, ie = port.pr(g, 0.85, 1e-9, 110)
+    assert it == ie and rel_err(r, re) < 1e-9
+    assert dg.renumbered("sssp") is None and "relabel" not in dg.profile_read()
+    dg.close()
