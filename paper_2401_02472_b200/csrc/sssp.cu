@@ -437,21 +437,13 @@ constexpr int32_t kSmallScan = 1 << 22;
 constexpr int kSmallDeg = GDX_SSSP_SMALLDEG;
 constexpr int kSmallLpi = kSmallDeg / 4;  // 4 edges per lane
 constexpr int kSmallCtr = 7;
-// COH: the loads of values other SMs write during the same kernel (the fused
-// small-graph loop, k_sssp_fused) go to L2 (ld.global.cg): the L1 is not
-// coherent within a kernel.  The per-round kernels read them through L1.
-template <bool COH, class D>
-__device__ __forceinline__ D ld_coh(const D* p) {
-    if constexpr (COH) return __ldcg(p);
-    else return *p;
-}
-
-template <class D, int PER, bool SPLIT, bool COH>
-__device__ __forceinline__ void scan_frontier_body(int32_t v0, int32_t v1,
-                                                   const int32_t* __restrict__ offsets,
-                                                   const D* __restrict__ dist, D* prev,
-                                                   int2* queue, unsigned long long* ctr,
-                                                   int2* squeue) {
+template <class D, int PER = kFPer, bool SPLIT = false>
+__global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int32_t v1,
+                                                           const int32_t* __restrict__ offsets,
+                                                           const D* __restrict__ dist, D* prev,
+                                                           int2* queue,
+                                                           unsigned long long* ctr,
+                                                           int2* squeue = nullptr) {
     constexpr int kPer = PER;  // vertices per thread per chunk
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -471,8 +463,8 @@ __device__ __forceinline__ void scan_frontier_body(int32_t v0, int32_t v1,
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int64_t v = c0 + int64_t(k) * kFBlock + threadIdx.x;
-            dk[k] = v < v1 ? ld_coh<COH>(dist + v) : D(0);
-            pk[k] = v < v1 ? ld_coh<COH>(prev + v) : D(0);
+            dk[k] = v < v1 ? dist[v] : D(0);
+            pk[k] = v < v1 ? prev[v] : D(0);
         }
         int items[kPer], first[kPer], last[kPer];
 #pragma unroll
@@ -572,16 +564,6 @@ __device__ __forceinline__ void scan_frontier_body(int32_t v0, int32_t v1,
     }
 }
 
-template <class D, int PER = kFPer, bool SPLIT = false>
-__global__ void __launch_bounds__(kFBlock) k_sssp_scan_frontier(int32_t v0, int32_t v1,
-                                                           const int32_t* __restrict__ offsets,
-                                                           const D* __restrict__ dist, D* prev,
-                                                           int2* queue,
-                                                           unsigned long long* ctr,
-                                                           int2* squeue = nullptr) {
-    scan_frontier_body<D, PER, SPLIT, false>(v0, v1, offsets, dist, prev, queue, ctr, squeue);
-}
-
 // Frontier-scan grid: up to 64 blocks per SM (a few chunks each; same-box C5:
 // 21.0 vs 21.35 ms with one resident wave of ~44-chunk blocks);
 // GDX_SSSP_FGRID = blocks per SM overrides.
@@ -632,27 +614,25 @@ struct SsspDelta {
     int32_t round;
 };
 
-template <class D, int LPI, bool DELTA, int CH, bool COH>
-__device__ __forceinline__ void relax_body(const int2* __restrict__ queue,
-                                           const unsigned long long* __restrict__ ctr,
-                                           const int32_t* __restrict__ offsets,
-                                           const int32_t* __restrict__ dests,
-                                           const int32_t* __restrict__ weights, D* dist,
-                                           unsigned long long* ovf, SsspDelta dl,
-                                           unsigned long long* upd) {
+template <class D, int LPI, bool DELTA = false, int CH = kShardChunk>
+__global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict__ queue,
+                                                        const unsigned long long* __restrict__ ctr,
+                                                        const int32_t* __restrict__ offsets,
+                                                        const int32_t* __restrict__ dests,
+                                                        const int32_t* __restrict__ weights,
+                                                        D* dist, unsigned long long* ovf,
+                                                        SsspDelta dl = {},
+                                                        unsigned long long* upd = nullptr) {
     // LPI lanes per item: lane groups of LPI take one item each
     const int sub = threadIdx.x & (LPI - 1);
     unsigned int issued = 0;  // relaxations that issued an atomicMin
     constexpr int kU = CH / LPI;  // edges per lane per item, all loads issued together
     static_assert(CH % LPI == 0, "an item's edges split evenly over its lanes");
-    const unsigned long long nq = ld_coh<COH>(ctr);
+    const unsigned long long nq = ctr[0];
     for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) / LPI;
          i < nq; i += ((unsigned long long)gridDim.x * blockDim.x) / LPI) {
-        const int2 it = ld_coh<COH>(queue + i);
-        // the item's own distance must be current (a stale, larger one would
-        // relax its edges too weakly); the neighbours' may be stale (larger):
-        // that only costs a redundant atomicMin
-        const D dv = ld_coh<COH>(dist + it.x);
+        const int2 it = queue[i];
+        const D dv = dist[it.x];
         // int64: it.y + CH passes INT32_MAX on the last items of m ~ 2^31 graphs
         const int32_t e1 = int32_t(min(int64_t(it.y) + CH, int64_t(offsets[it.x + 1])));
         int32_t u[kU];
@@ -687,54 +667,7 @@ __device__ __forceinline__ void relax_body(const int2* __restrict__ queue,
     if (upd) warp_count(issued, upd);
 }
 
-template <class D, int LPI, bool DELTA = false, int CH = kShardChunk>
-__global__ void __launch_bounds__(256) k_sssp_scan_relax(const int2* __restrict__ queue,
-                                                        const unsigned long long* __restrict__ ctr,
-                                                        const int32_t* __restrict__ offsets,
-                                                        const int32_t* __restrict__ dests,
-                                                        const int32_t* __restrict__ weights,
-                                                        D* dist, unsigned long long* ovf,
-                                                        SsspDelta dl = {},
-                                                        unsigned long long* upd = nullptr) {
-    relax_body<D, LPI, DELTA, CH, false>(queue, ctr, offsets, dests, weights, dist, ovf, dl, upd);
-}
-
 constexpr int kRelaxCarveout = -1;  // relaxation's shared-memory carveout (prefer_l1)
-
-// Small graphs (GDX_SSSP_MODE=fused): the whole round loop in one cooperative
-// kernel -- frontier scan, grid barrier, relaxation, grid barrier -- instead
-// of three graph nodes per round (a grid barrier costs ~1.2 us on B200,
-// tools/micro/gridsync.cu; a dependent kernel launch inside a graph several).
-// The round's counters alternate between two sets of 8 (a set is cleared by
-// block 0 one round after it was last read); loads of values other SMs wrote
-// go to L2 (COH).  graph_acc gets [rounds, vertices, edges, overflow] as in
-// the graph path.
-template <class D>
-__global__ void __launch_bounds__(256) k_sssp_fused(int32_t n, const int32_t* __restrict__ offsets,
-                                                    const int32_t* __restrict__ dests,
-                                                    const int32_t* __restrict__ weights, D* dist,
-                                                    D* prev, int2* queue, unsigned long long* fctr,
-                                                    unsigned long long* acc,
-                                                    unsigned long long* upd) {
-    cg::grid_group gg = cg::this_grid();
-    for (int r = 0;; ++r) {
-        unsigned long long* c = fctr + 8 * (r & 1);
-        scan_frontier_body<D, kFPerSmall, false, true>(0, n, offsets, dist, prev, queue, c, nullptr);
-        gg.sync();
-        if (__ldcg(c) == 0) break;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            acc[0] += 1;
-            acc[1] += __ldcg(c + 3);
-            acc[2] += __ldcg(c + 4);
-            unsigned long long* o = fctr + 8 * ((r + 1) & 1);  // last read a round ago
-            for (int i = 0; i < 8; ++i) o[i] = 0;
-        }
-        relax_body<D, 16, false, kShardChunk, true>(queue, c, offsets, dests, weights, dist,
-                                                    acc + 3, SsspDelta{}, upd);
-        gg.sync();
-        if (__ldcg(acc + 3)) break;  // a narrow-width overflow: the call reruns wider
-    }
-}
 
 // The round's relaxations: the <= 64-edge items (LPI lanes each) and, with the
 // split queue, the small vertices' one items (2 lanes, <= kSmallDeg edges).
@@ -848,7 +781,7 @@ static cudaGraphExec_t build_sssp_graph(gdx_graph* g, D* dist, D* prev, unsigned
 // when 32-bit distances overflowed.
 template <class D>
 static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* stats,
-                          bool use_graph = false, bool fused = false) {
+                          bool use_graph = false) {
     auto& w = *g->sssp;
     cudaStream_t s = g->stream;
     const int32_t n = g->n;
@@ -857,7 +790,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     const D inf = sizeof(D) < 8 ? std::numeric_limits<D>::max() : D(INT64_MAX / 2);
     const size_t items_cap = size_t(n) + size_t(g->m) / kShardChunk + 1;
     w.shard_queue.ensure(items_cap);
-    w.shard_ctr.ensure(16);  // fused: two sets of 8 round counters
+    w.shard_ctr.ensure(kSmallCtr + 1);
     w.upd_slots.ensure(kUpdSlots);
     unsigned long long* ctr = w.shard_ctr.get();
     // large graphs: small vertices in their own queue (one more launch per
@@ -874,8 +807,8 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     unsigned long long* ovf_flag = use_graph ? w.graph_acc.get() + 3 : ovf.get();
     timed_launch(g, "sssp_init", [&] {
         k_sssp_scan_init<D><<<blocks_for(n, 256, g->num_sms * 8), 256, 0, s>>>(
-            n, src, inf, dist, prev, ctr, fused ? 16 : kSmallCtr + 1,
-            use_graph ? w.graph_acc.get() : ovf.get(), use_graph ? 4 : 1, w.upd_slots.get());
+            n, src, inf, dist, prev, ctr, kSmallCtr + 1, use_graph ? w.graph_acc.get() : ovf.get(),
+            use_graph ? 4 : 1, w.upd_slots.get());
     });
     unsigned long long* h = reinterpret_cast<unsigned long long*>(g->pinned);
     unsigned long long vvis = 0, evis = 0;
@@ -892,25 +825,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
     prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, 16>), kRelaxCarveout);
     prefer_l1(reinterpret_cast<const void*>(&k_sssp_scan_relax<D, kSmallLpi, false, kSmallDeg>),
               kRelaxCarveout);
-    if (fused) {
-        static int per_sm = -1;  // co-resident 256-thread blocks of the fused kernel
-        if (per_sm < 0)
-            GDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sssp_fused<D>, 256, 0));
-        const char* fb = std::getenv("GDX_SSSP_FUSED_BLOCKS");  // blocks per SM (A/B)
-        const int grid = std::max(1, std::min(per_sm, fb ? std::atoi(fb) : 8)) * g->num_sms;
-        const int32_t* wts = g->weighted ? g->weights.get() : nullptr;
-        const int32_t* offs = g->offsets.get();
-        const int32_t* dsts = g->dests.get();
-        int2* queue = w.shard_queue.get();
-        unsigned long long* acc = w.graph_acc.get();
-        unsigned long long* upd = w.upd_slots.get();
-        int32_t nn = n;
-        void* args[] = {&nn, &offs, &dsts, &wts, &dist, &prev, &queue, &ctr, &acc, &upd};
-        timed_launch(g, "sssp_graph", [&] {
-            GDX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sssp_fused<D>),
-                                                 grid, 256, args, 0, s));
-        });
-    } else if (use_graph) {
+    if (use_graph) {
         const int di = sizeof(D) == 2 ? 2 : sizeof(D) == 4 ? 0 : 1;
         // the instantiated graph bakes in these buffers and the CSR arrays
         // (gdx_graph_set_hash_weights reallocates / enables the weights)
@@ -972,7 +887,7 @@ static bool run_sssp_scan(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stat
         rounds = int(h[0]);
         vvis = h[1];
         evis = h[2];
-        launches += fused ? 1 : (split ? 4 : 3) * (rounds + 1);
+        launches += (split ? 4 : 3) * (rounds + 1);
     }
     if (stats) {
         stats->rounds = rounds;
@@ -1162,15 +1077,9 @@ static void sssp_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
     // of small rounds) take the persistent kernel instead: its queue touches
     // only the frontier while a scan reads all n per round (2000^2 grid:
     // 27 ms vs 76 ms).
-    // Small graphs (CSR L2-resident, ~25 us rounds) run the round loop as one
-    // cooperative kernel (k_sssp_fused: same-box C1 kernel 0.254 -> 0.238 ms).
     const char* mode = std::getenv("GDX_SSSP_MODE");
-    const bool small = g->n < kSmallScan && g->m < (int64_t(1) << 26);
-    const std::string md = mode ? mode
-                         : graph_max_degree(g) <= 64 ? "persistent"
-                         : small ? "fused" : "graph";
-    const bool fused = md == "fused";
-    const bool graph = md == "graph" || fused;
+    const std::string md = mode ? mode : graph_max_degree(g) <= 64 ? "persistent" : "graph";
+    const bool graph = md == "graph";
     const bool scan = md == "scan" || graph;
     if (scan) {
         w.prev.ensure(size_t(g->n));
@@ -1184,11 +1093,11 @@ static void sssp_run(gdx_graph* g, int32_t src, int64_t* dist_out, gdx_stats* st
                                             : (g->n >= (1 << 22) && !w.narrow_overflowed);
         bool ovf = true;
         if (narrow) {
-            ovf = run_sssp_scan<unsigned short>(g, src, dist_out, stats, graph, fused);
+            ovf = run_sssp_scan<unsigned short>(g, src, dist_out, stats, graph);
             if (ovf) w.narrow_overflowed = true;
         }
-        if (ovf && run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph, fused))
-            run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph, fused);
+        if (ovf && run_sssp_scan<unsigned int>(g, src, dist_out, stats, graph))
+            run_sssp_scan<unsigned long long>(g, src, dist_out, stats, graph);
     } else {
         // the persistent kernel's queues exist only in this mode (C5 in the
         // default graph mode would otherwise hold 2 x ~2 GB of unused items);

@@ -172,8 +172,7 @@ def test_sssp_c1_bit_exact(gdx, port):
             assert st["rounds"] >= 2 and st["edges_visited"] >= g.m * 0.5
 
 
-@pytest.mark.parametrize("mode", ["persistent", "scan", "graph", "fused", "scan_split",
-                                  "graph_split"])
+@pytest.mark.parametrize("mode", ["persistent", "scan", "graph", "scan_split", "graph_split"])
 def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
     """Both SSSP executions (persistent cooperative kernel for small graphs,
     frontier-scan rounds for large ones) are bit-exact on config 1; *_split:
@@ -187,7 +186,7 @@ def test_sssp_modes_c1(gdx, port, mode, monkeypatch):
         assert np.array_equal(dg.sssp(src), port.sssp(g, src)), src
 
 
-@pytest.mark.parametrize("mode", ["persistent", "scan", "graph", "fused"])
+@pytest.mark.parametrize("mode", ["persistent", "scan", "graph"])
 def test_sssp_64bit_distances(gdx, port, mode, monkeypatch):
     monkeypatch.setenv("GDX_SSSP_MODE", mode)
     u, v = port.gen_rmat_edges(5000, 40000, 8)
@@ -209,7 +208,7 @@ def test_sssp_16bit_first_attempt(gdx, port, weights, monkeypatch):
     g = port.build_from_edges(100 * 100, gu, gv, None, False)
     g.weights = np.random.default_rng(3).integers(*weights, size=g.m).astype(np.int32)
     dg = gdx.DeviceGraph.from_csr(g)
-    for mode in ("graph", "scan", "fused"):
+    for mode in ("graph", "scan"):
         monkeypatch.setenv("GDX_SSSP_MODE", mode)
         for src in (0, 5050, 0):
             exp = port.sssp(g, src)
